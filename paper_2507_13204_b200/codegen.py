@@ -1,0 +1,451 @@
+"""Program tree -> CUDA C++ for the statement-granular execution path.
+
+One module per function: a grid-stride kernel per ``parallel_for``
+(reference: _Compiler / _Interpreter.parallel_for,
+/root/reference/pkg/src/krn/runtime.py:230-447, 567-624) and a one-thread kernel
+per run of function-scope element statements (runtime.py:536-550).  The text
+is compiled by NVRTC for sm_100a with ``--fmad=false``; it includes the
+library's hand-written prelude (csrc/krn_prelude.cuh) for the accumulation
+policies.
+
+Semantics carried over from the interpreter, with the reference line:
+
+* every access is bounds checked (runtime.py:299-321): the first failure is
+  recorded in the context's status word and the iteration stops there
+* a view value used as an index truncates toward zero (runtime.py:335)
+* value expressions keep the tree's evaluation order; literals are emitted as
+  hexadecimal floats so no decimal rounding can creep in
+* ``atomic_add`` inside a kernel is deferred to the kernel boundary and applied
+  in (iteration, program order) (runtime.py:430-447, 615-620).  Two policies,
+  chosen per target view by ``plan_atomics``:
+
+  - *gather* (targets of the form ``v(i + c [, const])``): the kernel stores
+    each site's contribution into a staging column; a second generated kernel
+    walks the *target locations* and adds the contributions that land there in
+    exactly the reference's order.  Conflict-free, no atomics, bit-identical to
+    the interpreter, and reads inside the kernel see pre-kernel values as the
+    deferred semantics demand.
+  - *atomic* (indirect or otherwise non-injective targets): hardware fp64
+    reductions, warp-aggregated; the sum is exact up to reassociation (the
+    1e-12 relative tolerance of the parity contract).  If the kernel also reads
+    or plainly writes the target view the contributions are staged and applied
+    by a second kernel so that the deferral is still honoured.
+"""
+
+from __future__ import annotations
+
+import dataclasses as _dc
+
+from .lang.dataflow import normalize_index
+from .lang.nodes import kind, walk_expr, walk_statements
+
+_ELEMENT = ("DeclScalar", "AssignScalar", "AssignView", "AtomicAdd", "If")
+
+
+def c_double(v: float) -> str:
+    v = float(v)
+    if v != v or v in (float("inf"), float("-inf")):
+        raise ValueError("non-finite literal")
+    return "(" + v.hex() + ")"
+
+
+# ---------------------------------------------------------------------------
+# atomic scheduling
+
+
+@_dc.dataclass
+class Site:
+    """One atomic_add statement of a kernel."""
+
+    index: int  # program order among the kernel's sites
+    stmt: object
+    guards: tuple  # enclosing If conditions, outermost first
+    view: str
+    offset: object = None  # int c when the row index is `counter + c`
+    column: object = None  # int or None (rank-1)
+    mode: str = "atomic"  # "gather" | "atomic" | "staged_atomic"
+
+
+def _unit_affine(idx, counter):
+    """``counter + c`` with literal c -> c, else None."""
+    try:
+        const, terms = normalize_index(idx)
+    except (TypeError, ValueError):
+        return None
+    if terms == ((("counter", counter), 1),):
+        return const
+    return None
+
+
+def _constant(idx):
+    try:
+        const, terms = normalize_index(idx)
+    except (TypeError, ValueError):
+        return None
+    return const if not terms else None
+
+
+def plan_atomics(loop) -> list:
+    """Sites of a kernel with their accumulation policy."""
+    sites: list = []
+
+    def collect(body, guards):
+        for s in body:
+            if kind(s) == "AtomicAdd":
+                sites.append(Site(len(sites), s, guards, s.target.view))
+            elif kind(s) == "If":
+                collect(s.body, guards + (s.cond,))
+
+    collect(loop.body, ())
+    if not sites:
+        return sites
+
+    touched_plainly = set()  # views read or plainly written by the kernel
+    for s in walk_statements(loop.body):
+        k = kind(s)
+        exprs = []
+        if k == "AssignView":
+            touched_plainly.add(s.target.view)
+            exprs = list(s.target.indices) + [s.rhs]
+        elif k == "AtomicAdd":
+            exprs = list(s.target.indices) + [s.value]
+        elif k == "DeclScalar":
+            exprs = [s.init]
+        elif k == "AssignScalar":
+            exprs = [s.rhs]
+        for e in exprs:
+            for n in walk_expr(e):
+                if kind(n) == "ViewAccess":
+                    touched_plainly.add(n.view)
+
+    by_view: dict = {}
+    for st in sites:
+        by_view.setdefault(st.view, []).append(st)
+    for view, group in by_view.items():
+        gather = True
+        for st in group:
+            idx = st.stmt.target.indices
+            st.offset = _unit_affine(idx[0], loop.counter)
+            st.column = _constant(idx[1]) if len(idx) == 2 else None
+            if st.offset is None or (len(idx) == 2 and st.column is None):
+                gather = False
+        for st in group:
+            if gather:
+                st.mode = "gather"
+            else:
+                st.mode = "staged_atomic" if view in touched_plainly else "atomic"
+    return sites
+
+
+# ---------------------------------------------------------------------------
+# module generation
+
+_PREAMBLE = r"""
+#include "krn_prelude.cuh"
+#define NV %(nv)d
+struct Env {
+    double *v[NV > 0 ? NV : 1];
+    krn_i64 e0[NV > 0 ? NV : 1];
+    krn_i64 e1[NV > 0 ? NV : 1];
+    double *S;
+    krn_i64 *status;
+};
+// bounds-checked linear offsets; on failure record {code,line,view,i,j} and flag the iteration
+__device__ __forceinline__ krn_i64 off1(const Env &E, int v, krn_i64 i, int line, bool &bad)
+{
+    if (i < 0 || i >= E.e0[v]) {
+        if (!bad) krn_fail(E.status, 1, line, v, i, 0);
+        bad = true;
+        return 0;
+    }
+    return i;
+}
+__device__ __forceinline__ krn_i64 off2(const Env &E, int v, krn_i64 i, krn_i64 j, int line, bool &bad)
+{
+    if (i < 0 || i >= E.e0[v] || j < 0 || j >= E.e1[v]) {
+        if (!bad) krn_fail(E.status, 1, line, v, i, j);
+        bad = true;
+        return 0;
+    }
+    return i * E.e1[v] + j;
+}
+__device__ __forceinline__ double rd(const Env &E, int v, krn_i64 off, bool bad)
+{
+    return bad ? 0.0 : E.v[v][off];
+}
+// int(value): truncation toward zero; NaN/Inf cannot be converted
+__device__ __forceinline__ krn_i64 to_index(const Env &E, double x, int line, int v, bool &bad)
+{
+    if (bad) return 0;
+    if (!(x == x) || x - x != 0.0) {
+        krn_fail(E.status, 2, line, v, x == x ? 1 : 0, 0);
+        bad = true;
+        return 0;
+    }
+    if (x >= 4.0e18) return 4000000000000000000ll;
+    if (x <= -4.0e18) return -4000000000000000000ll;
+    return (krn_i64)x;
+}
+"""
+
+
+class ModuleBuilder:
+    """Generates the CUDA source of one function and the launch recipes the
+    executor needs (kernel names, staging requirements)."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        self.views: list = []  # view table: name -> index
+        self.rank: dict = {}
+        self.slots: dict = {}  # function-scope scalar -> slot in S
+        self.parts: list = []
+        self.kernels: dict = {}  # id(stmt) -> recipe
+        for p in fn.params:
+            if p.is_view:
+                self._add_view(p.name, p.type.rank)
+            else:
+                self.slot(p.name)
+        for s in walk_statements(fn.body):
+            if kind(s) == "DeclView":
+                self._add_view(s.name, s.descriptor.rank)
+
+    def _add_view(self, name, rank):
+        if name not in self.rank:
+            self.views.append(name)
+            self.rank[name] = rank
+
+    def vid(self, name) -> int:
+        return self.views.index(name)
+
+    def slot(self, name) -> int:
+        if name not in self.slots:
+            self.slots[name] = len(self.slots)
+        return self.slots[name]
+
+    # ---- expressions -----------------------------------------------------------
+
+    def index(self, e, local) -> str:
+        k = kind(e)
+        if k == "IntLiteral":
+            return f"((krn_i64){e.value}ll)" if e.value >= 0 else f"((krn_i64)({e.value}ll))"
+        if k == "Counter":
+            return "i"
+        if k == "Extent":
+            return f"E.e{e.dim}[{self.vid(e.view)}]"
+        if k == "ViewAccess":
+            line = getattr(e.span, "line", 0)
+            return f"to_index(E, {self.load(e, local)}, {line}, {self.vid(e.view)}, bad)"
+        if k == "IdxBinary":
+            return f"({self.index(e.lhs, local)} {e.op} {self.index(e.rhs, local)})"
+        raise TypeError(f"cannot generate index {k}")
+
+    def offset(self, acc, local) -> str:
+        v = self.vid(acc.view)
+        line = getattr(acc.span, "line", 0)
+        idx = [self.index(i, local) for i in acc.indices]
+        if len(idx) == 1:
+            return f"off1(E, {v}, {idx[0]}, {line}, bad)"
+        return f"off2(E, {v}, {idx[0]}, {idx[1]}, {line}, bad)"
+
+    def load(self, acc, local) -> str:
+        # the offset expression may set `bad`; rd() then yields 0.0 without touching memory
+        return f"krn_seq_rd(E, {self.vid(acc.view)}, {self.offset(acc, local)}, bad)"
+
+    def value(self, e, local) -> str:
+        k = kind(e)
+        if k == "Literal":
+            return c_double(e.value)
+        if k == "ScalarVar":
+            if e.name in local:
+                return f"L_{e.name}"
+            return f"E.S[{self.slot(e.name)}]"
+        if k == "IndexVar":
+            return "((double)i)"
+        if k == "ViewAccess":
+            return self.load(e, local)
+        if k == "Extent":
+            return f"((double)E.e{e.dim}[{self.vid(e.view)}])"
+        if k == "Neg":
+            return f"(-{self.value(e.operand, local)})"
+        if k == "Binary":
+            # C++ leaves operand evaluation order unspecified; only `bad` bookkeeping is
+            # order-sensitive and it is idempotent, the arithmetic itself is a tree
+            return f"({self.value(e.lhs, local)} {e.op} {self.value(e.rhs, local)})"
+        raise TypeError(f"cannot generate value {k}")
+
+    def compare(self, c, local) -> str:
+        return f"({self.index(c.lhs, local)} {c.op} {self.index(c.rhs, local)})"
+
+    # ---- statements ----------------------------------------------------------------
+
+    def element(self, s, local: set, out: list, pad: str, sites: dict, in_kernel: bool):
+        """One element statement; `local` = names living in C++ locals."""
+        k = kind(s)
+        stop = "continue;" if in_kernel else "return;"
+        if k == "DeclScalar":
+            if in_kernel:
+                local.add(s.name)
+                out.append(f"{pad}double L_{s.name} = {self.value(s.init, local)};")
+            else:
+                out.append(f"{pad}{{ double t_ = {self.value(s.init, local)}; if (bad) {stop} "
+                           f"E.S[{self.slot(s.name)}] = t_; }}")
+                return
+            out.append(f"{pad}if (bad) {stop}")
+        elif k == "AssignScalar":
+            tgt = f"L_{s.name}" if s.name in local else f"E.S[{self.slot(s.name)}]"
+            rhs = self.value(s.rhs, local)
+            expr = {"=": "t_", "+=": f"{tgt} + t_", "-=": f"{tgt} - t_"}[s.op]
+            out.append(f"{pad}{{ double t_ = {rhs}; if (bad) {stop} {tgt} = {expr}; }}")
+        elif k == "AssignView":
+            v = self.vid(s.target.view)
+            expr = {"=": "t_", "+=": f"E.v[{v}][o_] + t_", "-=": f"E.v[{v}][o_] - t_"}[s.op]
+            out.append(
+                f"{pad}{{ krn_i64 o_ = {self.offset(s.target, local)}; if (bad) {stop} "
+                f"double t_ = {self.value(s.rhs, local)}; if (bad) {stop} E.v[{v}][o_] = {expr}; }}"
+            )
+        elif k == "AtomicAdd":
+            v = self.vid(s.target.view)
+            head = (f"{pad}{{ krn_i64 o_ = {self.offset(s.target, local)}; if (bad) {stop} "
+                    f"double t_ = {self.value(s.value, local)}; if (bad) {stop} ")
+            site = sites.get(id(s)) if sites else None
+            if site is None:  # function scope: applies immediately (runtime.py:441-442)
+                out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
+            elif site.mode == "gather":
+                out.append(head + f"stage[{site.index} * n + i] = t_; }}")
+            elif site.mode == "staged_atomic":
+                out.append(head + f"stage[{site.index} * n + i] = t_; "
+                                  f"ostage[{site.index} * n + i] = o_; }}")
+            else:
+                out.append(head + f"krn_red_add(&E.v[{v}][o_], t_); }}")
+        elif k == "If":
+            out.append(f"{pad}if {self.compare(s.cond, local)} {{")
+            for inner in s.body:
+                self.element(inner, local, out, pad + "    ", sites, in_kernel)
+            out.append(f"{pad}}}")
+        else:
+            raise TypeError(f"statement not allowed here: {k}")
+
+    def kernel(self, loop, name: str) -> dict:
+        sites = plan_atomics(loop)
+        by_id = {id(st.stmt): st for st in sites}
+        staged = [st for st in sites if st.mode in ("gather", "staged_atomic")]
+        needs_offsets = any(st.mode == "staged_atomic" for st in sites)
+        body: list = []
+        local = {loop.counter}
+        for s in loop.body:
+            self.element(s, local, body, "        ", by_id, True)
+        src = [
+            f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, double *stage, '
+            "krn_i64 *ostage)",
+            "{",
+            "    for (krn_i64 i = blockIdx.x * (krn_i64)blockDim.x + threadIdx.x; i < n; "
+            "i += (krn_i64)gridDim.x * blockDim.x) {",
+            "        bool bad = false;",
+        ]
+        if staged:
+            # a site that does not execute (guard false) must not contribute: mark with the
+            # offsets column when present, else re-evaluate guards in the apply kernel
+            for st in staged:
+                if st.mode == "staged_atomic":
+                    src.append(f"        ostage[{st.index} * n + i] = -1;")
+        src += body + ["    }", "}"]
+        self.parts.append("\n".join(src))
+        recipe = dict(name=name, sites=sites, n_staged=len(sites) if staged else 0,
+                      needs_offsets=needs_offsets, apply=[])
+        # apply kernels
+        gather_views: dict = {}
+        for st in sites:
+            if st.mode == "gather":
+                gather_views.setdefault(st.view, []).append(st)
+        for view, group in gather_views.items():
+            recipe["apply"].append(self._gather_apply(loop, view, group, f"{name}_g{self.vid(view)}"))
+        if needs_offsets:
+            recipe["apply"].append(self._staged_apply(sites, f"{name}_a"))
+        return recipe
+
+    def _gather_apply(self, loop, view, group, name) -> dict:
+        """Kernel over the rows k of `view`: adds, in (iteration, program order),
+        the staged contributions whose target is row k."""
+        v = self.vid(view)
+        rank2 = self.rank[view] == 2
+        # iteration of site s for row k is k - c_s: ascending iteration = descending c_s
+        order = sorted(group, key=lambda st: (-st.offset, st.index))
+        lines = [
+            f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, '
+            "const double *stage, const krn_i64 *ostage)",
+            "{",
+            f"    const krn_i64 rows = E.e0[{v}];",
+            "    for (krn_i64 k = blockIdx.x * (krn_i64)blockDim.x + threadIdx.x; k < rows; "
+            "k += (krn_i64)gridDim.x * blockDim.x) {",
+        ]
+        columns = sorted({st.column for st in group}) if rank2 else [None]
+        for col in columns:
+            if rank2:
+                lines.append(f"        if ({col} >= 0 && {col} < E.e1[{v}]) {{")
+                lines.append(f"            double acc = E.v[{v}][k * E.e1[{v}] + {col}];")
+            else:
+                lines.append("        {")
+                lines.append(f"            double acc = E.v[{v}][k];")
+            for st in order:
+                if rank2 and st.column != col:
+                    continue
+                guard = " && ".join(
+                    ["i >= 0", "i < n"] + [self.compare(g, {loop.counter}) for g in st.guards]
+                )
+                lines.append(f"            {{ const krn_i64 i = k - ({st.offset}); bool bad = false; (void)bad; "
+                             f"if ({guard}) acc = acc + stage[{st.index} * n + i]; }}")
+            if rank2:
+                lines.append(f"            E.v[{v}][k * E.e1[{v}] + {col}] = acc;")
+            else:
+                lines.append(f"            E.v[{v}][k] = acc;")
+            lines.append("        }")
+        lines += ["    }", "}"]
+        self.parts.append("\n".join(lines))
+        return dict(name=name, over="rows", view=view)
+
+    def _staged_apply(self, sites, name) -> dict:
+        lines = [
+            f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, '
+            "const double *stage, const krn_i64 *ostage)",
+            "{",
+            "    for (krn_i64 i = blockIdx.x * (krn_i64)blockDim.x + threadIdx.x; i < n; "
+            "i += (krn_i64)gridDim.x * blockDim.x) {",
+        ]
+        for st in sites:
+            if st.mode == "staged_atomic":
+                v = self.vid(st.view)
+                lines.append(f"        {{ krn_i64 o = ostage[{st.index} * n + i]; "
+                             f"if (o >= 0) krn_red_add(&E.v[{v}][o], stage[{st.index} * n + i]); }}")
+        lines += ["    }", "}"]
+        self.parts.append("\n".join(lines))
+        return dict(name=name, over="iterations", view=None)
+
+    def scalar_block(self, stmts, name: str) -> dict:
+        """One-thread kernel for a run of function-scope element statements."""
+        body: list = []
+        for s in stmts:
+            self.element(s, set(), body, "    ", None, False)
+        src = [f'extern "C" __global__ void {name}(Env E)', "{", "    bool bad = false;"] + body + ["}"]
+        self.parts.append("\n".join(src))
+        return dict(name=name)
+
+    def return_block(self, expr, name: str) -> dict:
+        slot = self.slot("__return__")
+        src = [
+            f'extern "C" __global__ void {name}(Env E)',
+            "{",
+            "    bool bad = false;",
+            f"    double t_ = {self.value(expr, set())};",
+            f"    if (!bad) E.S[{slot}] = t_;",
+            "}",
+        ]
+        self.parts.append("\n".join(src))
+        return dict(name=name, slot=slot)
+
+    def source(self) -> str:
+        head = _PREAMBLE % dict(nv=len(self.views))
+        head += (
+            "__device__ __forceinline__ double krn_seq_rd(const Env &E, int v, krn_i64 off, bool &bad)\n"
+            "{ return rd(E, v, off, bad); }\n"
+        )
+        return head + "\n\n" + "\n\n".join(self.parts) + "\n"

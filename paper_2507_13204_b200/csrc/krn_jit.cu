@@ -1,0 +1,172 @@
+// Loader for kernels generated from program trees: NVRTC -> cubin -> driver
+// launch.  libnvrtc and libcuda are opened lazily with dlopen so the library
+// itself loads (and exports its symbols) on a machine without a GPU driver.
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "krn_common.cuh"
+
+static const char kPreludeSource[] = {
+#include "krn_prelude_embed.inc"
+    , 0};
+
+struct krn_module {
+    CUmodule module = nullptr;
+    std::map<std::string, CUfunction> functions;
+};
+
+namespace {
+
+struct Api {
+    bool tried = false, ok = false;
+    // nvrtc
+    nvrtcResult (*CreateProgram)(nvrtcProgram *, const char *, const char *, int, const char *const *,
+                                 const char *const *) = nullptr;
+    nvrtcResult (*CompileProgram)(nvrtcProgram, int, const char *const *) = nullptr;
+    nvrtcResult (*GetProgramLogSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetProgramLog)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetCUBIN)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*DestroyProgram)(nvrtcProgram *) = nullptr;
+    // driver
+    CUresult (*ModuleLoadData)(CUmodule *, const void *) = nullptr;
+    CUresult (*ModuleUnload)(CUmodule) = nullptr;
+    CUresult (*ModuleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
+    CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                             CUstream, void **, void **) = nullptr;
+    CUresult (*GetErrorString)(CUresult, const char **) = nullptr;
+} api;
+
+void *open_first(const std::vector<const char *> &names)
+{
+    for (const char *n : names) {
+        if (void *h = dlopen(n, RTLD_NOW | RTLD_GLOBAL)) return h;
+    }
+    return nullptr;
+}
+
+int load_api()
+{
+    if (api.tried) {
+        if (!api.ok) krn_set_error("libnvrtc / libcuda unavailable (earlier load failed)");
+        return api.ok ? KRN_OK : KRN_E_UNAVAILABLE;
+    }
+    api.tried = true;
+    void *rtc = open_first({"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                            "/usr/local/cuda/lib64/libnvrtc.so"});
+    void *drv = open_first({"libcuda.so.1", "libcuda.so"});
+    if (!rtc || !drv) {
+        krn_set_error("cannot load %s: %s", !rtc ? "libnvrtc" : "libcuda", dlerror());
+        return KRN_E_UNAVAILABLE;
+    }
+#define KRN_SYM(handle, field, name)                                        \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(handle, name)); \
+    if (!api.field) {                                                       \
+        krn_set_error("symbol %s not found", name);                         \
+        return KRN_E_UNAVAILABLE;                                           \
+    }
+    KRN_SYM(rtc, CreateProgram, "nvrtcCreateProgram")
+    KRN_SYM(rtc, CompileProgram, "nvrtcCompileProgram")
+    KRN_SYM(rtc, GetProgramLogSize, "nvrtcGetProgramLogSize")
+    KRN_SYM(rtc, GetProgramLog, "nvrtcGetProgramLog")
+    KRN_SYM(rtc, GetCUBINSize, "nvrtcGetCUBINSize")
+    KRN_SYM(rtc, GetCUBIN, "nvrtcGetCUBIN")
+    KRN_SYM(rtc, DestroyProgram, "nvrtcDestroyProgram")
+    KRN_SYM(drv, ModuleLoadData, "cuModuleLoadData")
+    KRN_SYM(drv, ModuleUnload, "cuModuleUnload")
+    KRN_SYM(drv, ModuleGetFunction, "cuModuleGetFunction")
+    KRN_SYM(drv, LaunchKernel, "cuLaunchKernel")
+    KRN_SYM(drv, GetErrorString, "cuGetErrorString")
+#undef KRN_SYM
+    api.ok = true;
+    return KRN_OK;
+}
+
+int driver_fail(const char *what, CUresult r)
+{
+    const char *msg = "unknown";
+    api.GetErrorString(r, &msg);
+    krn_set_error("%s failed: %s", what, msg ? msg : "unknown");
+    return KRN_E_CUDA;
+}
+
+}  // namespace
+
+extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_module **out)
+{
+    KRN_REQUIRE(ctx && cuda_source && out, "null argument");
+    *out = nullptr;
+    int rc = load_api();
+    if (rc) return rc;
+    KRN_CUDA(cudaSetDevice(ctx->device));
+    KRN_CUDA(cudaFree(nullptr));  // make sure the primary context exists
+
+    nvrtcProgram prog;
+    const char *headers[] = {kPreludeSource};
+    const char *names[] = {"krn_prelude.cuh"};
+    if (api.CreateProgram(&prog, cuda_source, "krn_generated.cu", 1, headers, names) != NVRTC_SUCCESS) {
+        krn_set_error("nvrtcCreateProgram failed");
+        return KRN_E_NVRTC;
+    }
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
+                          "--prec-div=true", "--prec-sqrt=true", "--ftz=false"};
+    nvrtcResult cr = api.CompileProgram(prog, int(sizeof(opts) / sizeof(opts[0])), opts);
+    if (cr != NVRTC_SUCCESS) {
+        size_t n = 0;
+        api.GetProgramLogSize(prog, &n);
+        std::string log(n, '\0');
+        if (n) api.GetProgramLog(prog, &log[0]);
+        krn_set_error("NVRTC compilation failed:\n%s", log.c_str());
+        api.DestroyProgram(&prog);
+        return KRN_E_NVRTC;
+    }
+    size_t size = 0;
+    api.GetCUBINSize(prog, &size);
+    std::vector<char> cubin(size);
+    api.GetCUBIN(prog, cubin.data());
+    api.DestroyProgram(&prog);
+
+    krn_module *m = new krn_module();
+    CUresult r = api.ModuleLoadData(&m->module, cubin.data());
+    if (r != CUDA_SUCCESS) {
+        delete m;
+        return driver_fail("cuModuleLoadData", r);
+    }
+    *out = m;
+    return KRN_OK;
+}
+
+extern "C" int krn_module_destroy(krn_module *m)
+{
+    if (m == nullptr) return KRN_OK;
+    if (m->module && api.ok) api.ModuleUnload(m->module);
+    delete m;
+    return KRN_OK;
+}
+
+extern "C" int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, size_t n_iterations,
+                                 void **args)
+{
+    KRN_REQUIRE(ctx && m && name, "null argument");
+    auto it = m->functions.find(name);
+    if (it == m->functions.end()) {
+        CUfunction f;
+        CUresult r = api.ModuleGetFunction(&f, m->module, name);
+        if (r != CUDA_SUCCESS) return driver_fail("cuModuleGetFunction", r);
+        it = m->functions.emplace(name, f).first;
+    }
+    if (n_iterations == 0) return KRN_OK;
+    const unsigned block = 256;
+    size_t want = (n_iterations + block - 1) / block;
+    size_t cap = size_t(ctx->sms) * 32;  // grid-stride loops inside; whole multiples of the SM count
+    unsigned grid = unsigned(want < cap ? want : cap);
+    CUresult r = api.LaunchKernel(it->second, grid, 1, 1, block, 1, 1, 0, ctx->stream, args, nullptr);
+    if (r != CUDA_SUCCESS) return driver_fail("cuLaunchKernel", r);
+    ctx->launches++;
+    return KRN_OK;
+}

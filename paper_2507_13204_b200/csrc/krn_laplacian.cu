@@ -1,0 +1,396 @@
+// Fused kernels for the headline objective normRes1DLaplacianSQ and its
+// generated gradient: one launch each, every compulsory byte moved once.
+//
+//   primal   reads x, b (16 B/row), writes 3x (8 B/row)                = 24 B/row
+//   gradient reads x, b [, _d_x, _d_b], writes 3x, _d_x, _d_b   = 40 or 56 B/row
+//
+// What is computed is the execution of the reference's statement sequence
+// (forward: programs/laplacian.krn:4-21; reverse: the emitted text frozen in
+// reference tests/test_adjoint.py:43-94) with the same IEEE operations in the
+// same order per output element:
+//
+//   xs_j  = 3.0 * x_j
+//   y_j   = ((2.0*xs_j - b_j) - [j!=0] xs_{j-1}) - [j!=n-1] xs_{j+1}
+//   f     = tree_j(y_j * y_j)                      (reference pairwise tree)
+//   r4    = 0.0 + (0.0 + seed)                     (_d_sum, then _d_y2 broadcast)
+//   dy_j  = (0.0 + r4*y_j) + y_j*r4
+//   [j!=n-1]  r3 = dy; dy = (dy - r3) + r3         -> -r3 to _d_x(j+1)
+//   [j!=0]    r2 = dy; dy = (dy - r2) + r2         -> -r2 to _d_x(j-1)
+//   r1 = dy                                        -> 2.0*r1 to _d_x(j), -r1 to _d_b(j)
+//
+// The reference queues the three _d_x contributions as atomic adds and applies
+// them after the kernel sorted by (iteration, program order)
+// (runtime.py:615-620).  Location k therefore receives, in this order,
+// -r3_{k-1}, 2.0*r1_k, -r2_{k+1}.  Here every thread *gathers* those three
+// terms for its own k in exactly that order: no atomics, no conflicts, and the
+// result is bit-identical to the interpreter.  The reverse of the scale kernel
+// is folded in: r0 = acc; _d_x_k = (acc - r0) + 3.0*r0.
+//
+// Work decomposition: a block owns an aligned chunk of 1024*R rows, warp w the
+// aligned sub-chunk of 128*R rows, processed as R steps of 128 rows (4 per lane,
+// one LDG.E.256 per operand).  Neighbour values travel by warp shuffle; the two
+// edge lanes fetch the ghost rows of the neighbouring warp themselves (L2 hits).
+// Interior steps need no guard at all; the (at most three) steps per shard that
+// touch row 0, row n-1, a shard boundary or the ragged tail take a scalar,
+// fully guarded path.
+#include "krn_common.cuh"
+#include "krn_prelude.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kStep = 128;  // rows per warp step
+
+struct Shard {
+    const double *x;     // original x, local rows
+    const double *b;
+    const double *halo;  // x[-2], x[-1], b[-1], x[n], x[n+1], b[n] (local indexing) or null
+    krn_i64 n_local;
+    krn_i64 offset;
+    krn_i64 n_global;
+};
+
+// original x / b at local row i in [-2, n_local + 2); caller guarantees the global row exists
+__device__ __forceinline__ double x_at(const Shard &s, krn_i64 i)
+{
+    if (i < 0) return s.halo[2 + i];
+    if (i >= s.n_local) return s.halo[3 + (i - s.n_local)];
+    return krn_ld1(s.x + i);
+}
+__device__ __forceinline__ double b_at(const Shard &s, krn_i64 i)
+{
+    if (i < 0) return s.halo[2];
+    if (i >= s.n_local) return s.halo[5];
+    return krn_ld1(s.b + i);
+}
+
+struct Chain {
+    double r3, r2, r1;
+};
+
+// reverse of the stencil kernel for one row, statement by statement
+__device__ __forceinline__ Chain adjoint_chain(double y, double r4, bool has_up, bool has_down)
+{
+    Chain c;
+    double dy = 0.0 + r4 * y;   // _d_y(j) += _r_d4 * y(j)   (shadow starts at +0.0)
+    dy = dy + y * r4;           // _d_y(j) += y(j) * _r_d4
+    c.r3 = 0.0;
+    c.r2 = 0.0;
+    if (has_up) {               // if (j != extent - 1)
+        c.r3 = dy;
+        dy = dy - c.r3;
+        dy = dy + c.r3;
+    }
+    if (has_down) {             // if (j != 0)
+        c.r2 = dy;
+        dy = dy - c.r2;
+        dy = dy + c.r2;
+    }
+    c.r1 = dy;
+    return c;
+}
+
+__device__ __forceinline__ double stencil_row(double xm, double xc, double xp, double b, bool has_down,
+                                              bool has_up)
+{
+    double y = 2.0 * xc - b;
+    if (has_down) y = y - xm;
+    if (has_up) y = y - xp;
+    return y;
+}
+
+// _d_x(k): gather of the queued contributions in the reference's order, then the
+// reverse of the scale kernel
+__device__ __forceinline__ double finish_dx(double dx_in, double r3_left, double r1, double r2_right,
+                                            bool has_left, bool has_right)
+{
+    double acc = dx_in;
+    if (has_left) acc = acc + (-r3_left);
+    acc = acc + 2.0 * r1;
+    if (has_right) acc = acc + (-r2_right);
+    double r0 = acc;
+    acc = acc - r0;
+    acc = acc + 3.0 * r0;
+    return acc;
+}
+
+// ---- guarded scalar path: any step, any boundary --------------------------------
+template <bool GRAD>
+__device__ __forceinline__ double edge_step(const Shard &s, krn_i64 base, int lane, double *x_out,
+                                            double *dx, double *db, bool dx_zero, bool db_zero,
+                                            double r4)
+{
+    double node[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        krn_i64 i = base + 4 * lane + e;
+        krn_i64 g = s.offset + i;
+        if (i >= s.n_local) {
+            // beyond the shard: tree padding if also beyond the problem, identity otherwise
+            node[e] = (g >= s.n_global) ? krn_tree_pad((krn_u64)g, (krn_u64)s.n_global) : -0.0;
+            continue;
+        }
+        const krn_i64 last = s.n_global - 1;
+        // scaled rows g-2 .. g+2 where they exist
+        double xs[5];
+#pragma unroll
+        for (int d = -2; d <= 2; ++d) {
+            krn_i64 gg = g + d;
+            bool need = GRAD || (d >= -1 && d <= 1);
+            xs[d + 2] = (need && gg >= 0 && gg <= last) ? 3.0 * x_at(s, i + d) : 0.0;
+        }
+        double y = stencil_row(xs[1], xs[2], xs[3], b_at(s, i), g != 0, g != last);
+        x_out[i] = xs[2];
+        if (!GRAD) {
+            node[e] = y * y;
+            continue;
+        }
+        node[e] = -0.0;
+        Chain own = adjoint_chain(y, r4, g != last, g != 0);
+        double r3_left = 0.0, r2_right = 0.0;
+        if (g != 0) {  // row g-1 exists: its "j+1" contribution lands here
+            double yl = stencil_row(xs[0], xs[1], xs[2], b_at(s, i - 1), g - 1 != 0, true);
+            r3_left = adjoint_chain(yl, r4, true, g - 1 != 0).r3;
+        }
+        if (g != last) {  // row g+1 exists: its "j-1" contribution lands here
+            double yr = stencil_row(xs[2], xs[3], xs[4], b_at(s, i + 1), true, g + 1 != last);
+            r2_right = adjoint_chain(yr, r4, g + 1 != last, true).r2;
+        }
+        if (dx != nullptr) {
+            double in = dx_zero ? 0.0 : dx[i];
+            dx[i] = finish_dx(in, r3_left, own.r1, r2_right, g != 0, g != last);
+        }
+        if (db != nullptr) {
+            double in = db_zero ? 0.0 : db[i];
+            db[i] = in + (-own.r1);
+        }
+    }
+    return (node[0] + node[1]) + (node[2] + node[3]);
+}
+
+// ---- interior path: 128 full rows, ghosts inside the shard, no guards -----------------
+template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO>
+__device__ __forceinline__ double interior_step(const double *__restrict__ x, const double *__restrict__ b,
+                                                krn_i64 base, int lane, double *__restrict__ x_out,
+                                                double *dx, double *db, double r4)
+{
+    const krn_i64 i0 = base + 4 * lane;
+    krn_d4 xv = krn_ld4_stream(x + i0);
+    krn_d4 bv = krn_ld4_stream(b + i0);
+    krn_d4 dxv = {0.0, 0.0, 0.0, 0.0}, dbv = {0.0, 0.0, 0.0, 0.0};
+    if (GRAD && HAS_DX && !DX_ZERO) dxv = krn_ld4_rmw(dx + i0);
+    if (GRAD && HAS_DB && !DB_ZERO) dbv = krn_ld4_rmw(db + i0);
+
+    // ghost rows of the neighbouring warp step, fetched by the two edge lanes
+    const bool left_edge = lane == 0, right_edge = lane == 31;
+    double g_far = 0.0, g_near = 0.0, g_b = 0.0;
+    if (left_edge) {
+        g_near = krn_ld1(x + i0 - 1);
+        if (GRAD) {
+            g_far = krn_ld1(x + i0 - 2);
+            g_b = krn_ld1(b + i0 - 1);
+        }
+    } else if (right_edge) {
+        g_near = krn_ld1(x + i0 + 4);
+        if (GRAD) {
+            g_far = krn_ld1(x + i0 + 5);
+            g_b = krn_ld1(b + i0 + 4);
+        }
+    }
+
+    krn_d4 xs = {3.0 * xv.a, 3.0 * xv.b, 3.0 * xv.c, 3.0 * xv.d};
+    krn_st4(x_out + i0, xs);
+
+    double xl = __shfl_up_sync(KRN_FULL_MASK, xs.d, 1);
+    double xr = __shfl_down_sync(KRN_FULL_MASK, xs.a, 1);
+    const double g_near_s = 3.0 * g_near;
+    if (left_edge) xl = g_near_s;
+    if (right_edge) xr = g_near_s;
+
+    double y0 = stencil_row(xl, xs.a, xs.b, bv.a, true, true);
+    double y1 = stencil_row(xs.a, xs.b, xs.c, bv.b, true, true);
+    double y2 = stencil_row(xs.b, xs.c, xs.d, bv.c, true, true);
+    double y3 = stencil_row(xs.c, xs.d, xr, bv.d, true, true);
+
+    if (!GRAD) return (y0 * y0 + y1 * y1) + (y2 * y2 + y3 * y3);
+
+    Chain c0 = adjoint_chain(y0, r4, true, true);
+    Chain c1 = adjoint_chain(y1, r4, true, true);
+    Chain c2 = adjoint_chain(y2, r4, true, true);
+    Chain c3 = adjoint_chain(y3, r4, true, true);
+
+    if (HAS_DX) {
+        // r3 of the row left of this lane, r2 of the row right of it
+        double r3_left = __shfl_up_sync(KRN_FULL_MASK, c3.r3, 1);
+        double r2_right = __shfl_down_sync(KRN_FULL_MASK, c0.r2, 1);
+        if (left_edge || right_edge) {
+            const double g_far_s = 3.0 * g_far;
+            double ym = left_edge ? g_far_s : xs.d;
+            double yp = left_edge ? xs.a : g_far_s;
+            Chain g = adjoint_chain(stencil_row(ym, g_near_s, yp, g_b, true, true), r4, true, true);
+            if (left_edge) r3_left = g.r3;
+            if (right_edge) r2_right = g.r2;
+        }
+        krn_d4 o;
+        o.a = finish_dx(dxv.a, r3_left, c0.r1, c1.r2, true, true);
+        o.b = finish_dx(dxv.b, c0.r3, c1.r1, c2.r2, true, true);
+        o.c = finish_dx(dxv.c, c1.r3, c2.r1, c3.r2, true, true);
+        o.d = finish_dx(dxv.d, c2.r3, c3.r1, r2_right, true, true);
+        krn_st4(dx + i0, o);
+    }
+    if (HAS_DB) {
+        krn_d4 o = {dbv.a + (-c0.r1), dbv.b + (-c1.r1), dbv.c + (-c2.r1), dbv.d + (-c3.r1)};
+        krn_st4(db + i0, o);
+    }
+    return -0.0;
+}
+
+template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO>
+__global__ void __launch_bounds__(kThreads)
+laplacian_kernel(Shard s, double *__restrict__ x_out, double *dx, double *db, double seed, int steps,
+                 bool vector_ok, double *partials, double *scratch, unsigned int *ticket, double *f_out,
+                 int accumulate)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const krn_i64 chunk = (krn_i64)kThreads * 4 * steps;
+    const krn_i64 warp_base = (krn_i64)blockIdx.x * chunk + (krn_i64)warp * kStep * steps;
+    const double d_sum = 0.0 + seed;   // let _d_sum = 0.0;  _d_sum += seed;
+    const double r4 = 0.0 + d_sum;     // parallel_sum(_d_y2, _d_sum) on a zero shadow
+
+    double stack[4];  // binary-counter tree over the warp's steps (steps <= 16)
+    int depth = 0;
+    for (int t = 0; t < steps; ++t) {
+        const krn_i64 base = warp_base + (krn_i64)t * kStep;
+        double node;
+        if (base >= s.n_local) {
+            // nothing of this step lies in the shard; it still owns a node of the tree
+            node = -0.0;
+            if (!GRAD) {
+                double v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    krn_i64 g = s.offset + base + 4 * lane + e;
+                    v[e] = g >= s.n_global ? krn_tree_pad((krn_u64)g, (krn_u64)s.n_global) : -0.0;
+                }
+                node = (v[0] + v[1]) + (v[2] + v[3]);
+            }
+        } else if (vector_ok && base >= 2 && base + kStep + 2 <= s.n_local) {
+            node = interior_step<GRAD, HAS_DX, HAS_DB, DX_ZERO, DB_ZERO>(s.x, s.b, base, lane, x_out, dx,
+                                                                           db, r4);
+        } else {
+            node = edge_step<GRAD>(s, base, lane, x_out, HAS_DX ? dx : nullptr, HAS_DB ? db : nullptr,
+                                   DX_ZERO, DB_ZERO, r4);
+        }
+        if (!GRAD) {
+            node = krn_warp_tree(node);
+            int m = t;
+            while (m & 1) {
+                node = stack[--depth] + node;
+                m >>= 1;
+            }
+            stack[depth++] = node;
+        }
+    }
+    if (GRAD) return;
+
+    __shared__ double s_warp[kWarps];
+    if (lane == 0) s_warp[warp] = stack[0];
+    __syncthreads();
+    if (warp == 0) {
+        double v = krn_smem_tree(s_warp, kWarps, lane);
+        if (lane == 0) partials[blockIdx.x] = v;
+    }
+    if (krn_last_block(ticket, gridDim.x)) {
+        double root = krn_final_tree(partials, scratch, gridDim.x);
+        if (threadIdx.x == 0) *f_out = (accumulate ? *f_out : 0.0) + root;
+    }
+}
+
+int steps_for(size_t n_global)
+{
+    // small problems are latency bound: spread them over as many blocks as possible;
+    // large ones amortise the per-block epilogue and keep the partial count low
+    return n_global <= (size_t(1) << 20) ? 1 : 8;
+}
+
+template <bool GRAD>
+int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, double *dx, double *db,
+           int dx_zero, int db_zero, size_t n_local, size_t offset, size_t n_global, const double *halo,
+           double seed, double *f, int accumulate)
+{
+    KRN_REQUIRE(ctx != nullptr, "null context");
+    KRN_REQUIRE(x_in && x_out && b, "null view pointer");
+    KRN_REQUIRE(x_in != x_out, "x_out must not alias x_in");
+    KRN_REQUIRE(offset + n_local <= n_global, "shard exceeds the problem");
+    KRN_REQUIRE(halo != nullptr || (offset == 0 && n_local == n_global),
+                "a shard that is not the whole problem needs halo rows");
+    KRN_REQUIRE(n_global < (size_t(1) << 62), "problem too large");
+    if (!GRAD) KRN_REQUIRE(f != nullptr, "null result pointer");
+    if (n_local == 0) {
+        if (!GRAD && !accumulate) KRN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), ctx->stream));
+        return KRN_OK;
+    }
+    const int steps = steps_for(n_global);
+    const size_t chunk = size_t(kThreads) * 4 * steps;
+    // the primal's tree runs over the padded problem so the last block owns every pad node
+    const size_t blocks = (n_local + chunk - 1) / chunk;
+    KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
+    if (!GRAD) {
+        int rc = krn_reserve_partials(ctx, blocks);
+        if (rc) return rc;
+    }
+    Shard s{x_in, b, halo, (krn_i64)n_local, (krn_i64)offset, (krn_i64)n_global};
+    bool vec = krn_aligned32(x_in) && krn_aligned32(x_out) && krn_aligned32(b) &&
+               (dx == nullptr || krn_aligned32(dx)) && (db == nullptr || krn_aligned32(db));
+    double *partials = ctx->d_partials, *scratch = ctx->d_partials + ctx->partial_capacity;
+    dim3 grid((unsigned)blocks), block(kThreads);
+#define KRN_LAP(G, HX, HB, ZX, ZB)                                                                    \
+    laplacian_kernel<G, HX, HB, ZX, ZB><<<grid, block, 0, ctx->stream>>>(                            \
+        s, x_out, dx, db, seed, steps, vec, partials, scratch, ctx->d_ticket, f, accumulate)
+    if (!GRAD) {
+        KRN_LAP(false, false, false, false, false);
+    } else {
+        const bool hx = dx != nullptr, hb = db != nullptr, zx = hx && dx_zero, zb = hb && db_zero;
+        if (hx && hb) {
+            if (zx && zb) KRN_LAP(true, true, true, true, true);
+            else if (zx) KRN_LAP(true, true, true, true, false);
+            else if (zb) KRN_LAP(true, true, true, false, true);
+            else KRN_LAP(true, true, true, false, false);
+        } else if (hx) {
+            if (zx) KRN_LAP(true, true, false, true, false);
+            else KRN_LAP(true, true, false, false, false);
+        } else if (hb) {
+            if (zb) KRN_LAP(true, false, true, false, true);
+            else KRN_LAP(true, false, true, false, false);
+        } else {
+            KRN_LAP(true, false, false, false, false);
+        }
+    }
+#undef KRN_LAP
+    KRN_LAUNCH_CHECK(ctx);
+    return KRN_OK;
+}
+
+}  // namespace
+
+extern "C" size_t krn_laplacian_partial_span(size_t n_global)
+{
+    return size_t(kThreads) * 4 * steps_for(n_global);
+}
+
+extern "C" int krn_laplacian_primal(krn_ctx *ctx, const double *d_x_in, double *d_x_out,
+                                    const double *d_b, size_t n_local, size_t offset, size_t n_global,
+                                    const double *d_halo, double *d_f, int accumulate)
+{
+    return launch<false>(ctx, d_x_in, d_x_out, d_b, nullptr, nullptr, 0, 0, n_local, offset, n_global,
+                         d_halo, 1.0, d_f, accumulate);
+}
+
+extern "C" int krn_laplacian_grad(krn_ctx *ctx, const double *d_x_in, double *d_x_out, const double *d_b,
+                                  double *d_dx, double *d_db, int dx_zero, int db_zero, size_t n_local,
+                                  size_t offset, size_t n_global, const double *d_halo, double seed)
+{
+    return launch<true>(ctx, d_x_in, d_x_out, d_b, d_dx, d_db, dx_zero, db_zero, n_local, offset,
+                        n_global, d_halo, seed, nullptr, 0);
+}

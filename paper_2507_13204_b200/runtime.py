@@ -1,0 +1,754 @@
+"""Execution of kernel-language functions on a B200.
+
+Drop-in for the reference's ``krn.runtime``
+(/root/reference/pkg/src/krn/runtime.py): same names, argument meaning and
+error behaviour for ``ViewStorage``, ``ExecutionConfig``, ``execute`` and the
+exception classes - but Views live in HBM and every array operation is a CUDA
+kernel in libkrn_b200.so (or generated through it).  There is no CPU
+execution path: without the library or without a device ``execute`` raises.
+
+Two execution policies (``ExecutionConfig.policy``):
+
+``"fused"`` (default)
+    a function whose tree matches the headline objective or its generated
+    gradient runs as ONE hand-written kernel (csrc/krn_laplacian.cu); anything
+    else falls through to ``"statements"``.
+``"statements"``
+    every statement is one launch, like the reference (and like Kokkos): bulk
+    builtins from the library, ``parallel_for`` bodies generated from the tree
+    (codegen.py).  This is the like-for-like granularity for the
+    gradient/primal ratio.
+
+Host/device coherence of a View: ``.buffer`` / ``.flat`` hand out the host
+array (refreshed from the device when stale) and, because the caller may write
+through it, mark the device copy stale; ``.peek()`` reads without invalidating.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses as _dc
+import os
+import struct
+import weakref
+
+import numpy as np
+
+from . import _cabi, codegen
+from .lang import nodes as N
+from .lang.nodes import ViewDescriptor, kind
+
+
+class ShapeMismatch(ValueError):
+    pass
+
+
+class OutOfBounds(IndexError):
+    pass
+
+
+class NonFiniteDetected(ArithmeticError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# device
+
+
+class Device:
+    """One libkrn_b200 context (device + stream + pool).  ``Device.get()``
+    returns the process-wide default for a device ordinal."""
+
+    _default: dict = {}
+
+    def __init__(self, ordinal: int = 0, stream: int = 0):
+        self.lib = _cabi.lib()
+        self.ordinal = ordinal
+        h = C.c_void_p()
+        _cabi.check(self.lib.krn_ctx_create(ordinal, C.c_void_p(stream), C.byref(h)))
+        self.h = h
+        # pinned staging block for small transfers: [0:64) status, [64:...) scalars
+        p = C.c_void_p()
+        _cabi.check(self.lib.krn_host_alloc(4096, C.byref(p)))
+        self._pinned = p
+        self.staging = np.frombuffer((C.c_char * 4096).from_address(p.value), dtype=np.uint8)
+        sp = C.c_void_p()
+        _cabi.check(self.lib.krn_status_device_ptr(self.h, C.byref(sp)))
+        self.status_ptr = sp.value
+        self._modules: dict = {}
+
+    @classmethod
+    def get(cls, ordinal=None) -> "Device":
+        if ordinal is None:
+            ordinal = int(os.environ.get("KRN_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+        d = cls._default.get(ordinal)
+        if d is None:
+            d = cls._default[ordinal] = Device(ordinal)
+        return d
+
+    # memory ----------------------------------------------------------------
+    def alloc(self, nbytes: int) -> int:
+        p = C.c_void_p()
+        _cabi.check(self.lib.krn_alloc(self.h, nbytes, C.byref(p)))
+        return p.value
+
+    def free(self, ptr: int):
+        if ptr:
+            self.lib.krn_free(self.h, C.c_void_p(ptr))
+
+    def upload(self, dptr: int, arr: np.ndarray):
+        _cabi.check(self.lib.krn_upload(self.h, C.c_void_p(dptr), C.c_void_p(arr.ctypes.data), arr.nbytes))
+
+    def download(self, arr: np.ndarray, dptr: int):
+        _cabi.check(self.lib.krn_download(self.h, C.c_void_p(arr.ctypes.data), C.c_void_p(dptr), arr.nbytes))
+
+    def download_async(self, arr: np.ndarray, dptr: int):
+        _cabi.check(
+            self.lib.krn_download_async(self.h, C.c_void_p(arr.ctypes.data), C.c_void_p(dptr), arr.nbytes)
+        )
+
+    def sync(self):
+        _cabi.check(self.lib.krn_sync(self.h))
+
+    def launches(self) -> int:
+        n = C.c_uint64()
+        _cabi.check(self.lib.krn_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def sm_count(self) -> int:
+        n = C.c_int()
+        _cabi.check(self.lib.krn_ctx_sm_count(self.h, C.byref(n)))
+        return n.value
+
+    # events ------------------------------------------------------------------
+    def event(self) -> int:
+        e = C.c_void_p()
+        _cabi.check(self.lib.krn_event_create(C.byref(e)))
+        return e.value
+
+    def record(self, event: int):
+        _cabi.check(self.lib.krn_event_record(self.h, C.c_void_p(event)))
+
+    def elapsed_ms(self, start: int, stop: int) -> float:
+        ms = C.c_float()
+        _cabi.check(self.lib.krn_event_elapsed_ms(C.c_void_p(start), C.c_void_p(stop), C.byref(ms)))
+        return ms.value
+
+    # builtins (thin) -----------------------------------------------------------
+    def fill(self, ptr, n, value=0.0, d_value=0):
+        _cabi.check(self.lib.krn_fill(self.h, C.c_void_p(ptr), n, float(value), C.c_void_p(d_value)))
+
+    def copy(self, dst, src, n):
+        _cabi.check(self.lib.krn_copy(self.h, C.c_void_p(dst), C.c_void_p(src), n))
+
+    def add_scalar(self, ptr, n, s=0.0, d_s=0):
+        _cabi.check(self.lib.krn_add_scalar(self.h, C.c_void_p(ptr), n, float(s), C.c_void_p(d_s)))
+
+    def add_view(self, dst, src, n):
+        _cabi.check(self.lib.krn_add_view(self.h, C.c_void_p(dst), C.c_void_p(src), n))
+
+    def reduce_pairwise(self, ptr, n, d_out, accumulate):
+        _cabi.check(
+            self.lib.krn_reduce_pairwise(self.h, C.c_void_p(ptr), n, C.c_void_p(d_out), int(accumulate))
+        )
+
+    def check_finite(self, ptr, n, d_flag):
+        _cabi.check(self.lib.krn_check_finite(self.h, C.c_void_p(ptr), n, C.c_void_p(d_flag)))
+
+    def module(self, source: str):
+        m = self._modules.get(source)
+        if m is None:
+            h = C.c_void_p()
+            _cabi.check(self.lib.krn_module_compile(self.h, source.encode(), C.byref(h)))
+            m = self._modules[source] = h
+        return m
+
+
+# ---------------------------------------------------------------------------
+# View storage
+
+
+class _DeviceBuffer:
+    """Owns one device allocation; returned to the pool when collected."""
+
+    __slots__ = ("dev", "ptr", "nbytes", "__weakref__")
+
+    def __init__(self, dev: Device, nbytes: int):
+        self.dev, self.nbytes = dev, nbytes
+        self.ptr = dev.alloc(nbytes)
+
+    def __del__(self):
+        try:
+            self.dev.free(self.ptr)
+        except Exception:
+            pass
+
+
+class ViewStorage:
+    """A rank-1 or rank-2 float64 View with reference semantics, resident in
+    HBM (reference: runtime.py:74-115).
+
+    State: ``_host`` (ndarray or None), ``_dev`` (_DeviceBuffer or None) and
+    which of them is current.  ``_zero`` marks a View known to hold +0.0
+    everywhere with no storage touched yet (``ViewStorage.zeros`` provenance):
+    the fused gradient kernel skips reading such a shadow.
+    """
+
+    __slots__ = ("descriptor", "_shape", "_host", "_dev", "_host_ok", "_dev_ok", "_zero")
+
+    def __init__(self, descriptor, buffer):
+        buffer = np.asarray(buffer)
+        if buffer.dtype != np.float64 or not buffer.flags.c_contiguous:
+            buffer = np.ascontiguousarray(buffer, dtype=np.float64)
+        if buffer.ndim != descriptor.rank:
+            raise ShapeMismatch(
+                f"view '{descriptor.name}': rank {descriptor.rank} descriptor, rank {buffer.ndim} data"
+            )
+        self.descriptor = descriptor
+        self._shape = tuple(buffer.shape)
+        self._host = buffer
+        self._dev = None
+        self._host_ok, self._dev_ok, self._zero = True, False, False
+
+    # -- construction -----------------------------------------------------------
+    @classmethod
+    def _blank(cls, name, extents) -> "ViewStorage":
+        self = object.__new__(cls)
+        self._shape = tuple(int(e) for e in extents)
+        self.descriptor = ViewDescriptor(name, rank=len(self._shape))
+        self._host = self._dev = None
+        self._host_ok = self._dev_ok = False
+        self._zero = False
+        return self
+
+    @classmethod
+    def zeros(cls, name: str, extents) -> "ViewStorage":
+        self = cls._blank(name, extents)
+        self._zero = True
+        return self
+
+    @classmethod
+    def from_values(cls, name: str, values) -> "ViewStorage":
+        arr = np.array(values, dtype=np.float64, order="C")
+        return cls(ViewDescriptor(name, rank=arr.ndim), arr)
+
+    def copy(self) -> "ViewStorage":
+        out = ViewStorage._blank(self.descriptor.name, self._shape)
+        out.descriptor = self.descriptor
+        if self._zero:
+            out._zero = True
+        elif self._dev_ok:
+            out._dev = _DeviceBuffer(self._dev.dev, self.nbytes)
+            self._dev.dev.copy(out._dev.ptr, self._dev.ptr, self.size)
+            out._dev_ok = True
+        else:
+            out._host = self._host.copy()
+            out._host_ok = True
+        return out
+
+    # -- shape --------------------------------------------------------------------
+    @property
+    def extents(self) -> tuple:
+        return self._shape
+
+    @property
+    def name(self) -> str:
+        return self.descriptor.name
+
+    @property
+    def size(self) -> int:
+        n = 1
+        for e in self._shape:
+            n *= e
+        return n
+
+    @property
+    def nbytes(self) -> int:
+        return 8 * self.size
+
+    # -- host side -------------------------------------------------------------------
+    def _sync_host(self):
+        if self._host is None:
+            self._host = np.zeros(self._shape, dtype=np.float64)
+            if self._zero:
+                self._host_ok = True
+        elif self._zero and not self._host_ok:
+            self._host.fill(0.0)
+            self._host_ok = True
+        if not self._host_ok:
+            self._dev.dev.download(self._host, self._dev.ptr)
+            self._host_ok = True
+
+    def peek(self) -> np.ndarray:
+        """Current contents as a read-only host array; the device copy stays valid."""
+        self._sync_host()
+        out = self._host.view()
+        out.flags.writeable = False
+        return out
+
+    @property
+    def buffer(self) -> np.ndarray:
+        """The host array (same object on every call).  The caller may write
+        through it, so the device copy is considered stale afterwards."""
+        self._sync_host()
+        self._dev_ok = False
+        self._zero = False
+        return self._host
+
+    @property
+    def flat(self) -> np.ndarray:
+        return self.buffer.reshape(-1)
+
+    # -- device side ---------------------------------------------------------------------
+    def device_ptr(self, dev: Device, *, write: bool = True, discard: bool = False) -> int:
+        """Device pointer with current contents (``discard``: contents will be
+        fully overwritten, skip upload / zero fill).  ``write`` marks the host
+        copy stale."""
+        if self._dev is None or self._dev.dev is not dev:
+            if self._dev is not None and self._dev_ok and not self._host_ok:
+                self._sync_host()
+            self._dev = _DeviceBuffer(dev, self.nbytes)
+            self._dev_ok = False
+        if not self._dev_ok and not discard:
+            if self._zero:
+                dev.fill(self._dev.ptr, self.size, 0.0)
+            else:
+                dev.upload(self._dev.ptr, self._host)
+        self._dev_ok = True
+        if write or discard:
+            self._host_ok = False
+            self._zero = False
+        return self._dev.ptr
+
+    def _adopt(self, buf: _DeviceBuffer):
+        """Replace the device storage (out-of-place kernels swap buffers)."""
+        self._dev = buf
+        self._dev_ok, self._host_ok, self._zero = True, False, False
+
+    def __repr__(self) -> str:
+        return f"ViewStorage({self.name!r}, shape={self._shape})"
+
+
+# ---------------------------------------------------------------------------
+# configuration / results
+
+
+@_dc.dataclass
+class ExecutionConfig:
+    """Reference fields (runtime.py:118-128) plus the GPU knobs.  ``threads``
+    is accepted for compatibility and ignored: iterations map to CUDA threads."""
+
+    threads: int = 1
+    deterministic_reduction: bool = True
+    conflict_detect: bool = False
+    rng_seed: int = 0
+    check_finite: bool = False
+    policy: str = "fused"  # "fused" | "statements"
+    device: object = None  # device ordinal; None = KRN_DEVICE / LOCAL_RANK / 0
+
+    def __post_init__(self):
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.policy not in ("fused", "statements"):
+            raise ValueError("policy must be 'fused' or 'statements'")
+
+
+def effective_threads(cfg: ExecutionConfig) -> int:
+    env = os.environ.get("KRN_THREADS")
+    return max(1, int(env)) if env else cfg.threads
+
+
+@_dc.dataclass(frozen=True)
+class ConflictRecord:
+    kernel: int
+    view: str
+    offset: int
+    iterations: tuple
+    kinds: tuple
+
+
+@_dc.dataclass(frozen=True)
+class ConflictReport:
+    records: tuple = ()
+
+    def __bool__(self) -> bool:
+        return bool(self.records)
+
+    def write_write(self) -> tuple:
+        return tuple(r for r in self.records if "write" in r.kinds)
+
+
+@_dc.dataclass
+class ExecResult:
+    value: object
+    conflicts: object = None
+
+
+# ---------------------------------------------------------------------------
+# statement-granular plan
+
+
+class _Plan:
+    """Compiled form of one function: generated module + step list."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        b = self.builder = codegen.ModuleBuilder(fn)
+        self.steps: list = []
+        bound = {p.name for p in fn.params if not p.is_view}
+        run: list = []
+
+        def flush():
+            if run:
+                self.steps.append(("scalars", b.scalar_block(list(run), f"s{len(self.steps)}")))
+                run.clear()
+
+        for s in fn.body:
+            k = kind(s)
+            if k in codegen._ELEMENT:
+                run.append(s)
+                if k == "DeclScalar":
+                    bound.add(s.name)
+                continue
+            flush()
+            if k == "DeclView":
+                self.steps.append(("declview", s))
+            elif k == "ParallelFor":
+                self.steps.append(("kernel", s, b.kernel(s, f"k{len(self.steps)}")))
+            elif k == "DeepCopy":
+                self.steps.append(("deepcopy", s))
+            elif k == "ParallelSum":
+                self.steps.append(("gather", s, s.dst in bound))
+                bound.add(s.dst)
+                b.slot(s.dst)
+            elif k == "ParallelSumInto":
+                self.steps.append(("suminto", s))
+            elif k == "Return":
+                self.steps.append(("return", b.return_block(s.value, f"r{len(self.steps)}")))
+            else:
+                raise TypeError(f"cannot execute {k}")
+        flush()
+        self.source = b.source()
+        self.nslots = max(len(b.slots), 1) + 1
+
+
+_plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_plans_by_id: dict = {}
+
+
+def _plan_for(fn) -> _Plan:
+    key = id(fn)
+    hit = _plans_by_id.get(key)
+    if hit is not None and hit[0] is fn:
+        return hit[1]
+    plan = _Plan(fn)
+    _plans_by_id[key] = (fn, plan)  # holds fn alive so the id stays unique
+    return plan
+
+
+def _scalar_src(dev, plan, S, src):
+    """(host value, device pointer) for a Literal / ScalarVar bulk operand."""
+    if kind(src) == "Literal":
+        return float(src.value), 0
+    return 0.0, S + 8 * plan.builder.slot(src.name)
+
+
+def _index_value(e, views) -> int:
+    """Host evaluation of a view-free index expression (extents are host data)."""
+    k = kind(e)
+    if k == "IntLiteral":
+        return e.value
+    if k == "Extent":
+        return views[e.view].extents[e.dim]
+    if k == "IdxBinary":
+        a, b = _index_value(e.lhs, views), _index_value(e.rhs, views)
+        return a + b if e.op == "+" else a - b if e.op == "-" else a * b
+    raise TypeError(f"index expression is not host-evaluable: {kind(e)}")
+
+
+class _Run:
+    """One call of a function under the statement policy."""
+
+    def __init__(self, dev: Device, plan: _Plan, views: dict, scalars: dict, cfg):
+        self.dev, self.plan, self.views, self.cfg = dev, plan, views, cfg
+        self.b = plan.builder
+        self.mod = dev.module(plan.source)
+        nslots = plan.nslots
+        self.S = _DeviceBuffer(dev, 8 * nslots)
+        init = np.zeros(nslots)
+        for name, v in scalars.items():
+            init[self.b.slot(name)] = v
+        host = dev.staging[64 : 64 + 8 * nslots].view(np.float64) if 8 * nslots <= 4096 - 64 else init
+        host[:] = init
+        dev.upload(self.S.ptr, host)
+        _cabi.check(dev.lib.krn_status_reset(dev.h))
+        self.kernel_index = 0
+
+    def env(self) -> bytes:
+        nv = max(len(self.b.views), 1)
+        ptrs, e0, e1 = [0] * nv, [0] * nv, [0] * nv
+        for i, name in enumerate(self.b.views):
+            v = self.views.get(name)
+            if v is not None:
+                ptrs[i] = v.device_ptr(self.dev)
+                e0[i] = v.extents[0]
+                e1[i] = v.extents[1] if len(v.extents) == 2 else 1
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr)
+
+    def launch(self, name: str, n: int, extra=()):
+        env = C.create_string_buffer(self.env())
+        holders = [env]
+        args = [C.addressof(env)]
+        for x in extra:
+            h = C.c_longlong(x) if isinstance(x, int) else x
+            holders.append(h)
+            args.append(C.addressof(h))
+        arr = (C.c_void_p * len(args))(*args)
+        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), n, arr))
+
+    def go(self):
+        for step in self.plan.steps:
+            getattr(self, "do_" + step[0])(*step[1:])
+        return self.finish()
+
+    # -- steps ----------------------------------------------------------------------
+    def do_declview(self, s):
+        args = iter(s.dyn_args)
+        dims = [
+            e.size if kind(e) == "StaticExtent" else int(_index_value(next(args), self.views))
+            for e in s.descriptor.extents
+        ]
+        if any(d < 0 for d in dims):
+            raise ShapeMismatch(f"view '{s.name}': negative extent {dims}")
+        self.views[s.name] = ViewStorage.zeros(s.name, dims)
+
+    def do_scalars(self, recipe):
+        self.launch(recipe["name"], 1)
+        self.guard()
+
+    def do_kernel(self, loop, recipe):
+        n = int(_index_value(loop.upper, self.views))
+        stage = ostage = None
+        extra = [max(n, 0), C.c_void_p(0), C.c_void_p(0)]
+        if recipe["n_staged"] and n > 0:
+            stage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
+            extra[1] = C.c_void_p(stage.ptr)
+            if recipe["needs_offsets"]:
+                ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
+                extra[2] = C.c_void_p(ostage.ptr)
+        if n > 0:
+            self.launch(recipe["name"], n, extra)
+            for ap in recipe["apply"]:
+                count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
+                if count > 0:
+                    self.launch(ap["name"], count, extra)
+        self.kernel_index += 1
+        self.guard()
+
+    def do_deepcopy(self, s):
+        d = self.views[s.dst]
+        if isinstance(s.src, str):
+            src = self.views[s.src]
+            if d.extents != src.extents:
+                raise ShapeMismatch(f"deep_copy: {s.dst}{d.extents} vs {s.src}{src.extents}")
+            self.dev.copy(d.device_ptr(self.dev, discard=True), src.device_ptr(self.dev, write=False), d.size)
+        else:
+            value, dptr = _scalar_src(self.dev, self.plan, self.S.ptr, s.src)
+            self.dev.fill(d.device_ptr(self.dev, discard=True), d.size, value, dptr)
+        self.guard()
+
+    def do_gather(self, s, accumulate):
+        src = self.views[s.src]
+        out = self.S.ptr + 8 * self.b.slot(s.dst)
+        self.dev.reduce_pairwise(src.device_ptr(self.dev, write=False), src.size, out, accumulate)
+        if self.cfg.check_finite:
+            self.guard_scalar(self.b.slot(s.dst))
+
+    def do_suminto(self, s):
+        d = self.views[s.dst]
+        if isinstance(s.src, str):
+            src = self.views[s.src]
+            if d.extents != src.extents:
+                raise ShapeMismatch(f"parallel_sum: {s.dst}{d.extents} vs {s.src}{src.extents}")
+            self.dev.add_view(d.device_ptr(self.dev), src.device_ptr(self.dev, write=False), d.size)
+        else:
+            value, dptr = _scalar_src(self.dev, self.plan, self.S.ptr, s.src)
+            self.dev.add_scalar(d.device_ptr(self.dev), d.size, value, dptr)
+        self.guard()
+
+    def do_return(self, recipe):
+        self.launch(recipe["name"], 1)
+        self.ret_slot = recipe["slot"]
+
+    ret_slot = None
+
+    # -- sync points -------------------------------------------------------------------
+    def read_status(self):
+        st = self.dev.staging[:64].view(np.int64)
+        self.dev.download(st, self.dev.status_ptr)
+        if st[0] != 0:
+            raise self.error_from(st.copy())
+
+    def error_from(self, st):
+        code, line, vid, i0, i1 = (int(x) for x in st[:5])
+        name = self.b.views[vid] if 0 <= vid < len(self.b.views) else "?"
+        view = self.views.get(name)
+        if code == _cabi.KRN_ST_OUT_OF_BOUNDS:
+            if view is not None and len(view.extents) == 2:
+                n0, n1 = view.extents
+                return OutOfBounds(f"line {line}: {name}({i0}, {i1}) outside extents {n0}x{n1}")
+            n0 = view.extents[0] if view is not None else "?"
+            return OutOfBounds(f"line {line}: {name}({i0}) outside extent {n0}")
+        if code == _cabi.KRN_ST_BAD_INDEX:
+            if i0:  # infinite
+                return OverflowError("cannot convert float infinity to integer")
+            return ValueError("cannot convert float NaN to integer")
+        return RuntimeError(f"device status {code}")
+
+    def guard(self):
+        """check_finite: trap after every kernel / bulk statement (runtime.py:669-672)."""
+        if not self.cfg.check_finite:
+            return
+        self.read_status()
+        live = [(n, v) for n, v in self.views.items() if v.size]
+        words = (len(live) + 1) // 2 + 1
+        flags = _DeviceBuffer(self.dev, 8 * words)
+        self.dev.fill(flags.ptr, words, 0.0)
+        for i, (_, v) in enumerate(live):
+            self.dev.check_finite(v.device_ptr(self.dev, write=False), v.size, flags.ptr + 4 * i)
+        host = np.zeros(max(len(live), 1), dtype=np.int32)
+        self.dev.download(host, flags.ptr)
+        for i, (name, _) in enumerate(live):
+            if host[i]:
+                raise NonFiniteDetected(f"non-finite value in view '{name}'")
+
+    def guard_scalar(self, slot):
+        v = np.zeros(1)
+        self.dev.download(v, self.S.ptr + 8 * slot)
+        if not np.isfinite(v[0]):
+            raise NonFiniteDetected(f"non-finite scalar {float(v[0])!r}")
+
+    def finish(self):
+        value = None
+        if self.ret_slot is not None:
+            out = self.dev.staging[64:72].view(np.float64)
+            self.dev.download_async(out, self.S.ptr + 8 * self.ret_slot)
+        self.read_status()  # synchronises the stream
+        if self.ret_slot is not None:
+            value = float(self.dev.staging[64:72].view(np.float64)[0])
+            if self.cfg.check_finite and not np.isfinite(value):
+                raise NonFiniteDetected(f"non-finite scalar {value!r}")
+        return value
+
+
+# ---------------------------------------------------------------------------
+# entry points
+
+
+def _bind(fn, inputs: dict):
+    """Parameter binding with the reference's checks and messages (runtime.py:481-511)."""
+    want, got = {p.name for p in fn.params}, set(inputs)
+    if want != got:
+        parts = []
+        if want - got:
+            parts.append(f"missing {sorted(want - got)}")
+        if got - want:
+            parts.append(f"unexpected {sorted(got - want)}")
+        raise ShapeMismatch(f"inputs do not match parameters: {'; '.join(parts)}")
+    views, scalars = {}, {}
+    for p in fn.params:
+        v = inputs[p.name]
+        if p.is_view:
+            if not isinstance(v, ViewStorage):
+                v = ViewStorage.from_values(p.name, v)
+                inputs[p.name] = v
+            if len(v.extents) != p.type.rank:
+                raise ShapeMismatch(
+                    f"parameter '{p.name}': rank {p.type.rank} expected, got rank {len(v.extents)}"
+                )
+            for dim, ext in enumerate(p.type.extents):
+                if kind(ext) == "StaticExtent" and v.extents[dim] != ext.size:
+                    raise ShapeMismatch(
+                        f"parameter '{p.name}' dim {dim}: static extent {ext.size} expected, "
+                        f"got {v.extents[dim]}"
+                    )
+            views[p.name] = v
+        else:
+            scalars[p.name] = float(v)
+    return views, scalars
+
+
+def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = None) -> ExecResult:
+    """Run ``fn_name`` on the GPU.  View inputs are mutated in place (their
+    device storage is; ``.buffer`` shows the result).  Synchronous, like the
+    reference (runtime.py:689-706)."""
+    from . import fused
+
+    cfg = cfg or ExecutionConfig()
+    fn = program.function(fn_name)
+    if fn is None:
+        raise KeyError(f"no function named '{fn_name}'")
+    if cfg.conflict_detect:
+        raise NotImplementedError(
+            "conflict detection is the reference's sequential CPU debugging aid "
+            "(runtime.py:574-585) and is outside the GPU path"
+        )
+    views, scalars = _bind(fn, inputs)
+    dev = Device.get(cfg.device)
+    if cfg.policy == "fused" and not cfg.check_finite:
+        hit = fused.match(fn)
+        if hit is not None and hit.applicable(views):
+            return ExecResult(hit.run(dev, views, scalars))
+    plan = _plan_for(fn)
+    return ExecResult(_Run(dev, plan, views, scalars, cfg).go())
+
+
+def detect_conflicts(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = None):
+    raise NotImplementedError(
+        "detect_conflicts replays kernels sequentially on the CPU by design "
+        "(reference runtime.py:709-726); it is not part of the GPU path"
+    )
+
+
+def pairwise_sum(values) -> float:
+    """The reference's fixed-tree sum (runtime.py:166-177), evaluated on the device."""
+    a = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+    if a.size == 0:
+        return 0.0
+    dev = Device.get()
+    v = ViewStorage.from_values("v", a)
+    out = _DeviceBuffer(dev, 8)
+    dev.reduce_pairwise(v.device_ptr(dev, write=False), a.size, out.ptr, False)
+    host = np.zeros(1)
+    dev.download(host, out.ptr)
+    return float(host[0])
+
+
+# ---------------------------------------------------------------------------
+# tensor files (host-side text format of the reference, runtime.py:733-757)
+
+
+def save_tensor(path, storage: ViewStorage) -> None:
+    data = storage.peek()
+    with open(path, "w", encoding="utf-8") as f:
+        f.write("f64 %d %s\n" % (data.ndim, " ".join(str(d) for d in data.shape)))
+        for x in data.reshape(-1):
+            f.write(repr(float(x)) + "\n")
+
+
+def load_tensor(path, name: str | None = None) -> ViewStorage:
+    with open(path, "r", encoding="utf-8") as f:
+        header = f.readline().split()
+        if len(header) < 3 or header[0] != "f64":
+            raise ShapeMismatch(f"{path}: malformed tensor header {header!r}")
+        rank = int(header[1])
+        dims = [int(d) for d in header[2 : 2 + rank]]
+        if len(dims) != rank or rank not in (1, 2):
+            raise ShapeMismatch(f"{path}: bad rank/extents {header!r}")
+        tokens = f.read().split()
+    data = np.array(tokens, dtype=np.float64) if tokens else np.zeros(0)
+    if data.size != int(np.prod(dims)):
+        raise ShapeMismatch(f"{path}: expected {int(np.prod(dims))} values, found {data.size}")
+    if name is None:
+        name = os.path.splitext(os.path.basename(path))[0]
+    return ViewStorage.from_values(name, data.reshape(dims))
