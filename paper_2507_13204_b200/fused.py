@@ -124,7 +124,7 @@ class _Bound:
         objs = [id(views[name]) for name in self.roles.values()]
         return len(set(objs)) == len(objs)
 
-    def run(self, dev, views, scalars):
+    def run(self, dev, views, scalars, synchronous=True):
         from .runtime import _DeviceBuffer
 
         lib = dev.lib
@@ -142,6 +142,9 @@ class _Bound:
                                                      C.c_void_p(b_ptr), n, 0, n, None, C.c_void_p(f), 0))
                 x._adopt(x_out)
                 out = dev.staging[64:72].view("float64")
+                if not synchronous:
+                    dev.download_async(out, f)
+                    return None
                 dev.download(out, f)
                 return float(out[0])
             finally:
@@ -156,7 +159,8 @@ class _Bound:
                                            C.c_void_p(dx_ptr), C.c_void_p(db_ptr), int(dx_zero), int(db_zero),
                                            n, 0, n, None, float(self.m.seed)))
         x._adopt(x_out)
-        dev.sync()
+        if synchronous:
+            dev.sync()
         return None
 
 

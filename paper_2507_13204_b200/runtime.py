@@ -79,6 +79,8 @@ class Device:
 
     @classmethod
     def get(cls, ordinal=None) -> "Device":
+        if isinstance(ordinal, Device):
+            return ordinal
         if ordinal is None:
             ordinal = int(os.environ.get("KRN_DEVICE", os.environ.get("LOCAL_RANK", "0")))
         d = cls._default.get(ordinal)
@@ -184,6 +186,35 @@ class _DeviceBuffer:
             pass
 
 
+class _PinnedBlock:
+    """Owns one cudaMallocHost block; numpy views keep it alive via ``base``."""
+
+    def __init__(self, nbytes: int):
+        lib = _cabi.lib()
+        p = C.c_void_p()
+        _cabi.check(lib.krn_host_alloc(max(nbytes, 8), C.byref(p)))
+        self.ptr, self.nbytes, self._lib = p.value, nbytes, lib
+        self.raw = (C.c_char * max(nbytes, 8)).from_address(p.value)
+
+    def __del__(self):
+        try:
+            self._lib.krn_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+def pinned_array(extents) -> np.ndarray:
+    """Zero-filled float64 array in page-locked host memory."""
+    shape = tuple(int(e) for e in extents)
+    n = int(np.prod(shape)) if shape else 1
+    block = _PinnedBlock(8 * n)
+    arr = np.frombuffer(block.raw, dtype=np.float64, count=n).reshape(shape)
+    arr[...] = 0.0
+    # numpy keeps `block.raw` alive through arr.base; tie the block's lifetime to it
+    block.raw._owner = block
+    return arr
+
+
 class ViewStorage:
     """A rank-1 or rank-2 float64 View with reference semantics, resident in
     HBM (reference: runtime.py:74-115).
@@ -231,6 +262,12 @@ class ViewStorage:
     def from_values(cls, name: str, values) -> "ViewStorage":
         arr = np.array(values, dtype=np.float64, order="C")
         return cls(ViewDescriptor(name, rank=arr.ndim), arr)
+
+    @classmethod
+    def pinned(cls, name: str, extents) -> "ViewStorage":
+        """A View whose host array lives in page-locked memory (zero filled), so
+        host<->device copies run at full PCIe speed and asynchronously."""
+        return cls(ViewDescriptor(name, rank=len(tuple(extents))), pinned_array(extents))
 
     def copy(self) -> "ViewStorage":
         out = ViewStorage._blank(self.descriptor.name, self._shape)
@@ -344,7 +381,10 @@ class ExecutionConfig:
     rng_seed: int = 0
     check_finite: bool = False
     policy: str = "fused"  # "fused" | "statements"
-    device: object = None  # device ordinal; None = KRN_DEVICE / LOCAL_RANK / 0
+    device: object = None  # device ordinal or Device; None = KRN_DEVICE / LOCAL_RANK / 0
+    # False: enqueue only (no host sync, no status check, value not fetched); for timing
+    # the launch sequence with events.  The reference contract is synchronous.
+    synchronous: bool = True
 
     def __post_init__(self):
         if self.threads < 1:
@@ -633,6 +673,8 @@ class _Run:
         if self.ret_slot is not None:
             out = self.dev.staging[64:72].view(np.float64)
             self.dev.download_async(out, self.S.ptr + 8 * self.ret_slot)
+        if not self.cfg.synchronous:
+            return None
         self.read_status()  # synchronises the stream
         if self.ret_slot is not None:
             value = float(self.dev.staging[64:72].view(np.float64)[0])
@@ -698,7 +740,7 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
     if cfg.policy == "fused" and not cfg.check_finite:
         hit = fused.match(fn)
         if hit is not None and hit.applicable(views):
-            return ExecResult(hit.run(dev, views, scalars))
+            return ExecResult(hit.run(dev, views, scalars, cfg.synchronous))
     plan = _plan_for(fn)
     return ExecResult(_Run(dev, plan, views, scalars, cfg).go())
 
