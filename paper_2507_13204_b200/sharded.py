@@ -81,9 +81,9 @@ class ShardedLaplacian:
         if self.world == 1:
             return None
         mine = pack_boundary(x, b)
-        gathered = torch.empty(self.world, 6, dtype=x.dtype, device=x.device)
+        gathered = torch.empty(self.world * 6, dtype=x.dtype, device=x.device)  # flat: gloo and nccl agree
         self.dist.all_gather_into_tensor(gathered, mine, group=self.group)
-        return assemble_halo(gathered, self.rank, self.world)
+        return assemble_halo(gathered.view(self.world, 6), self.rank, self.world)
 
     def primal(self, x, x_out, b, f_out):
         """f_out (1-element tensor) <- global objective; x_out <- 3x (local rows)."""

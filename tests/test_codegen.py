@@ -1,0 +1,55 @@
+"""CPU tier: host logic of the statement path - accumulation policy per atomic
+target, generated module shape, plan steps."""
+
+import numpy as np
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import codegen
+from paper_2507_13204_b200.lang import nodes as N
+from paper_2507_13204_b200.runtime import _plan_for
+from conftest import CORPUS
+
+
+def _grad(stem):
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+    return krn.differentiate(prog, fn.name, wrt).functions[-1]
+
+
+def _loops(fn):
+    return [s for s in fn.body if N.kind(s) == "ParallelFor"]
+
+
+def test_atomic_policies():
+    lap = _loops(_grad("laplacian"))[2]
+    sites = codegen.plan_atomics(lap)
+    assert [(s.view, s.offset, s.mode) for s in sites] == [
+        ("_d_x", 1, "gather"), ("_d_x", -1, "gather"), ("_d_x", 0, "gather")]
+    gi = _loops(_grad("gather_indirect"))[1]
+    assert [s.mode for s in codegen.plan_atomics(gi)] == ["atomic", "atomic"]
+    rs = _loops(_grad("rowscale_rank2"))[1]
+    sites = codegen.plan_atomics(rs)
+    assert {s.mode for s in sites} == {"gather"}
+    assert sorted({(s.view, s.column) for s in sites}) == [("_d_m", 0), ("_d_m", 1), ("_d_m", 2),
+                                                          ("_d_q", 0), ("_d_q", 1), ("_d_q", 2)]
+    # a target that the kernel also reads through an indirect index must be staged
+    p = krn.parse("fn f(x: view<f64,1>, idx: view<f64,1>) { parallel_for i in 0..extent(idx,0) {"
+                  " atomic_add(x(idx(i)), x(i)); } }")
+    assert [s.mode for s in codegen.plan_atomics(p.functions[0].body[0])] == ["staged_atomic"]
+
+
+def test_every_corpus_function_plans():
+    for stem in CORPUS:
+        prog = krn.load_program(stem)
+        for fn in (prog.functions[0], _grad(stem)):
+            plan = _plan_for(fn)
+            assert plan.source.count('extern "C" __global__') >= 1
+            kinds = [s[0] for s in plan.steps]
+            assert kinds.count("kernel") == len(_loops(fn))
+
+
+def test_literals_are_exact():
+    for v in (0.1, 1.5, -0.25, 3.0, 1e-300, 5e-324, -0.0):
+        text = codegen.c_double(v).strip("()")
+        assert float.fromhex(text) == v and np.signbit(float.fromhex(text)) == np.signbit(v)
