@@ -68,38 +68,38 @@ int launch_stream(krn_ctx *ctx, double *dst, const double *src, size_t n, double
 // ---- pairwise-tree gather --------------------------------------------------------
 // Same decomposition as the fused objective kernel: block = aligned chunk of
 // 1024*steps leaves, warp = aligned sub-chunk, lane = 4 consecutive leaves.
-template <bool VEC>
+template <bool VEC, int STEPS>
 __global__ void __launch_bounds__(kThreads)
-tree_kernel(const double *__restrict__ v, krn_u64 n, int steps, double *partials, double *scratch,
+tree_kernel(const double *__restrict__ v, krn_u64 n, double *partials, double *scratch,
             unsigned int *ticket, double *out, int accumulate)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const krn_u64 chunk = krn_u64(kThreads) * 4 * steps;
-    const krn_u64 warp_base = krn_u64(blockIdx.x) * chunk + krn_u64(warp) * kStep * steps;
-    double stack[4];
-    int depth = 0;
-    for (int t = 0; t < steps; ++t) {
+    constexpr krn_u64 chunk = krn_u64(kThreads) * 4 * STEPS;
+    const krn_u64 warp_base = krn_u64(blockIdx.x) * chunk + krn_u64(warp) * kStep * STEPS;
+    // all loads of the warp's sub-chunk are issued before the first add
+    krn_d4 q[STEPS];
+#pragma unroll
+    for (int t = 0; t < STEPS; ++t) {
         const krn_u64 j0 = warp_base + krn_u64(t) * kStep + 4 * lane;
-        double a, b, c, d;
         if (VEC && j0 + 4 <= n) {
-            krn_d4 q = krn_ld4_stream(v + j0);
-            a = q.a, b = q.b, c = q.c, d = q.d;
+            q[t] = krn_ld4_stream(v + j0);
         } else {
-            a = j0 + 0 < n ? krn_ld1(v + j0 + 0) : krn_tree_pad(j0 + 0, n);
-            b = j0 + 1 < n ? krn_ld1(v + j0 + 1) : krn_tree_pad(j0 + 1, n);
-            c = j0 + 2 < n ? krn_ld1(v + j0 + 2) : krn_tree_pad(j0 + 2, n);
-            d = j0 + 3 < n ? krn_ld1(v + j0 + 3) : krn_tree_pad(j0 + 3, n);
+            q[t].a = j0 + 0 < n ? krn_ld1(v + j0 + 0) : krn_tree_pad(j0 + 0, n);
+            q[t].b = j0 + 1 < n ? krn_ld1(v + j0 + 1) : krn_tree_pad(j0 + 1, n);
+            q[t].c = j0 + 2 < n ? krn_ld1(v + j0 + 2) : krn_tree_pad(j0 + 2, n);
+            q[t].d = j0 + 3 < n ? krn_ld1(v + j0 + 3) : krn_tree_pad(j0 + 3, n);
         }
-        double node = krn_warp_tree((a + b) + (c + d));
-        int m = t;
-        while (m & 1) {
-            node = stack[--depth] + node;
-            m >>= 1;
-        }
-        stack[depth++] = node;
+    }
+    double nodes[STEPS];
+#pragma unroll
+    for (int t = 0; t < STEPS; ++t) nodes[t] = krn_warp_tree((q[t].a + q[t].b) + (q[t].c + q[t].d));
+#pragma unroll
+    for (int w = 1; w < STEPS; w <<= 1) {
+#pragma unroll
+        for (int i = 0; i < STEPS; i += 2 * w) nodes[i] = nodes[i] + nodes[i + w];
     }
     __shared__ double s_warp[kWarps];
-    if (lane == 0) s_warp[warp] = stack[0];
+    if (lane == 0) s_warp[warp] = nodes[0];
     __syncthreads();
     if (warp == 0) {
         double r = krn_smem_tree(s_warp, kWarps, lane);
@@ -177,12 +177,18 @@ extern "C" int krn_reduce_pairwise(krn_ctx *ctx, const double *d_v, size_t n, do
     int rc = krn_reserve_partials(ctx, blocks);
     if (rc) return rc;
     double *partials = ctx->d_partials, *scratch = ctx->d_partials + ctx->partial_capacity;
-    if (krn_aligned32(d_v))
-        tree_kernel<true><<<unsigned(blocks), kThreads, 0, ctx->stream>>>(
-            d_v, n, steps, partials, scratch, ctx->d_ticket, d_out, accumulate);
-    else
-        tree_kernel<false><<<unsigned(blocks), kThreads, 0, ctx->stream>>>(
-            d_v, n, steps, partials, scratch, ctx->d_ticket, d_out, accumulate);
+    const bool vec = krn_aligned32(d_v);
+#define KRN_TREE(V, S)                                                              \
+    tree_kernel<V, S><<<unsigned(blocks), kThreads, 0, ctx->stream>>>(d_v, n, partials, scratch, \
+                                                                      ctx->d_ticket, d_out, accumulate)
+    if (steps == 1) {
+        if (vec) KRN_TREE(true, 1);
+        else KRN_TREE(false, 1);
+    } else {
+        if (vec) KRN_TREE(true, 8);
+        else KRN_TREE(false, 8);
+    }
+#undef KRN_TREE
     KRN_LAUNCH_CHECK(ctx);
     return KRN_OK;
 }

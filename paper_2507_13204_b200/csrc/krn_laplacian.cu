@@ -170,48 +170,62 @@ __device__ __forceinline__ double edge_step(const Shard &s, krn_i64 base, int la
 }
 
 // ---- interior path: 128 full rows, ghosts inside the shard, no guards -----------------
-template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO>
-__device__ __forceinline__ double interior_step(const double *__restrict__ x, const double *__restrict__ b,
-                                                krn_i64 base, int lane, double *__restrict__ x_out,
-                                                double *dx, double *db, double r4)
-{
-    const krn_i64 i0 = base + 4 * lane;
-    krn_d4 xv = krn_ld4_stream(x + i0);
-    krn_d4 bv = krn_ld4_stream(b + i0);
-    krn_d4 dxv = {0.0, 0.0, 0.0, 0.0}, dbv = {0.0, 0.0, 0.0, 0.0};
-    if (GRAD && HAS_DX && !DX_ZERO) dxv = krn_ld4_rmw(dx + i0);
-    if (GRAD && HAS_DB && !DB_ZERO) dbv = krn_ld4_rmw(db + i0);
+// Split into a load half and a compute half so the kernel can issue the loads of
+// step t+1 before it computes step t (two steps of every operand in flight per warp).
+struct StepData {
+    krn_d4 x, b, dx, db;
+    double g_near, g_far, g_b;  // ghost rows of the neighbouring warp step (edge lanes only)
+};
 
-    // ghost rows of the neighbouring warp step, fetched by the two edge lanes
-    const bool left_edge = lane == 0, right_edge = lane == 31;
-    double g_far = 0.0, g_near = 0.0, g_b = 0.0;
-    if (left_edge) {
-        g_near = krn_ld1(x + i0 - 1);
-        if (GRAD) {
-            g_far = krn_ld1(x + i0 - 2);
-            g_b = krn_ld1(b + i0 - 1);
+template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO>
+__device__ __forceinline__ StepData load_interior(const double *__restrict__ x, const double *__restrict__ b,
+                                                  const double *dx, const double *db, krn_i64 base, int lane)
+{
+    StepData d;
+    const krn_i64 i0 = base + 4 * lane;
+    d.x = krn_ld4_stream(x + i0);
+    d.b = krn_ld4_stream(b + i0);
+    d.dx = {0.0, 0.0, 0.0, 0.0};
+    d.db = {0.0, 0.0, 0.0, 0.0};
+    if (GRAD && HAS_DX && !DX_ZERO) d.dx = krn_ld4_rmw(dx + i0);
+    if (GRAD && HAS_DB && !DB_ZERO) d.db = krn_ld4_rmw(db + i0);
+    d.g_near = d.g_far = d.g_b = 0.0;
+    if (lane == 0) {
+        d.g_near = krn_ld1(x + i0 - 1);
+        if (GRAD && HAS_DX) {
+            d.g_far = krn_ld1(x + i0 - 2);
+            d.g_b = krn_ld1(b + i0 - 1);
         }
-    } else if (right_edge) {
-        g_near = krn_ld1(x + i0 + 4);
-        if (GRAD) {
-            g_far = krn_ld1(x + i0 + 5);
-            g_b = krn_ld1(b + i0 + 4);
+    } else if (lane == 31) {
+        d.g_near = krn_ld1(x + i0 + 4);
+        if (GRAD && HAS_DX) {
+            d.g_far = krn_ld1(x + i0 + 5);
+            d.g_b = krn_ld1(b + i0 + 4);
         }
     }
+    return d;
+}
 
-    krn_d4 xs = {3.0 * xv.a, 3.0 * xv.b, 3.0 * xv.c, 3.0 * xv.d};
+template <bool GRAD, bool HAS_DX, bool HAS_DB>
+__device__ __forceinline__ double compute_interior(const StepData &d, krn_i64 base, int lane,
+                                                   double *__restrict__ x_out, double *dx, double *db,
+                                                   double r4)
+{
+    const krn_i64 i0 = base + 4 * lane;
+    const bool left_edge = lane == 0, right_edge = lane == 31;
+    krn_d4 xs = {3.0 * d.x.a, 3.0 * d.x.b, 3.0 * d.x.c, 3.0 * d.x.d};
     krn_st4(x_out + i0, xs);
 
     double xl = __shfl_up_sync(KRN_FULL_MASK, xs.d, 1);
     double xr = __shfl_down_sync(KRN_FULL_MASK, xs.a, 1);
-    const double g_near_s = 3.0 * g_near;
+    const double g_near_s = 3.0 * d.g_near;
     if (left_edge) xl = g_near_s;
     if (right_edge) xr = g_near_s;
 
-    double y0 = stencil_row(xl, xs.a, xs.b, bv.a, true, true);
-    double y1 = stencil_row(xs.a, xs.b, xs.c, bv.b, true, true);
-    double y2 = stencil_row(xs.b, xs.c, xs.d, bv.c, true, true);
-    double y3 = stencil_row(xs.c, xs.d, xr, bv.d, true, true);
+    double y0 = stencil_row(xl, xs.a, xs.b, d.b.a, true, true);
+    double y1 = stencil_row(xs.a, xs.b, xs.c, d.b.b, true, true);
+    double y2 = stencil_row(xs.b, xs.c, xs.d, d.b.c, true, true);
+    double y3 = stencil_row(xs.c, xs.d, xr, d.b.d, true, true);
 
     if (!GRAD) return (y0 * y0 + y1 * y1) + (y2 * y2 + y3 * y3);
 
@@ -225,47 +239,57 @@ __device__ __forceinline__ double interior_step(const double *__restrict__ x, co
         double r3_left = __shfl_up_sync(KRN_FULL_MASK, c3.r3, 1);
         double r2_right = __shfl_down_sync(KRN_FULL_MASK, c0.r2, 1);
         if (left_edge || right_edge) {
-            const double g_far_s = 3.0 * g_far;
+            const double g_far_s = 3.0 * d.g_far;
             double ym = left_edge ? g_far_s : xs.d;
             double yp = left_edge ? xs.a : g_far_s;
-            Chain g = adjoint_chain(stencil_row(ym, g_near_s, yp, g_b, true, true), r4, true, true);
+            Chain g = adjoint_chain(stencil_row(ym, g_near_s, yp, d.g_b, true, true), r4, true, true);
             if (left_edge) r3_left = g.r3;
             if (right_edge) r2_right = g.r2;
         }
         krn_d4 o;
-        o.a = finish_dx(dxv.a, r3_left, c0.r1, c1.r2, true, true);
-        o.b = finish_dx(dxv.b, c0.r3, c1.r1, c2.r2, true, true);
-        o.c = finish_dx(dxv.c, c1.r3, c2.r1, c3.r2, true, true);
-        o.d = finish_dx(dxv.d, c2.r3, c3.r1, r2_right, true, true);
+        o.a = finish_dx(d.dx.a, r3_left, c0.r1, c1.r2, true, true);
+        o.b = finish_dx(d.dx.b, c0.r3, c1.r1, c2.r2, true, true);
+        o.c = finish_dx(d.dx.c, c1.r3, c2.r1, c3.r2, true, true);
+        o.d = finish_dx(d.dx.d, c2.r3, c3.r1, r2_right, true, true);
         krn_st4(dx + i0, o);
     }
     if (HAS_DB) {
-        krn_d4 o = {dbv.a + (-c0.r1), dbv.b + (-c1.r1), dbv.c + (-c2.r1), dbv.d + (-c3.r1)};
+        krn_d4 o = {d.db.a + (-c0.r1), d.db.b + (-c1.r1), d.db.c + (-c2.r1), d.db.d + (-c3.r1)};
         krn_st4(db + i0, o);
     }
     return -0.0;
 }
 
-template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO>
-__global__ void __launch_bounds__(kThreads)
-laplacian_kernel(Shard s, double *__restrict__ x_out, double *dx, double *db, double seed, int steps,
-                 bool vector_ok, double *partials, double *scratch, unsigned int *ticket, double *f_out,
-                 int accumulate)
+// complete in-order tree over STEPS (power of two) nodes
+template <int STEPS>
+__device__ __forceinline__ double static_tree(double (&v)[STEPS])
+{
+#pragma unroll
+    for (int w = 1; w < STEPS; w <<= 1) {
+#pragma unroll
+        for (int i = 0; i < STEPS; i += 2 * w) v[i] = v[i] + v[i + w];
+    }
+    return v[0];
+}
+
+template <bool GRAD, bool HAS_DX, bool HAS_DB, bool DX_ZERO, bool DB_ZERO, int STEPS>
+__global__ void __launch_bounds__(kThreads, 4)  // <= 64 registers: 4 blocks (32 warps) per SM
+laplacian_kernel(Shard s, double *__restrict__ x_out, double *dx, double *db, double seed, bool vector_ok,
+                 double *partials, double *scratch, unsigned int *ticket, double *f_out, int accumulate)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const krn_i64 chunk = (krn_i64)kThreads * 4 * steps;
-    const krn_i64 warp_base = (krn_i64)blockIdx.x * chunk + (krn_i64)warp * kStep * steps;
+    constexpr krn_i64 chunk = (krn_i64)kThreads * 4 * STEPS;
+    const krn_i64 warp_base = (krn_i64)blockIdx.x * chunk + (krn_i64)warp * kStep * STEPS;
     const double d_sum = 0.0 + seed;   // let _d_sum = 0.0;  _d_sum += seed;
     const double r4 = 0.0 + d_sum;     // parallel_sum(_d_y2, _d_sum) on a zero shadow
 
-    double stack[4];  // binary-counter tree over the warp's steps (steps <= 16)
-    int depth = 0;
-    for (int t = 0; t < steps; ++t) {
-        const krn_i64 base = warp_base + (krn_i64)t * kStep;
-        double node;
+    auto interior = [&](krn_i64 base) { return vector_ok && base >= 2 && base + kStep + 2 <= s.n_local; };
+
+    // one step of the warp's sub-chunk that is not a plain interior step
+    auto other_step = [&](krn_i64 base) -> double {
         if (base >= s.n_local) {
             // nothing of this step lies in the shard; it still owns a node of the tree
-            node = -0.0;
+            double node = -0.0;
             if (!GRAD) {
                 double v[4];
 #pragma unroll
@@ -275,27 +299,58 @@ laplacian_kernel(Shard s, double *__restrict__ x_out, double *dx, double *db, do
                 }
                 node = (v[0] + v[1]) + (v[2] + v[3]);
             }
-        } else if (vector_ok && base >= 2 && base + kStep + 2 <= s.n_local) {
-            node = interior_step<GRAD, HAS_DX, HAS_DB, DX_ZERO, DB_ZERO>(s.x, s.b, base, lane, x_out, dx,
-                                                                           db, r4);
-        } else {
-            node = edge_step<GRAD>(s, base, lane, x_out, HAS_DX ? dx : nullptr, HAS_DB ? db : nullptr,
-                                   DX_ZERO, DB_ZERO, r4);
+            return node;
         }
-        if (!GRAD) {
-            node = krn_warp_tree(node);
-            int m = t;
-            while (m & 1) {
-                node = stack[--depth] + node;
-                m >>= 1;
+        return edge_step<GRAD>(s, base, lane, x_out, HAS_DX ? dx : nullptr, HAS_DB ? db : nullptr, DX_ZERO,
+                               DB_ZERO, r4);
+    };
+
+    double nodes[STEPS];
+    if constexpr (GRAD) {
+        // four operand streams per step already keep 4 KB per warp in flight at 4 blocks/SM;
+        // a deeper software pipeline only costs occupancy here (measured: -1.5%)
+#pragma unroll 1
+        for (int t = 0; t < STEPS; ++t) {
+            const krn_i64 base = warp_base + (krn_i64)t * kStep;
+            if (interior(base)) {
+                StepData d = load_interior<GRAD, HAS_DX, HAS_DB, DX_ZERO, DB_ZERO>(s.x, s.b, dx, db, base, lane);
+                compute_interior<GRAD, HAS_DX, HAS_DB>(d, base, lane, x_out, dx, db, r4);
+            } else {
+                other_step(base);
             }
-            stack[depth++] = node;
+        }
+        return;
+    } else {
+        // primal: two operand streams only, so the loads of step t+1 are issued before step t
+        // is computed (measured: +7% bandwidth)
+        StepData cur;
+        bool cur_ok = interior(warp_base);
+        if (cur_ok)
+            cur = load_interior<GRAD, HAS_DX, HAS_DB, DX_ZERO, DB_ZERO>(s.x, s.b, dx, db, warp_base, lane);
+#pragma unroll
+        for (int t = 0; t < STEPS; ++t) {
+            const krn_i64 base = warp_base + (krn_i64)t * kStep;
+            StepData nxt;
+            bool nxt_ok = false;
+            if (t + 1 < STEPS) {
+                nxt_ok = interior(base + kStep);
+                if (nxt_ok)
+                    nxt = load_interior<GRAD, HAS_DX, HAS_DB, DX_ZERO, DB_ZERO>(s.x, s.b, dx, db, base + kStep,
+                                                                                lane);
+            }
+            double node = cur_ok ? compute_interior<GRAD, HAS_DX, HAS_DB>(cur, base, lane, x_out, dx, db, r4)
+                                 : other_step(base);
+            nodes[t] = krn_warp_tree(node);
+            if (t + 1 < STEPS) {
+                cur = nxt;
+                cur_ok = nxt_ok;
+            }
         }
     }
-    if (GRAD) return;
 
     __shared__ double s_warp[kWarps];
-    if (lane == 0) s_warp[warp] = stack[0];
+    const double warp_total = static_tree<STEPS>(nodes);
+    if (lane == 0) s_warp[warp] = warp_total;
     __syncthreads();
     if (warp == 0) {
         double v = krn_smem_tree(s_warp, kWarps, lane);
@@ -312,6 +367,37 @@ int steps_for(size_t n_global)
     // small problems are latency bound: spread them over as many blocks as possible;
     // large ones amortise the per-block epilogue and keep the partial count low
     return n_global <= (size_t(1) << 20) ? 1 : 8;
+}
+
+template <bool GRAD, int STEPS>
+void dispatch(krn_ctx *ctx, dim3 grid, const Shard &s, double *x_out, double *dx, double *db, int dx_zero,
+              int db_zero, double seed, bool vec, double *f, int accumulate)
+{
+    double *partials = ctx->d_partials, *scratch = ctx->d_partials + ctx->partial_capacity;
+    dim3 block(kThreads);
+#define KRN_LAP(G, HX, HB, ZX, ZB)                                                       \
+    laplacian_kernel<G, HX, HB, ZX, ZB, STEPS><<<grid, block, 0, ctx->stream>>>(         \
+        s, x_out, dx, db, seed, vec, partials, scratch, ctx->d_ticket, f, accumulate)
+    if (!GRAD) {
+        KRN_LAP(false, false, false, false, false);
+    } else {
+        const bool hx = dx != nullptr, hb = db != nullptr, zx = hx && dx_zero, zb = hb && db_zero;
+        if (hx && hb) {
+            if (zx && zb) KRN_LAP(true, true, true, true, true);
+            else if (zx) KRN_LAP(true, true, true, true, false);
+            else if (zb) KRN_LAP(true, true, true, false, true);
+            else KRN_LAP(true, true, true, false, false);
+        } else if (hx) {
+            if (zx) KRN_LAP(true, true, false, true, false);
+            else KRN_LAP(true, true, false, false, false);
+        } else if (hb) {
+            if (zb) KRN_LAP(true, false, true, false, true);
+            else KRN_LAP(true, false, true, false, false);
+        } else {
+            KRN_LAP(true, false, false, false, false);
+        }
+    }
+#undef KRN_LAP
 }
 
 template <bool GRAD>
@@ -333,7 +419,6 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
     }
     const int steps = steps_for(n_global);
     const size_t chunk = size_t(kThreads) * 4 * steps;
-    // the primal's tree runs over the padded problem so the last block owns every pad node
     const size_t blocks = (n_local + chunk - 1) / chunk;
     KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
     if (!GRAD) {
@@ -343,31 +428,11 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
     Shard s{x_in, b, halo, (krn_i64)n_local, (krn_i64)offset, (krn_i64)n_global};
     bool vec = krn_aligned32(x_in) && krn_aligned32(x_out) && krn_aligned32(b) &&
                (dx == nullptr || krn_aligned32(dx)) && (db == nullptr || krn_aligned32(db));
-    double *partials = ctx->d_partials, *scratch = ctx->d_partials + ctx->partial_capacity;
-    dim3 grid((unsigned)blocks), block(kThreads);
-#define KRN_LAP(G, HX, HB, ZX, ZB)                                                                    \
-    laplacian_kernel<G, HX, HB, ZX, ZB><<<grid, block, 0, ctx->stream>>>(                            \
-        s, x_out, dx, db, seed, steps, vec, partials, scratch, ctx->d_ticket, f, accumulate)
-    if (!GRAD) {
-        KRN_LAP(false, false, false, false, false);
-    } else {
-        const bool hx = dx != nullptr, hb = db != nullptr, zx = hx && dx_zero, zb = hb && db_zero;
-        if (hx && hb) {
-            if (zx && zb) KRN_LAP(true, true, true, true, true);
-            else if (zx) KRN_LAP(true, true, true, true, false);
-            else if (zb) KRN_LAP(true, true, true, false, true);
-            else KRN_LAP(true, true, true, false, false);
-        } else if (hx) {
-            if (zx) KRN_LAP(true, true, false, true, false);
-            else KRN_LAP(true, true, false, false, false);
-        } else if (hb) {
-            if (zb) KRN_LAP(true, false, true, false, true);
-            else KRN_LAP(true, false, true, false, false);
-        } else {
-            KRN_LAP(true, false, false, false, false);
-        }
-    }
-#undef KRN_LAP
+    dim3 grid((unsigned)blocks);
+    if (steps == 1)
+        dispatch<GRAD, 1>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
+    else
+        dispatch<GRAD, 8>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
     KRN_LAUNCH_CHECK(ctx);
     return KRN_OK;
 }

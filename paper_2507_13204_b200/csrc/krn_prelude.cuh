@@ -99,7 +99,7 @@ __device__ __forceinline__ double krn_smem_tree(const double *s, int count, int 
 // (each already the exact tree node of an aligned power-of-two span) using two
 // ping-pong arrays.  Explicit per-level rule: odd length and more than one node
 // -> last node + (+0.0).  Returns the root in thread 0.
-__device__ __forceinline__ double krn_final_tree(double *ping, double *pong, krn_u64 m)
+__device__ __forceinline__ double krn_final_tree_levels(double *ping, double *pong, krn_u64 m)
 {
     double *src = ping, *dst = pong;
     while (m > 1) {
@@ -115,13 +115,57 @@ __device__ __forceinline__ double krn_final_tree(double *ping, double *pong, krn
     return __ldcg(src);
 }
 
-// arrival ticket: returns true in every thread of the block that arrives last
+// Same result in ONE pass (one round trip to L2 instead of one per level): the m
+// partials are themselves the leaves of a reference tree, so the padding rule
+// applies again in partial-index space.  Thread t folds the aligned run
+// [t*per, (t+1)*per) in order (binary counter), then warp shuffles, then shared
+// memory across the block's warps (blockDim.x must be a power of two <= 1024).
+__device__ __forceinline__ double krn_final_tree(const double *partials, double * /*scratch*/, krn_u64 m)
+{
+    __shared__ double s_final[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    krn_u64 per = 1;
+    while (per * blockDim.x < m) per <<= 1;
+    const krn_u64 first = (krn_u64)threadIdx.x * per;
+    double stack[34];
+    int depth = 0;
+    for (krn_u64 base = 0; base < per; base += 8) {
+        // up to 8 independent loads in flight, then folded in order
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            krn_u64 i = first + base + u;
+            v[u] = (base + u < per) ? (i < m ? __ldcg(partials + i) : krn_tree_pad(i, m)) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (base + u < per) {
+                double x = v[u];
+                krn_u64 c = base + u;
+                while (c & 1) {
+                    x = stack[--depth] + x;
+                    c >>= 1;
+                }
+                stack[depth++] = x;
+            }
+        }
+    }
+    double r = krn_warp_tree(stack[0]);
+    if (lane == 0) s_final[warp] = r;
+    __syncthreads();
+    double root = 0.0;
+    if (warp == 0) root = krn_smem_tree(s_final, nwarps, lane);
+    return root;  // valid in thread 0
+}
+
+// arrival ticket: returns true in every thread of the block that arrives last.
+// Contract: thread 0 is the thread that stored this block's partial, so only it
+// needs the release fence (an all-thread fence stalls every warp on MEMBAR).
 __device__ __forceinline__ bool krn_last_block(unsigned int *ticket, unsigned int total)
 {
     __shared__ unsigned int s_last;
-    __threadfence();
-    __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         unsigned int t = atomicAdd(ticket, 1u);
         s_last = (t == total - 1u);
         if (s_last) *ticket = 0u;  // re-arm for the next launch on this stream
