@@ -81,6 +81,18 @@ int krn_event_destroy(void *event);
 int krn_event_record(krn_ctx *ctx, void *event);
 int krn_event_elapsed_ms(void *start, void *stop, float *ms);   /* synchronous on stop */
 
+/* ---- auxiliary copy streams: overlap host<->device transfers of one chunk of
+ *      rows with the kernels of another (the host-buffer path of execute();
+ *      the reference has no counterpart, its Views are host arrays) ------------- */
+int krn_stream_create(krn_ctx *ctx, void **stream);
+int krn_stream_destroy(void *stream);
+int krn_stream_sync(void *stream);                                   /* synchronous */
+int krn_upload_on(void *stream, void *d_dst, const void *h_src, size_t bytes);
+int krn_download_on(void *stream, void *h_dst, const void *d_src, size_t bytes);
+int krn_event_record_on(void *stream, void *event);
+int krn_stream_wait_event(void *stream, void *event);
+int krn_ctx_wait_event(krn_ctx *ctx, void *event);   /* the context's stream waits */
+
 /* ---- bulk builtins --------------------------------------------------------- */
 
 /* deep_copy(dst, scalar) and DeclView zero-fill   (runtime.py:637-639, 523-535); the

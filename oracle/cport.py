@@ -24,6 +24,7 @@ def lib():
         L.krn_oracle_laplacian_primal.argtypes = [_dp, _dp, C.c_size_t, _dp]
         L.krn_oracle_laplacian_grad.restype = None
         L.krn_oracle_laplacian_grad.argtypes = [_dp, _dp, _dp, _dp, C.c_size_t, C.c_double, _dp]
+        L.krn_oracle_threads.restype = C.c_int
         _lib = L
     return _lib
 
@@ -49,3 +50,8 @@ def laplacian_grad(x, b, dx, db, seed: float = 1.0) -> None:
     """Accumulates into dx, db; x scaled in place."""
     work = np.empty(5 * x.size + 1)
     lib().krn_oracle_laplacian_grad(_p(x), _p(b), _p(dx), _p(db), x.size, seed, _p(work))
+
+
+def threads() -> int:
+    """OpenMP threads the order-free loops of the C port use."""
+    return int(lib().krn_oracle_threads())

@@ -12,7 +12,7 @@
  * in the build container, see oracle/make_golden.py) and the reference's
  * known-answer tests.
  *
- * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC  (oracle/build.py)
+ * Build: gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math -shared -fPIC  (oracle/build.py)
  * -ffp-contract=off matters: the reference contract is IEEE double with no
  * fused multiply-add.
  *
@@ -29,6 +29,15 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#define KRN_OMP_FOR _Pragma("omp parallel for schedule(static) if (n > 65536)")
+int krn_oracle_threads(void) { return omp_get_max_threads(); }
+#else
+#define KRN_OMP_FOR
+int krn_oracle_threads(void) { return 1; }
+#endif
 
 /* ---- bulk builtins ------------------------------------------------------ */
 
@@ -60,7 +69,11 @@ void krn_oracle_add_view(double *dst, const double *src, size_t n) { for (size_t
  * way DeclView does).  x is scaled in place. */
 static void laplacian_forward(double *x, const double *b, double *y, double *y2, size_t n)
 {
+    /* iterations of a parallel_for are independent: the reference runs them on a thread
+     * pool (runtime.py:594-613); here OpenMP plays that role for the order-free loops */
+    KRN_OMP_FOR
     for (size_t j0 = 0; j0 < n; ++j0) x[j0] = 3.0 * x[j0];
+    KRN_OMP_FOR
     for (size_t j = 0; j < n; ++j) {
         y[j] = 2.0 * x[j] - b[j];
         if (j != 0)     y[j] -= x[j - 1];
@@ -87,7 +100,8 @@ double krn_oracle_laplacian_primal(double *x, const double *b, size_t n, double 
  * the reverse stencil kernel are applied by a sequential ascending-j loop,
  * which is exactly the (iteration, program-order) order the reference sorts
  * into; nothing in that kernel reads _d_x, so immediate application is
- * indistinguishable from deferred. */
+ * indistinguishable from deferred.  That loop (and the pairwise tree) stay
+ * sequential: their order IS the result.  The order-free loops use OpenMP. */
 void krn_oracle_laplacian_grad(double *x, const double *b, double *dx, double *db,
                                size_t n, double seed, double *work)
 {
@@ -99,6 +113,7 @@ void krn_oracle_laplacian_grad(double *x, const double *b, double *dx, double *d
     double sum = 0.0 + krn_oracle_pairwise_sum(y2, n, scratch); /* dead, kept: the forward is verbatim */
     (void)sum;
     d_sum += seed;
+    KRN_OMP_FOR
     for (size_t j = 0; j < n; ++j) d_y2[j] += d_sum;  /* parallel_sum(_d_y2, _d_sum) */
 
     for (size_t j = 0; j < n; ++j) {                  /* reverse of the stencil kernel */
@@ -123,6 +138,7 @@ void krn_oracle_laplacian_grad(double *x, const double *b, double *dx, double *d
         dx[j] += 2.0 * r1;                            /* atomic_add(_d_x(j), 2.0 * _r_d1) */
         db[j] += -r1;
     }
+    KRN_OMP_FOR
     for (size_t j0 = 0; j0 < n; ++j0) {               /* reverse of the scale kernel */
         double r0 = dx[j0];
         dx[j0] -= r0;

@@ -50,6 +50,14 @@ SIGNATURES = {
     "krn_event_destroy": (_i, [_vp]),
     "krn_event_record": (_i, [_vp, _vp]),
     "krn_event_elapsed_ms": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
+    "krn_stream_create": (_i, [_vp, _pp]),
+    "krn_stream_destroy": (_i, [_vp]),
+    "krn_stream_sync": (_i, [_vp]),
+    "krn_upload_on": (_i, [_vp, _vp, _vp, _sz]),
+    "krn_download_on": (_i, [_vp, _vp, _vp, _sz]),
+    "krn_event_record_on": (_i, [_vp, _vp]),
+    "krn_stream_wait_event": (_i, [_vp, _vp]),
+    "krn_ctx_wait_event": (_i, [_vp, _vp]),
     "krn_fill": (_i, [_vp, _dp, _sz, _d, _dp]),
     "krn_copy": (_i, [_vp, _dp, _dp, _sz]),
     "krn_add_scalar": (_i, [_vp, _dp, _sz, _d, _dp]),

@@ -209,6 +209,68 @@ extern "C" int krn_event_elapsed_ms(void *start, void *stop, float *ms)
     return KRN_OK;
 }
 
+// ---- auxiliary copy streams ------------------------------------------------------------
+
+extern "C" int krn_stream_create(krn_ctx *ctx, void **stream)
+{
+    KRN_REQUIRE(ctx && stream, "null argument");
+    KRN_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t s;
+    KRN_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream = s;
+    return KRN_OK;
+}
+
+extern "C" int krn_stream_destroy(void *stream)
+{
+    if (stream) KRN_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+    return KRN_OK;
+}
+
+extern "C" int krn_stream_sync(void *stream)
+{
+    KRN_REQUIRE(stream != nullptr, "null stream");
+    KRN_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return KRN_OK;
+}
+
+extern "C" int krn_upload_on(void *stream, void *d_dst, const void *h_src, size_t bytes)
+{
+    if (bytes == 0) return KRN_OK;
+    KRN_REQUIRE(stream && d_dst && h_src, "null argument");
+    KRN_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)));
+    return KRN_OK;
+}
+
+extern "C" int krn_download_on(void *stream, void *h_dst, const void *d_src, size_t bytes)
+{
+    if (bytes == 0) return KRN_OK;
+    KRN_REQUIRE(stream && h_dst && d_src, "null argument");
+    KRN_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+    return KRN_OK;
+}
+
+extern "C" int krn_event_record_on(void *stream, void *event)
+{
+    KRN_REQUIRE(stream && event, "null argument");
+    KRN_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)));
+    return KRN_OK;
+}
+
+extern "C" int krn_stream_wait_event(void *stream, void *event)
+{
+    KRN_REQUIRE(stream && event, "null argument");
+    KRN_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0));
+    return KRN_OK;
+}
+
+extern "C" int krn_ctx_wait_event(krn_ctx *ctx, void *event)
+{
+    KRN_REQUIRE(ctx && event, "null argument");
+    KRN_CUDA(cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(event), 0));
+    return KRN_OK;
+}
+
 // ---- status word ---------------------------------------------------------------------
 
 extern "C" int krn_status_reset(krn_ctx *ctx)

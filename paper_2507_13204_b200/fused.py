@@ -124,33 +124,39 @@ class _Bound:
         objs = [id(views[name]) for name in self.roles.values()]
         return len(set(objs)) == len(objs)
 
-    def run(self, dev, views, scalars, synchronous=True):
+    # rows per chunk of the pipelined host path: 4 Mi rows = 32 MB per View and chunk,
+    # ~0.6 ms of PCIe time, large against launch/event overheads, small against the whole
+    STREAM_CHUNK = 1 << 22
+    STREAM_MIN_ROWS = 1 << 23
+
+    def run(self, dev, views, scalars, cfg=None):
         from .runtime import _DeviceBuffer
 
+        synchronous = True if cfg is None else cfg.synchronous
         lib = dev.lib
         x, b = views[self.roles["x"]], views[self.roles["b"]]
         n = x.extents[0]
         if n == 0:
             return None if self.m.grad else 0.0
+        if (self.m.grad and synchronous and cfg is not None and cfg.stream_host_io
+                and n >= self.STREAM_MIN_ROWS and not x._dev_ok and not b._dev_ok):
+            return self.run_streamed(dev, views)
         x_in = x.device_ptr(dev, write=False)
         b_ptr = b.device_ptr(dev, write=False)
         x_out = _DeviceBuffer(dev, x.nbytes)
         if not self.m.grad:
-            f = dev.alloc(8)
-            try:
-                _cabi.check(lib.krn_laplacian_primal(dev.h, C.c_void_p(x_in), C.c_void_p(x_out.ptr),
-                                                     C.c_void_p(b_ptr), n, 0, n, None, C.c_void_p(f), 0))
-                x._adopt(x_out)
-                out = dev.staging[64:72].view("float64")
-                if not synchronous:
-                    dev.download_async(out, f)
-                    return None
-                dev.download(out, f)
-                return float(out[0])
-            finally:
-                dev.free(f)
-        dx = views.get(self.roles.get("dx")) if "dx" in self.roles else None
-        db = views.get(self.roles.get("db")) if "db" in self.roles else None
+            # the last block stores the objective straight into page-locked host memory
+            # (UVA: the pinned staging block is device-addressable): no result buffer, no
+            # separate D2H copy on the latency-bound path
+            f = dev._pinned.value + 64
+            _cabi.check(lib.krn_laplacian_primal(dev.h, C.c_void_p(x_in), C.c_void_p(x_out.ptr),
+                                                 C.c_void_p(b_ptr), n, 0, n, None, C.c_void_p(f), 0))
+            x._adopt(x_out)
+            if not synchronous:
+                return None
+            dev.sync()
+            return float(dev.staging[64:72].view("float64")[0])
+        dx, db = self._shadows(views)
         dx_zero = bool(dx is not None and dx._zero)
         db_zero = bool(db is not None and db._zero)
         dx_ptr = dx.device_ptr(dev, discard=dx_zero) if dx is not None else 0
@@ -161,6 +167,99 @@ class _Bound:
         x._adopt(x_out)
         if synchronous:
             dev.sync()
+        return None
+
+    def _shadows(self, views):
+        dx = views[self.roles["dx"]] if "dx" in self.roles else None
+        db = views[self.roles["db"]] if "db" in self.roles else None
+        return dx, db
+
+    def run_streamed(self, dev, views):
+        """Gradient with HOST-resident inputs: rows are cut into chunks; the upload of
+        chunk c+1, the kernel of chunk c and the download of the shadows of chunk c-1
+        run concurrently on three streams (PCIe is full duplex), so the call costs about
+        max(H2D, D2H) instead of H2D + kernel + D2H.  Each chunk is a shard of the
+        problem (csrc/krn_laplacian.cu); its halo rows come from the host arrays, packed
+        once.  Afterwards the Views are resident in HBM *and* the shadows' host arrays
+        are current."""
+        import numpy as np
+
+        from .runtime import _DeviceBuffer, pinned_array
+
+        lib = dev.lib
+        x, b = views[self.roles["x"]], views[self.roles["b"]]
+        dx, db = self._shadows(views)
+        n = x.extents[0]
+        hx, hb = x.peek(), b.peek()
+        chunk = self.STREAM_CHUNK
+        cuts = list(range(0, n, chunk)) + [n]
+        nch = len(cuts) - 1
+        # halo rows of every chunk, from the host copies (zeros where outside the problem)
+        halos = dev.pinned_scratch(6 * nch)
+        halos[:] = 0.0
+        h = halos.reshape(nch, 6)
+        for c in range(nch):
+            lo, hi = cuts[c], cuts[c + 1]
+            if lo >= 2:
+                h[c, 0:2] = hx[lo - 2:lo]
+            elif lo == 1:
+                h[c, 1] = hx[0]
+            if lo >= 1:
+                h[c, 2] = hb[lo - 1]
+            m = min(2, n - hi)
+            if m > 0:
+                h[c, 3:3 + m] = hx[hi:hi + m]
+                h[c, 5] = hb[hi]
+        bufs = {k: _DeviceBuffer(dev, 8 * n) for k in ("x", "xo", "b")}
+        d_halo = _DeviceBuffer(dev, 8 * 6 * nch)
+        shadows = []
+        for v in (dx, db):
+            if v is None:
+                shadows.append(None)
+                continue
+            zero = bool(v._zero)
+            if v._host is None:
+                v._host = pinned_array(v.extents)
+            buf = _DeviceBuffer(dev, 8 * n) if (v._dev is None or v._dev.dev is not dev) else v._dev
+            need_upload = (not zero) and not v._dev_ok
+            shadows.append((v, buf, zero, need_upload))
+        s_in, s_out = dev.aux_stream("in"), dev.aux_stream("out")
+        ev = dev.event_pool(2 * nch + 1)
+        P = C.c_void_p
+        _cabi.check(lib.krn_upload_on(s_in, P(d_halo.ptr), P(halos.ctypes.data), halos.nbytes))
+        # allocations above were made on the context's stream: let the copy streams see them
+        dev.record(ev[2 * nch])
+        _cabi.check(lib.krn_stream_wait_event(s_in, P(ev[2 * nch])))
+        _cabi.check(lib.krn_stream_wait_event(s_out, P(ev[2 * nch])))
+        for c in range(nch):
+            lo, hi = cuts[c], cuts[c + 1]
+            off, nb = 8 * lo, 8 * (hi - lo)
+            _cabi.check(lib.krn_upload_on(s_in, P(bufs["x"].ptr + off), P(hx.ctypes.data + off), nb))
+            _cabi.check(lib.krn_upload_on(s_in, P(bufs["b"].ptr + off), P(hb.ctypes.data + off), nb))
+            for sh in shadows:
+                if sh is not None and sh[3]:
+                    _cabi.check(lib.krn_upload_on(s_in, P(sh[1].ptr + off), P(sh[0]._host.ctypes.data + off), nb))
+            _cabi.check(lib.krn_event_record_on(s_in, P(ev[2 * c])))
+            _cabi.check(lib.krn_ctx_wait_event(dev.h, P(ev[2 * c])))
+            sx, sb = shadows
+            _cabi.check(lib.krn_laplacian_grad(
+                dev.h, P(bufs["x"].ptr + off), P(bufs["xo"].ptr + off), P(bufs["b"].ptr + off),
+                P(sx[1].ptr + off) if sx else None, P(sb[1].ptr + off) if sb else None,
+                int(sx[2]) if sx else 0, int(sb[2]) if sb else 0,
+                hi - lo, lo, n, P(d_halo.ptr + 48 * c), float(self.m.seed)))
+            dev.record(ev[2 * c + 1])
+            _cabi.check(lib.krn_stream_wait_event(s_out, P(ev[2 * c + 1])))
+            for sh in shadows:
+                if sh is not None:
+                    _cabi.check(lib.krn_download_on(s_out, P(sh[0]._host.ctypes.data + off), P(sh[1].ptr + off), nb))
+        _cabi.check(lib.krn_stream_sync(s_out))
+        dev.sync()
+        x._adopt(bufs["xo"])
+        b._dev, b._dev_ok = bufs["b"], True
+        for sh in shadows:
+            if sh is not None:
+                v, buf = sh[0], sh[1]
+                v._dev, v._dev_ok, v._host_ok, v._zero = buf, True, True, False
         return None
 
 

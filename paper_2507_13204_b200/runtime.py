@@ -122,6 +122,27 @@ class Device:
         _cabi.check(self.lib.krn_ctx_sm_count(self.h, C.byref(n)))
         return n.value
 
+    # auxiliary streams / scratch for the pipelined host path --------------------
+    def aux_stream(self, name: str):
+        streams = self.__dict__.setdefault("_aux_streams", {})
+        if name not in streams:
+            s = C.c_void_p()
+            _cabi.check(self.lib.krn_stream_create(self.h, C.byref(s)))
+            streams[name] = s
+        return streams[name]
+
+    def event_pool(self, count: int) -> list:
+        pool = self.__dict__.setdefault("_event_pool", [])
+        while len(pool) < count:
+            pool.append(self.event())
+        return pool[:count]
+
+    def pinned_scratch(self, count: int) -> np.ndarray:
+        cur = self.__dict__.get("_pinned_scratch")
+        if cur is None or cur.size < count:
+            cur = self.__dict__["_pinned_scratch"] = pinned_array((max(count, 1024),))
+        return cur[:count]
+
     # events ------------------------------------------------------------------
     def event(self) -> int:
         e = C.c_void_p()
@@ -264,10 +285,18 @@ class ViewStorage:
         return cls(ViewDescriptor(name, rank=arr.ndim), arr)
 
     @classmethod
-    def pinned(cls, name: str, extents) -> "ViewStorage":
+    def pinned(cls, name: str, extents, zero: bool = False) -> "ViewStorage":
         """A View whose host array lives in page-locked memory (zero filled), so
-        host<->device copies run at full PCIe speed and asynchronously."""
-        return cls(ViewDescriptor(name, rank=len(tuple(extents))), pinned_array(extents))
+        host<->device copies run at full PCIe speed and asynchronously.  ``zero=True``
+        additionally records the zeros provenance (like ``ViewStorage.zeros``): kernels
+        that can exploit a known-zero shadow skip its upload and its read."""
+        self = cls(ViewDescriptor(name, rank=len(tuple(extents))), pinned_array(extents))
+        self._zero = bool(zero)
+        return self
+
+    def mark_zero(self):
+        """Declare that the host array has been refilled with +0.0 by the caller."""
+        self._host_ok, self._dev_ok, self._zero = True, False, True
 
     def copy(self) -> "ViewStorage":
         out = ViewStorage._blank(self.descriptor.name, self._shape)
@@ -385,6 +414,9 @@ class ExecutionConfig:
     # False: enqueue only (no host sync, no status check, value not fetched); for timing
     # the launch sequence with events.  The reference contract is synchronous.
     synchronous: bool = True
+    # True: when the Views of a recognised gradient call live on the host, cut the rows into
+    # chunks and overlap upload / kernel / download of the shadows (fused.run_streamed)
+    stream_host_io: bool = False
 
     def __post_init__(self):
         if self.threads < 1:
@@ -740,7 +772,7 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
     if cfg.policy == "fused" and not cfg.check_finite:
         hit = fused.match(fn)
         if hit is not None and hit.applicable(views):
-            return ExecResult(hit.run(dev, views, scalars, cfg.synchronous))
+            return ExecResult(hit.run(dev, views, scalars, cfg))
     plan = _plan_for(fn)
     return ExecResult(_Run(dev, plan, views, scalars, cfg).go())
 
