@@ -143,12 +143,14 @@ def plan_atomics(loop) -> list:
 _PREAMBLE = r"""
 #include "krn_prelude.cuh"
 #define NV %(nv)d
+#define NH %(nh)d
 struct Env {
     double *v[NV > 0 ? NV : 1];
     krn_i64 e0[NV > 0 ? NV : 1];
     krn_i64 e1[NV > 0 ? NV : 1];
-    double *S;
+    double *S;          // function-scope scalars that live on the device (gather results, ...)
     krn_i64 *status;
+    double H[NH > 0 ? NH : 1];  // function-scope scalars the host knows, passed by value
 };
 // bounds-checked linear offsets; on failure record {code,line,view,i,j} and flag the iteration
 __device__ __forceinline__ krn_i64 off1(const Env &E, int v, krn_i64 i, int line, bool &bad)
@@ -193,8 +195,11 @@ class ModuleBuilder:
     """Generates the CUDA source of one function and the launch recipes the
     executor needs (kernel names, staging requirements)."""
 
-    def __init__(self, fn):
+    def __init__(self, fn, host_scalars=()):
         self.fn = fn
+        self.host_scalars = set(host_scalars)
+        self.hslots: dict = {}  # host-known scalar -> slot in Env.H
+        self.promoted: dict = {}  # view -> register array name, while a tile kernel is generated
         self.views: list = []  # view table: name -> index
         self.rank: dict = {}
         self.slots: dict = {}  # function-scope scalar -> slot in S
@@ -222,6 +227,17 @@ class ModuleBuilder:
             self.slots[name] = len(self.slots)
         return self.slots[name]
 
+    def hslot(self, name) -> int:
+        if name not in self.hslots:
+            self.hslots[name] = len(self.hslots)
+        return self.hslots[name]
+
+    def _reg(self, acc):
+        """Register holding acc's element when its view is promoted in the tile kernel
+        being generated (pointwise access by construction)."""
+        r = self.promoted.get(acc.view)
+        return f"{r}[e]" if r is not None else None
+
     # ---- expressions -----------------------------------------------------------
 
     def index(self, e, local) -> str:
@@ -248,6 +264,9 @@ class ModuleBuilder:
         return f"off2(E, {v}, {idx[0]}, {idx[1]}, {line}, bad)"
 
     def load(self, acc, local) -> str:
+        reg = self._reg(acc)
+        if reg is not None:
+            return reg
         # the offset expression may set `bad`; rd() then yields 0.0 without touching memory
         return f"krn_seq_rd(E, {self.vid(acc.view)}, {self.offset(acc, local)}, bad)"
 
@@ -258,6 +277,8 @@ class ModuleBuilder:
         if k == "ScalarVar":
             if e.name in local:
                 return f"L_{e.name}"
+            if e.name in self.host_scalars:
+                return f"E.H[{self.hslot(e.name)}]"
             return f"E.S[{self.slot(e.name)}]"
         if k == "IndexVar":
             return "((double)i)"
@@ -296,6 +317,10 @@ class ModuleBuilder:
             rhs = self.value(s.rhs, local)
             expr = {"=": "t_", "+=": f"{tgt} + t_", "-=": f"{tgt} - t_"}[s.op]
             out.append(f"{pad}{{ double t_ = {rhs}; if (bad) {stop} {tgt} = {expr}; }}")
+        elif k == "AssignView" and self._reg(s.target) is not None:
+            reg = self._reg(s.target)
+            expr = {"=": "t_", "+=": f"{reg} + t_", "-=": f"{reg} - t_"}[s.op]
+            out.append(f"{pad}{{ double t_ = {self.value(s.rhs, local)}; if (bad) {stop} {reg} = {expr}; }}")
         elif k == "AssignView":
             v = self.vid(s.target.view)
             expr = {"=": "t_", "+=": f"E.v[{v}][o_] + t_", "-=": f"E.v[{v}][o_] - t_"}[s.op]
@@ -310,6 +335,8 @@ class ModuleBuilder:
             site = sites.get(id(s)) if sites else None
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
+            elif site.mode == "gather" and self.promoted:
+                out.append(head + f"T{site.index}[e] = t_; }}")  # tile kernel: staging column in registers
             elif site.mode == "gather":
                 out.append(head + f"stage[{site.index} * n + i] = t_; }}")
             elif site.mode == "staged_atomic":
@@ -443,7 +470,7 @@ class ModuleBuilder:
         return dict(name=name, slot=slot)
 
     def source(self) -> str:
-        head = _PREAMBLE % dict(nv=len(self.views))
+        head = _PREAMBLE % dict(nv=len(self.views), nh=len(self.hslots))
         head += (
             "__device__ __forceinline__ double krn_seq_rd(const Env &E, int v, krn_i64 off, bool &bad)\n"
             "{ return rd(E, v, off, bad); }\n"

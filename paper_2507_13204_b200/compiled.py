@@ -1,0 +1,429 @@
+"""Execution of a function through the fusion pass (policy "fused" for anything
+that is not the hand-written headline, and policy "compiled" for everything).
+
+Plan = schedule of fused groups (tile kernels, tilegen.py) interleaved with the
+statements the pass leaves alone (library builtins, unfused generated kernels).
+Before anything is launched the run is checked *dry* on the host - all extents are
+host data - and if a fused group could not honour the reference's error semantics
+(an access that would be out of bounds, mismatching extents of a bulk statement)
+the whole call is handed to the statement path, which raises exactly where the
+reference does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+
+import numpy as np
+
+from . import _cabi, codegen, fusion, tilegen
+from .lang import nodes as N
+from .lang.nodes import kind, walk_expr, walk_statements
+
+
+def _views_in_stmts(stmts) -> set:
+    out = set()
+    for s in walk_statements(stmts):
+        k = kind(s)
+        if k in ("DeepCopy", "ParallelSumInto"):
+            out.add(s.dst)
+            if isinstance(s.src, str):
+                out.add(s.src)
+        elif k == "ParallelSum":
+            out.add(s.src)
+        for e in N.statement_exprs(s):
+            for n in walk_expr(e):
+                if kind(n) in ("ViewAccess", "Extent"):
+                    out.add(n.view)
+    return out
+
+
+def _views_of(item) -> set:
+    tag = item[0]
+    if tag == "group":
+        g = item[1]
+        out = set()
+        for loop in g.ops:
+            if loop.what == "apply":
+                out.add(loop.apply_of[0])
+            else:
+                out |= _views_in_stmts(loop.body)
+        if g.gather is not None:
+            out.add(g.gather[0].src)
+        return out
+    if tag == "gather":
+        return {item[1].src}
+    if tag == "scalars":
+        return _views_in_stmts(item[1])
+    if tag == "raw":
+        return _views_in_stmts([item[1]])
+    if tag == "return":
+        return {n.view for n in walk_expr(item[1]) if kind(n) in ("ViewAccess", "Extent")}
+    return set()
+
+
+def _host_evaluable(e, host_scalars) -> bool:
+    for n in walk_expr(e):
+        k = kind(n)
+        if k == "ViewAccess" or k == "IndexVar" or (k == "ScalarVar" and n.name not in host_scalars):
+            return False
+    return True
+
+
+class CompiledPlan:
+    def __init__(self, fn):
+        self.fn = fn
+        an = self.an = fusion.Analysis(fn)
+        self.schedule = fusion.form_groups(fusion.build_ops(fn, an), an)
+        b = self.builder = codegen.ModuleBuilder(fn, host_scalars=an.host_scalars)
+        params = {p.name for p in fn.params if p.is_view}
+        self.steps: list = []
+        bound = set()
+        for idx, item in enumerate(self.schedule):
+            tag = item[0]
+            if tag == "group":
+                later = set(params)
+                for nxt in self.schedule[idx + 1:]:
+                    later |= _views_of(nxt)
+                plan = tilegen.plan_group(b, item[1], an, later)
+                self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan)))
+            elif tag == "raw":
+                s = item[1]
+                if kind(s) == "ParallelFor":
+                    self.steps.append(("kernel", s, b.kernel(s, f"k{idx}")))
+                else:
+                    self.steps.append(("deepcopy" if kind(s) == "DeepCopy" else "suminto", s))
+            elif tag == "gather":
+                b.slot(item[1].dst)
+                self.steps.append(("gather", item[1], item[2]))
+            elif tag == "scalars":
+                self.steps.append(("scalars", b.scalar_block(item[1], f"s{idx}")))
+            elif tag == "return":
+                if _host_evaluable(item[1], an.host_scalars):
+                    self.steps.append(("hostreturn", item[1]))
+                elif kind(item[1]) == "ScalarVar":
+                    self.steps.append(("slotreturn", b.slot(item[1].name)))  # read the slot, no kernel
+                else:
+                    self.steps.append(("return", b.return_block(item[1], f"r{idx}")))
+            else:
+                self.steps.append(item)  # declview, hostscalar
+        self.source = b.source()
+        self.nslots = max(len(b.slots), 1) + 1
+        self.launch_count = sum(1 for s in self.steps if s[0] in ("group", "kernel", "scalars", "return", "gather"))
+
+
+_plans: dict = {}
+
+
+def plan_for(fn) -> CompiledPlan:
+    hit = _plans.get(id(fn))
+    if hit is not None and hit[0] is fn:
+        return hit[1]
+    plan = CompiledPlan(fn)
+    _plans[id(fn)] = (fn, plan)
+    return plan
+
+
+def host_eval(e, H: dict, views: dict):
+    k = kind(e)
+    if k == "Literal":
+        return np.float64(e.value)
+    if k == "ScalarVar":
+        return H[e.name]
+    if k == "Extent":
+        return np.float64(views[e.view].extents[e.dim])
+    if k == "Neg":
+        return -host_eval(e.operand, H, views)
+    if k == "Binary":
+        a, b = host_eval(e.lhs, H, views), host_eval(e.rhs, H, views)
+        with np.errstate(all="ignore"):
+            return a + b if e.op == "+" else a - b if e.op == "-" else a * b if e.op == "*" else a / b
+    raise TypeError(f"not host-evaluable: {k}")
+
+
+def run(dev, fn, views: dict, scalars: dict, cfg):
+    """Execute `fn`; falls back to the statement path when the dry check says a fused
+    group cannot preserve the reference's error behaviour."""
+    from .runtime import _Run, _plan_for
+
+    plan = plan_for(fn)
+    r = _CompiledRun(dev, plan, views, scalars, cfg)
+    if not r.dry_check():
+        return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
+    return r.go()
+
+
+class _CompiledRun:
+    def __init__(self, dev, plan: CompiledPlan, views, scalars, cfg):
+        self.dev, self.plan, self.views, self.cfg = dev, plan, views, cfg
+        self.b = plan.builder
+        self.H = {k: np.float64(v) for k, v in scalars.items()}
+        self.stage: dict = {}
+        self.ret_slot = None
+        self.host_value = None
+
+    # ---- host-only rehearsal ----------------------------------------------------------
+    def dry_check(self) -> bool:
+        from .runtime import _index_value
+
+        ext = {k: v.extents for k, v in self.views.items()}
+
+        class _V:  # extents-only stand-in for _index_value
+            def __init__(self, e):
+                self.extents = e
+
+        def trip(e):
+            return int(_index_value(e, {k: _V(v) for k, v in ext.items()}))
+
+        try:
+            for step in self.plan.steps:
+                tag = step[0]
+                if tag == "declview":
+                    s = step[1]
+                    args = iter(s.dyn_args)
+                    dims = tuple(e.size if kind(e) == "StaticExtent" else trip(next(args)) for e in s.descriptor.extents)
+                    if any(d < 0 for d in dims):
+                        return False
+                    ext[s.name] = dims
+                elif tag == "group":
+                    g, recipe = step[1], step[2]
+                    n = trip(g.ops[0].upper)
+                    if n < 0:
+                        return False
+                    promoted = {p["view"] for p in recipe["promoted"]}
+                    for loop in g.ops:
+                        if loop.what == "apply":
+                            continue
+                        if trip(loop.upper) != n:
+                            return False
+                        if loop.what in ("deepcopy", "suminto"):
+                            st = loop.origin
+                            if isinstance(st.src, str) and ext[st.dst] != ext[st.src]:
+                                return False
+                        for v in fusion_views(loop) & promoted:
+                            if n > ext[v][0]:
+                                return False  # would be OutOfBounds: let the statement path report it
+                    if g.gather is not None and ext[g.gather[0].src][0] != n:
+                        return False
+        except (TypeError, KeyError):
+            return False
+        return True
+
+    # ---- launching -----------------------------------------------------------------------
+    def env(self, ptrs: dict) -> bytes:
+        b = self.b
+        nv, nh = max(len(b.views), 1), max(len(b.hslots), 1)
+        p, e0, e1 = [0] * nv, [0] * nv, [0] * nv
+        for i, name in enumerate(b.views):
+            v = self.views.get(name)
+            if v is None:
+                continue
+            e0[i] = v.extents[0]
+            e1[i] = v.extents[1] if len(v.extents) == 2 else 1
+            p[i] = ptrs[name] if name in ptrs else v.device_ptr(self.dev)
+        h = [0.0] * nh
+        for name, slot in b.hslots.items():
+            h[slot] = float(self.H.get(name, 0.0))
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h)
+
+    def launch_raw(self, name, grid_items, env_bytes, extra):
+        env = C.create_string_buffer(env_bytes)
+        holders, args = [env], [C.addressof(env)]
+        for x in extra:
+            h = C.c_longlong(x) if isinstance(x, int) else x
+            holders.append(h)
+            args.append(C.addressof(h))
+        arr = (C.c_void_p * len(args))(*args)
+        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), grid_items, arr))
+
+    def go(self):
+        from .runtime import _DeviceBuffer
+
+        dev = self.dev
+        self.mod = dev.module(self.plan.source)
+        self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
+        dev.fill(self.S.ptr, self.plan.nslots, 0.0)
+        _cabi.check(dev.lib.krn_status_reset(dev.h))
+        for step in self.plan.steps:
+            getattr(self, "do_" + step[0])(*step[1:])
+        return self.finish()
+
+    def do_declview(self, s):
+        from .runtime import ViewStorage, _index_value
+
+        args = iter(s.dyn_args)
+        dims = [e.size if kind(e) == "StaticExtent" else int(_index_value(next(args), self.views))
+                for e in s.descriptor.extents]
+        self.views[s.name] = ViewStorage.zeros(s.name, dims)
+
+    def do_hostscalar(self, s):
+        v = host_eval(s.init if kind(s) == "DeclScalar" else s.rhs, self.H, self.views)
+        if kind(s) == "DeclScalar" or s.op == "=":
+            self.H[s.name] = v
+        elif s.op == "+=":
+            self.H[s.name] = self.H[s.name] + v
+        else:
+            self.H[s.name] = self.H[s.name] - v
+
+    def do_group(self, g, recipe):
+        from .runtime import _DeviceBuffer, _index_value
+
+        dev = self.dev
+        n = int(_index_value(g.ops[0].upper, self.views))
+        n_launch = n + recipe["max_shift"]
+        if n_launch <= 0:
+            if g.gather is not None:
+                self.do_gather(*g.gather)
+            return
+        ptrs, zero_mask, n_safe = {}, 0, n
+        for k_, p in enumerate(recipe["promoted"]):
+            v = self.views[p["view"]]
+            rows = v.extents[0]
+            n_safe = min(n_safe, rows)
+            zero = bool(v._zero)
+            if zero and p["store"] and rows > n_launch:
+                zero = False  # rows the kernel does not cover must really hold zeros
+            if zero:
+                zero_mask |= 1 << k_
+            if p["store"]:
+                ptrs[p["view"]] = v.device_ptr(dev, discard=zero)
+            elif zero:
+                ptrs[p["view"]] = 0
+            else:
+                ptrs[p["view"]] = v.device_ptr(dev, write=False)
+        ld = ((n_launch + 3) // 4) * 4 + tilegen.STRIDE_PAD
+        stage_ptr = 0
+        if recipe["stage_cols"]:
+            producer = recipe["stage_cols"][0][0]
+            ncols = max(idx for _, idx in recipe["stage_cols"]) + 1
+            buf = _DeviceBuffer(dev, 8 * ncols * ld)
+            self.stage[producer] = (buf, ld)
+            stage_ptr = buf.ptr
+        for loop in g.ops:
+            if loop.what == "apply":
+                buf, ld = self.stage[id(loop.apply_of[2])]
+                stage_ptr = buf.ptr
+        blocks_items = n_launch
+        red_out, acc, partials, scratch, ticket = 0, 0, 0, 0, 0
+        if g.gather is not None:
+            stmt, accumulate = g.gather
+            red_out, acc = self.S.ptr + 8 * self.b.slot(stmt.dst), int(accumulate)
+        env = self.env(ptrs)
+        extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
+        if g.gather is not None:
+            nblocks = (n_launch + 1023) // 1024
+            ws = _DeviceBuffer(dev, 8 * 2 * nblocks + 64)
+            tk = dev.ticket_ptr()
+            extra += [C.c_void_p(ws.ptr), C.c_void_p(ws.ptr + 8 * nblocks), C.c_void_p(tk), C.c_void_p(red_out),
+                      C.c_int(acc)]
+            self._keep = ws
+        else:
+            extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]
+        # grid: one thread per 4 iterations, whole blocks of 256 (the reduction needs every thread)
+        self.launch_tile(recipe["name"], (n_launch + 3) // 4, env, extra)
+
+    def launch_tile(self, name, threads, env_bytes, extra):
+        # krn_module_launch sizes a grid-stride grid; tile kernels need exactly ceil(threads/256) blocks
+        env = C.create_string_buffer(env_bytes)
+        holders, args = [env], [C.addressof(env)]
+        for x in extra:
+            h = C.c_longlong(x) if isinstance(x, int) else x
+            holders.append(h)
+            args.append(C.addressof(h))
+        arr = (C.c_void_p * len(args))(*args)
+        _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(),
+                                                         (threads + 255) // 256, 256, arr))
+
+    def do_kernel(self, loop, recipe):
+        from .runtime import _DeviceBuffer, _index_value
+
+        n = int(_index_value(loop.upper, self.views))
+        stage = ostage = None
+        extra = [max(n, 0), C.c_void_p(0), C.c_void_p(0)]
+        if recipe["n_staged"] and n > 0:
+            stage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
+            extra[1] = C.c_void_p(stage.ptr)
+            if recipe["needs_offsets"]:
+                ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
+                extra[2] = C.c_void_p(ostage.ptr)
+        if n > 0:
+            self.launch_raw(recipe["name"], n, self.env({}), extra)
+            for ap in recipe["apply"]:
+                count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
+                if count > 0:
+                    self.launch_raw(ap["name"], count, self.env({}), extra)
+
+    def do_deepcopy(self, s):
+        from .runtime import ShapeMismatch
+
+        d = self.views[s.dst]
+        if isinstance(s.src, str):
+            src = self.views[s.src]
+            if d.extents != src.extents:
+                raise ShapeMismatch(f"deep_copy: {s.dst}{d.extents} vs {s.src}{src.extents}")
+            self.dev.copy(d.device_ptr(self.dev, discard=True), src.device_ptr(self.dev, write=False), d.size)
+        else:
+            value, dptr = self.scalar_operand(s.src)
+            self.dev.fill(d.device_ptr(self.dev, discard=True), d.size, value, dptr)
+
+    def do_suminto(self, s):
+        from .runtime import ShapeMismatch
+
+        d = self.views[s.dst]
+        if isinstance(s.src, str):
+            src = self.views[s.src]
+            if d.extents != src.extents:
+                raise ShapeMismatch(f"parallel_sum: {s.dst}{d.extents} vs {s.src}{src.extents}")
+            self.dev.add_view(d.device_ptr(self.dev), src.device_ptr(self.dev, write=False), d.size)
+        else:
+            value, dptr = self.scalar_operand(s.src)
+            self.dev.add_scalar(d.device_ptr(self.dev), d.size, value, dptr)
+
+    def scalar_operand(self, src):
+        if kind(src) == "Literal":
+            return float(src.value), 0
+        if src.name in self.H and src.name in self.plan.an.host_scalars:
+            return float(self.H[src.name]), 0
+        return 0.0, self.S.ptr + 8 * self.b.slot(src.name)
+
+    def do_gather(self, s, accumulate):
+        src = self.views[s.src]
+        out = self.S.ptr + 8 * self.b.slot(s.dst)
+        self.dev.reduce_pairwise(src.device_ptr(self.dev, write=False), src.size, out, accumulate)
+
+    def do_scalars(self, recipe):
+        self.launch_raw(recipe["name"], 1, self.env({}), [])
+
+    def do_return(self, recipe):
+        self.launch_raw(recipe["name"], 1, self.env({}), [])
+        self.ret_slot = recipe["slot"]
+
+    def do_slotreturn(self, slot):
+        self.ret_slot = slot
+
+    def do_hostreturn(self, expr):
+        self.host_value = float(host_eval(expr, self.H, self.views))
+
+    def finish(self):
+        from .runtime import _Run
+
+        dev = self.dev
+        if not self.cfg.synchronous:
+            return None
+        if self.ret_slot is not None:
+            out = dev.staging[64:72].view(np.float64)
+            dev.download_async(out, self.S.ptr + 8 * self.ret_slot)
+        st = dev.staging[:64].view(np.int64)
+        dev.download(st, dev.status_ptr)
+        if st[0] != 0:
+            helper = _Run.__new__(_Run)
+            helper.b, helper.views = self.b, self.views
+            raise helper.error_from(st.copy())
+        if self.ret_slot is not None:
+            return float(dev.staging[64:72].view(np.float64)[0])
+        return self.host_value
+
+
+def fusion_views(loop) -> set:
+    return {a.view for a in loop.accesses()}

@@ -33,6 +33,8 @@ struct Api {
     nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t *) = nullptr;
     nvrtcResult (*GetCUBIN)(nvrtcProgram, char *) = nullptr;
     nvrtcResult (*DestroyProgram)(nvrtcProgram *) = nullptr;
+    nvrtcResult (*Version)(int *, int *) = nullptr;
+    bool ld256 = true;  // NVRTC >= 12.9 understands the 256-bit vector accesses of the prelude
     // driver
     CUresult (*ModuleLoadData)(CUmodule *, const void *) = nullptr;
     CUresult (*ModuleUnload)(CUmodule) = nullptr;
@@ -57,8 +59,9 @@ int load_api()
         return api.ok ? KRN_OK : KRN_E_UNAVAILABLE;
     }
     api.tried = true;
-    void *rtc = open_first({"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
-                            "/usr/local/cuda/lib64/libnvrtc.so"});
+    // the toolkit's NVRTC first: a Python environment may carry an older one on the loader path
+    void *rtc = open_first({"/usr/local/cuda/lib64/libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so",
+                            "libnvrtc.so.12", "libnvrtc.so"});
     void *drv = open_first({"libcuda.so.1", "libcuda.so"});
     if (!rtc || !drv) {
         krn_set_error("cannot load %s: %s", !rtc ? "libnvrtc" : "libcuda", dlerror());
@@ -77,12 +80,15 @@ int load_api()
     KRN_SYM(rtc, GetCUBINSize, "nvrtcGetCUBINSize")
     KRN_SYM(rtc, GetCUBIN, "nvrtcGetCUBIN")
     KRN_SYM(rtc, DestroyProgram, "nvrtcDestroyProgram")
+    KRN_SYM(rtc, Version, "nvrtcVersion")
     KRN_SYM(drv, ModuleLoadData, "cuModuleLoadData")
     KRN_SYM(drv, ModuleUnload, "cuModuleUnload")
     KRN_SYM(drv, ModuleGetFunction, "cuModuleGetFunction")
     KRN_SYM(drv, LaunchKernel, "cuLaunchKernel")
     KRN_SYM(drv, GetErrorString, "cuGetErrorString")
 #undef KRN_SYM
+    int major = 0, minor = 0;
+    if (api.Version(&major, &minor) == NVRTC_SUCCESS) api.ld256 = major > 12 || (major == 12 && minor >= 9);
     api.ok = true;
     return KRN_OK;
 }
@@ -114,8 +120,9 @@ extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_mod
         return KRN_E_NVRTC;
     }
     const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
-                          "--prec-div=true", "--prec-sqrt=true", "--ftz=false"};
-    nvrtcResult cr = api.CompileProgram(prog, int(sizeof(opts) / sizeof(opts[0])), opts);
+                          "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-DKRN_NO_LD256"};
+    const int nopts = int(sizeof(opts) / sizeof(opts[0])) - (api.ld256 ? 1 : 0);
+    nvrtcResult cr = api.CompileProgram(prog, nopts, opts);
     if (cr != NVRTC_SUCCESS) {
         size_t n = 0;
         api.GetProgramLogSize(prog, &n);
@@ -146,6 +153,35 @@ extern "C" int krn_module_destroy(krn_module *m)
     if (m == nullptr) return KRN_OK;
     if (m->module && api.ok) api.ModuleUnload(m->module);
     delete m;
+    return KRN_OK;
+}
+
+static int find_function(krn_module *m, const char *name, CUfunction *out)
+{
+    auto it = m->functions.find(name);
+    if (it == m->functions.end()) {
+        CUfunction f;
+        CUresult r = api.ModuleGetFunction(&f, m->module, name);
+        if (r != CUDA_SUCCESS) return driver_fail("cuModuleGetFunction", r);
+        it = m->functions.emplace(name, f).first;
+    }
+    *out = it->second;
+    return KRN_OK;
+}
+
+extern "C" int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_t blocks,
+                                       unsigned threads_per_block, void **args)
+{
+    KRN_REQUIRE(ctx && m && name, "null argument");
+    KRN_REQUIRE(threads_per_block >= 32 && threads_per_block <= 1024, "bad block size");
+    KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
+    CUfunction f;
+    int rc = find_function(m, name, &f);
+    if (rc) return rc;
+    if (blocks == 0) return KRN_OK;
+    CUresult r = api.LaunchKernel(f, unsigned(blocks), 1, 1, threads_per_block, 1, 1, 0, ctx->stream, args, nullptr);
+    if (r != CUDA_SUCCESS) return driver_fail("cuLaunchKernel", r);
+    ctx->launches++;
     return KRN_OK;
 }
 

@@ -18,12 +18,16 @@ struct krn_d4 {
 
 // ---- 256-bit global accesses (LDG.E.256 / STG.E.256, new on sm_100) --------
 // "stream": read-once data, bypasses L1 allocation.
+// The 256-bit forms need PTX ISA 8.8 (CUDA 12.9).  When this header is compiled at run
+// time by an older NVRTC the loader defines KRN_NO_LD256 and each access becomes two
+// 128-bit ones (same bytes, same coalescing, twice the instructions).
+#ifndef KRN_NO_LD256
 __device__ __forceinline__ krn_d4 krn_ld4_stream(const double *p)
 {
     krn_d4 v;
     asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v.a), "=d"(v.b), "=d"(v.c), "=d"(v.d)
-                 : "l"(p));
+        : "=d"(v.a), "=d"(v.b), "=d"(v.c), "=d"(v.d)
+        : "l"(p));
     return v;
 }
 // same, for buffers the kernel also writes (read-modify-write shadows): no .nc
@@ -41,6 +45,27 @@ __device__ __forceinline__ void krn_st4(double *p, const krn_d4 &v)
                  "d"(v.c), "d"(v.d)
                  : "memory");
 }
+#else
+__device__ __forceinline__ krn_d4 krn_ld4_stream(const double *p)
+{
+    krn_d4 v;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.a), "=d"(v.b) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.c), "=d"(v.d) : "l"(p + 2));
+    return v;
+}
+__device__ __forceinline__ krn_d4 krn_ld4_rmw(const double *p)
+{
+    krn_d4 v;
+    asm("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.a), "=d"(v.b) : "l"(p));
+    asm("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.c), "=d"(v.d) : "l"(p + 2));
+    return v;
+}
+__device__ __forceinline__ void krn_st4(double *p, const krn_d4 &v)
+{
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.a), "d"(v.b) : "memory");
+    asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p + 2), "d"(v.c), "d"(v.d) : "memory");
+}
+#endif
 __device__ __forceinline__ double krn_ld1(const double *p) { return __ldg(p); }
 
 // ---- the reference's reduction tree ----------------------------------------

@@ -1,0 +1,401 @@
+"""Automatic fusion of a function's statements into fewer, wider kernels
+(the paper lists kernel fusion as future work,
+PAPER.md:837).
+
+The statement path (one launch per statement, like the reference's interpreter
+and like Kokkos) moves every intermediate View through HBM.  This pass keeps
+the reference's semantics bit for bit and removes the traffic that is only an
+artefact of statement granularity:
+
+* consecutive loop-shaped statements over the same range are merged into one
+  kernel when every View they share is touched *pointwise* (always at the
+  running index), so a value written by one statement and read by the next
+  travels in a register;
+* Views that are pointwise in a group are loaded once with a 256-bit access,
+  kept in registers, and stored once - or not at all when nothing after the
+  group reads them (dead intermediates such as ``y2``);
+* zero-initialised Views (``DeclView``, ``ViewStorage.zeros``) are never
+  materialised ahead of a kernel that only touches them pointwise: the kernel is
+  told they read as +0.0;
+* ``s = parallel_sum(v)`` fuses into the kernel that produces ``v`` (the block
+  tree of csrc/krn_prelude.cuh), and disappears when ``s`` is never read (the
+  verbatim forward reduction inside a generated gradient);
+* function-scope scalars whose value the host can know (literals, parameters and
+  arithmetic on them: seeds, ``base = c*c``) are evaluated on the host and passed
+  as kernel arguments instead of running one-thread kernels.
+
+Deferred ``atomic_add`` keeps its two policies (codegen.plan_atomics).  In gather
+mode the staging columns are ordinary pointwise Views of the producing group, and
+the apply loop is a synthetic statement that may itself fuse with what follows
+(e.g. the reversal of the in-place scale kernel).
+
+Fusion legality (what "pointwise" buys): iterations of a ``parallel_for`` are
+independent, and a kernel boundary is only observable through a View that some
+iteration reads or writes at an index other than its own.  If every shared View
+is accessed at exactly the running index by both statements, iteration i of the
+second statement depends only on iteration i of the first, and running them back
+to back inside one thread is indistinguishable from two launches.
+
+Anything outside the supported shape (rank-2 Views, staged atomics, differing
+ranges) simply stays an unfused statement and runs through the statement path.
+"""
+
+from __future__ import annotations
+
+import dataclasses as _dc
+
+from . import codegen
+from .lang import nodes as N
+from .lang.dataflow import normalize_index
+from .lang.nodes import kind, walk_expr, walk_statements
+
+K = "__k"  # counter of synthetic loops
+
+
+@_dc.dataclass
+class Access:
+    view: str
+    indices: tuple
+    write: bool
+    atomic: bool = False
+
+
+@_dc.dataclass
+class LoopOp:
+    """A loop-shaped statement: a parallel_for, a bulk builtin rewritten as one, or
+    the apply loop of gather-mode atomics."""
+
+    counter: str
+    upper: object  # index expression (trip count)
+    body: tuple
+    origin: object  # the source statement (for shape checks / fallback)
+    what: str  # "kernel" | "deepcopy" | "suminto" | "apply"
+    sites: list = _dc.field(default_factory=list)  # atomic sites of a kernel
+    apply_of: object = None  # (view, sites) for an apply loop
+    shift: int = 0  # apply loops run over upper + shift rows
+
+    def accesses(self) -> list:
+        out: list = []
+
+        def index_accesses(e):
+            for n in walk_expr(e):
+                if kind(n) == "ViewAccess":
+                    out.append(Access(n.view, tuple(n.indices), False))
+
+        def value(e):
+            for n in walk_expr(e):
+                if kind(n) == "ViewAccess":
+                    out.append(Access(n.view, tuple(n.indices), False))
+
+        for s in walk_statements(self.body):
+            k = kind(s)
+            if k == "AssignView":
+                out.append(Access(s.target.view, tuple(s.target.indices), True))
+                if s.op != "=":
+                    out.append(Access(s.target.view, tuple(s.target.indices), False))
+                for i in s.target.indices:
+                    index_accesses(i)
+                value(s.rhs)
+            elif k == "AtomicAdd":
+                out.append(Access(s.target.view, tuple(s.target.indices), True, True))
+                for i in s.target.indices:
+                    index_accesses(i)
+                value(s.value)
+            elif k == "DeclScalar":
+                value(s.init)
+            elif k == "AssignScalar":
+                value(s.rhs)
+        return out
+
+
+def _is_pointwise(acc: Access, counter: str) -> bool:
+    return len(acc.indices) == 1 and kind(acc.indices[0]) == "Counter" and acc.indices[0].name == counter
+
+
+@_dc.dataclass
+class Group:
+    ops: list
+    gather: object = None  # (ParallelSum stmt, accumulate) fused at the end
+    promoted: dict = _dc.field(default_factory=dict)  # view -> dict(load=, store=, written=)
+    name: str = ""
+
+
+class Analysis:
+    """Whole-function facts the grouping needs."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        self.rank = {p.name: p.type.rank for p in fn.params if p.is_view}
+        self.params = {p.name for p in fn.params}
+        self.extent_alias: dict = {}  # local view -> normalized declared extent (rank 1)
+        for s in walk_statements(fn.body):
+            if kind(s) == "DeclView":
+                self.rank[s.name] = s.descriptor.rank
+                if s.descriptor.rank == 1 and len(s.dyn_args) == 1:
+                    try:
+                        self.extent_alias[s.name] = self.trip(s.dyn_args[0])
+                    except (TypeError, ValueError):
+                        pass
+        self.host_scalars = self._host_scalars()
+        self.live_scalars = self._live_scalars()
+
+    # symbolic trip counts ------------------------------------------------------
+    def trip(self, e):
+        """Canonical (constant, terms) form with local-view extents replaced by the
+        expression they were declared with."""
+        const, terms = normalize_index(e)
+        out_c, out_t = const, {}
+        for atom, c in terms:
+            if atom[0] == "extent" and atom[2] == 0 and atom[1] in self.extent_alias:
+                ac, at = self.extent_alias[atom[1]]
+                out_c += c * ac
+                for a2, c2 in at:
+                    out_t[a2] = out_t.get(a2, 0) + c * c2
+            else:
+                out_t[atom] = out_t.get(atom, 0) + c
+        return out_c, tuple(sorted((a, c) for a, c in out_t.items() if c != 0))
+
+    # host-evaluable scalars ------------------------------------------------------
+    def _host_scalars(self) -> set:
+        """Function-scope scalars every definition of which is literal/parameter
+        arithmetic.  Decided per name (straight-line code, but one name may be
+        assigned several times)."""
+        device = set()
+        defs: dict = {}
+        for s in self.fn.body:
+            k = kind(s)
+            if k == "DeclScalar":
+                defs.setdefault(s.name, []).append(s.init)
+            elif k == "AssignScalar":
+                defs.setdefault(s.name, []).append(s.rhs)
+            elif k == "ParallelSum":
+                device.add(s.dst)
+            elif k == "If":
+                for inner in walk_statements(s.body):
+                    if kind(inner) in ("DeclScalar", "AssignScalar"):
+                        device.add(inner.name)  # guarded function-scope scalars: keep on the device
+        host = {p.name for p in self.fn.params if not p.is_view}
+        changed = True
+        cand = set(defs) - device
+        while changed:
+            changed = False
+            for name in list(cand):
+                for e in defs[name]:
+                    ok = True
+                    for n in walk_expr(e):
+                        kk = kind(n)
+                        if kk == "ViewAccess" or (kk == "ScalarVar" and n.name not in cand and n.name not in host):
+                            ok = False
+                    if not ok:
+                        cand.discard(name)
+                        changed = True
+                        break
+        return host | cand
+
+    def _live_scalars(self) -> set:
+        """Scalars that are ever read (anywhere): a gather into a scalar outside this
+        set is dead code."""
+        live = set()
+        for s in walk_statements(self.fn.body):
+            for e in N.statement_exprs(s):
+                for n in walk_expr(e):
+                    if kind(n) == "ScalarVar":
+                        live.add(n.name)
+            if kind(s) == "AssignScalar" and s.op != "=":
+                pass  # `s += e` reads s, but only to feed s itself
+        return live
+
+
+def _bulk_as_loop(stmt, an: Analysis):
+    """deep_copy / accumulate parallel_sum over rank-1 views as an equivalent loop."""
+    k = kind(stmt)
+    if an.rank.get(stmt.dst) != 1:
+        return None
+    tgt = N.ViewAccess(stmt.dst, (N.Counter(K),))
+    if isinstance(stmt.src, str):
+        if an.rank.get(stmt.src) != 1:
+            return None
+        rhs = N.ViewAccess(stmt.src, (N.Counter(K),))
+    else:
+        rhs = stmt.src
+    op = "=" if k == "DeepCopy" else "+="
+    body = (N.AssignView(tgt, op, rhs),)
+    return LoopOp(K, N.Extent(stmt.dst, 0), body, stmt, "deepcopy" if k == "DeepCopy" else "suminto")
+
+
+def build_ops(fn, an: Analysis) -> list:
+    """Statement list -> op list.  Ops are ('loop', LoopOp) | ('gather', stmt, acc) |
+    ('scalars', [stmts]) | ('hostscalar', stmt) | ('declview', stmt) | ('return', expr) |
+    ('raw', stmt) for statements the fusion pass does not model."""
+    ops: list = []
+    bound = {p.name for p in fn.params if not p.is_view}
+    run: list = []
+
+    def flush():
+        if run:
+            ops.append(("scalars", list(run)))
+            run.clear()
+
+    for s in fn.body:
+        k = kind(s)
+        if k in ("DeclScalar", "AssignScalar") and s.name in an.host_scalars:
+            flush()
+            bound.add(s.name)
+            ops.append(("hostscalar", s))
+            continue
+        if k in codegen._ELEMENT:
+            run.append(s)
+            if k == "DeclScalar":
+                bound.add(s.name)
+            continue
+        flush()
+        if k == "DeclView":
+            ops.append(("declview", s))
+        elif k == "ParallelFor":
+            sites = codegen.plan_atomics(s)
+            modes = {st.mode for st in sites}
+            rank2 = any(an.rank.get(a.view, 1) != 1 for a in LoopOp(s.counter, s.upper, s.body, s, "kernel").accesses())
+            if rank2 or "staged_atomic" in modes:
+                ops.append(("raw", s))
+                continue
+            loop = LoopOp(s.counter, s.upper, tuple(s.body), s, "kernel", sites)
+            ops.append(("loop", loop))
+            targets: dict = {}
+            for st in sites:
+                if st.mode == "gather":
+                    targets.setdefault(st.view, []).append(st)
+            for view, group in targets.items():
+                shift = max(0, max(st.offset for st in group))
+                ops.append(("loop", LoopOp(K, s.upper, (), s, "apply", apply_of=(view, group, loop), shift=shift)))
+        elif k in ("DeepCopy", "ParallelSumInto"):
+            loop = _bulk_as_loop(s, an)
+            ops.append(("loop", loop) if loop is not None else ("raw", s))
+        elif k == "ParallelSum":
+            if s.dst not in an.live_scalars:
+                bound.add(s.dst)
+                continue  # the sum is never read: dead statement
+            ops.append(("gather", s, s.dst in bound))
+            bound.add(s.dst)
+        elif k == "Return":
+            ops.append(("return", s.value))
+        else:
+            raise TypeError(f"cannot execute {k}")
+    flush()
+    return ops
+
+
+def _reads_scalar(group: "Group", name: str) -> bool:
+    for loop in group.ops:
+        bodies = [loop.body]
+        if loop.what == "apply":
+            bodies = []
+        for body in bodies:
+            for s in walk_statements(body):
+                for e in N.statement_exprs(s):
+                    for n in walk_expr(e):
+                        if kind(n) == "ScalarVar" and n.name == name:
+                            return True
+    return False
+
+
+def form_groups(ops: list, an: Analysis) -> list:
+    """Greedy left-to-right grouping.  Returns a schedule of
+    ('group', Group) | the non-loop ops unchanged."""
+    schedule: list = []
+    cur = None  # (Group, trip, access summary)
+
+    def close():
+        nonlocal cur
+        if cur is not None:
+            schedule.append(("group", cur[0]))
+            cur = None
+
+    def summary(loop: LoopOp):
+        """view -> (pointwise_only, written, atomic_direct)"""
+        out: dict = {}
+        accs = loop.accesses()
+        if loop.what == "apply":
+            view, group, producer = loop.apply_of
+            accs = [Access(view, (N.Counter(K),), True), Access(view, (N.Counter(K),), False)]
+            for st in group:
+                accs.append(Access(f"__stage{st.index}@{id(producer)}", (N.IntLiteral(0),), False))
+        if loop.what == "kernel":
+            for st in loop.sites:
+                if st.mode == "gather":
+                    accs.append(Access(f"__stage{st.index}@{id(loop)}", (N.Counter(loop.counter),), True))
+        staged_views = {st.view for st in loop.sites if st.mode == "gather"}
+        for a in accs:
+            if a.atomic and a.view in staged_views:
+                continue  # staged: the write goes to the staging column, not to the view
+            pw = _is_pointwise(a, loop.counter)
+            e = out.setdefault(a.view, [True, False, False])
+            e[0] = e[0] and pw
+            e[1] = e[1] or a.write
+            e[2] = e[2] or (a.atomic)
+        return out
+
+    for op in ops:
+        if op[0] != "loop":
+            if op[0] == "gather" and cur is not None:
+                g, trip, acc = cur
+                stmt = op[1]
+                src = stmt.src
+                try:
+                    src_trip = an.trip(N.Extent(src, 0))
+                except (TypeError, ValueError):
+                    src_trip = None
+                info = acc.get(src)
+                if (an.rank.get(src) == 1 and src_trip == trip and all(o.shift == 0 for o in g.ops)
+                        and (info is None or (info[0] and not info[2]))):
+                    g.gather = (stmt, op[2])
+                    close()
+                    continue
+            if op[0] == "declview":
+                # creates a new (lazy, zero) View: nothing in the open group can refer to it, so
+                # it is scheduled ahead of the group, which stays open
+                schedule.append(op)
+                continue
+            if op[0] == "hostscalar" and cur is not None and not _reads_scalar(cur[0], op[1].name):
+                schedule.append(op)  # host bookkeeping the open group does not depend on
+                continue
+            close()
+            schedule.append(op)
+            continue
+        loop = op[1]
+        try:
+            trip = an.trip(loop.upper)
+        except (TypeError, ValueError):
+            close()
+            schedule.append(("group", Group([loop])))
+            continue
+        acc = summary(loop)
+        if cur is not None:
+            g, gtrip, gacc = cur
+            ok = gtrip == trip
+            # one staging buffer per kernel: a group holds at most one producer of staged
+            # contributions, and never a producer together with an apply loop
+            producer = loop.what == "kernel" and any(st.mode == "gather" for st in loop.sites)
+            has_producer = any(o.what == "kernel" and any(st.mode == "gather" for st in o.sites) for o in g.ops)
+            has_apply = any(o.what == "apply" for o in g.ops)
+            if (producer and (has_producer or has_apply)) or (loop.what == "apply" and (has_producer or has_apply)):
+                ok = False
+            if ok:
+                for v, (pw, wr, at) in acc.items():
+                    if v in gacc:
+                        gpw, gwr, gat = gacc[v]
+                        if at or gat:
+                            ok = False
+                        elif (wr or gwr) and not (pw and gpw):
+                            ok = False
+                    if not ok:
+                        break
+            if ok:
+                g.ops.append(loop)
+                for v, (pw, wr, at) in acc.items():
+                    e = gacc.setdefault(v, [True, False, False])
+                    e[0], e[1], e[2] = e[0] and pw, e[1] or wr, e[2] or at
+                continue
+            close()
+        cur = (Group([loop]), trip, {v: list(t) for v, t in acc.items()})
+    close()
+    return schedule

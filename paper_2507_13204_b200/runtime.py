@@ -137,6 +137,15 @@ class Device:
             pool.append(self.event())
         return pool[:count]
 
+    def ticket_ptr(self) -> int:
+        """Arrival counter for block-level reductions of generated kernels (kept at zero
+        between launches: the last block re-arms it)."""
+        t = self.__dict__.get("_ticket")
+        if t is None:
+            t = self.__dict__["_ticket"] = self.alloc(8)
+            self.fill(t, 1, 0.0)
+        return t
+
     def pinned_scratch(self, count: int) -> np.ndarray:
         cur = self.__dict__.get("_pinned_scratch")
         if cur is None or cur.size < count:
@@ -421,8 +430,8 @@ class ExecutionConfig:
     def __post_init__(self):
         if self.threads < 1:
             raise ValueError("threads must be >= 1")
-        if self.policy not in ("fused", "statements"):
-            raise ValueError("policy must be 'fused' or 'statements'")
+        if self.policy not in ("fused", "compiled", "statements"):
+            raise ValueError("policy must be 'fused', 'compiled' or 'statements'")
 
 
 def effective_threads(cfg: ExecutionConfig) -> int:
@@ -565,7 +574,9 @@ class _Run:
                 ptrs[i] = v.device_ptr(self.dev)
                 e0[i] = v.extents[0]
                 e1[i] = v.extents[1] if len(v.extents) == 2 else 1
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr)
+        nh = max(len(self.b.hslots), 1)  # Env.H: unused on the statement path, but part of the layout
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
+                           *([0.0] * nh))
 
     def launch(self, name: str, n: int, extra=()):
         env = C.create_string_buffer(self.env())
@@ -773,6 +784,10 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
         hit = fused.match(fn)
         if hit is not None and hit.applicable(views):
             return ExecResult(hit.run(dev, views, scalars, cfg))
+    if cfg.policy in ("fused", "compiled") and not cfg.check_finite:
+        from . import compiled
+
+        return ExecResult(compiled.run(dev, fn, views, scalars, cfg))
     plan = _plan_for(fn)
     return ExecResult(_Run(dev, plan, views, scalars, cfg).go())
 

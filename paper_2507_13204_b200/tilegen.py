@@ -1,0 +1,186 @@
+"""CUDA generation for a fused group of loop-shaped statements (fusion.py).
+
+Shape of a tile kernel: every thread owns 4 consecutive iterations j0..j0+3.
+
+    prologue   each *promoted* View (rank 1, touched only at the running index by every
+               statement of the group) is read once: one LDG.E.256 on the fast path,
+               guarded scalar loads on the ragged tail; a View the host knows to be all
+               +0.0 is not read at all (zero_mask bit)
+    body       the statements of the group, per iteration, in program order; promoted
+               Views are registers, every other access goes through the bounds-checked
+               accessors of the statement path; staged atomic contributions go to
+               per-site register columns
+    epilogue   promoted Views that were written AND are read by anything after the group
+               (or belong to the caller) are stored once (STG.E.256); staging columns are
+               stored; a trailing `s = parallel_sum(v)` is folded with the reference's
+               tree (block partial + last-block final pass, csrc/krn_prelude.cuh)
+
+The generated text only uses helpers of the statement path's preamble and of the
+hand-written prelude, and is compiled with the same flags (--fmad=false).
+"""
+
+from __future__ import annotations
+
+from .lang import nodes as N
+from .lang.nodes import kind, walk_statements
+
+STRIDE_PAD = 8  # staging columns are padded so that column starts stay 32-byte aligned
+
+
+def _first_access_is_full_store(group, view, ops_with_full_range) -> bool:
+    """True when, in program order, the first statement of the group touching `view`
+    is an unguarded top-level `view(i) = rhs` whose rhs does not read `view`, in a
+    statement that runs over the whole range of the group."""
+    for loop in group.ops:
+        if loop.what == "apply":
+            if loop.apply_of[0] == view:
+                return False
+            continue
+        for s in loop.body:  # top level only
+            touches = False
+            for inner in walk_statements([s]):
+                for e in N.statement_exprs(inner):
+                    for n in N.walk_expr(e):
+                        if kind(n) == "ViewAccess" and n.view == view:
+                            touches = True
+            if not touches:
+                continue
+            if (kind(s) == "AssignView" and s.op == "=" and s.target.view == view and id(loop) in ops_with_full_range
+                    and not any(kind(n) == "ViewAccess" and n.view == view for n in N.walk_expr(s.rhs))):
+                return True
+            return False
+    return False
+
+
+def plan_group(builder, group, an, live_after: set) -> dict:
+    """Decide what is promoted, loaded and stored; returns the recipe dict (without text)."""
+    accessed: dict = {}  # view -> [all pointwise?, written?]
+    direct_atomic: set = set()
+    for loop in group.ops:
+        if loop.what == "apply":
+            v = loop.apply_of[0]
+            e = accessed.setdefault(v, [True, False])
+            e[1] = True
+            continue
+        staged = {st.view for st in loop.sites if st.mode == "gather"}
+        for a in loop.accesses():
+            if a.atomic and a.view in staged:
+                continue
+            if a.atomic:
+                direct_atomic.add(a.view)
+            pw = len(a.indices) == 1 and kind(a.indices[0]) == "Counter" and a.indices[0].name == loop.counter
+            e = accessed.setdefault(a.view, [True, False])
+            e[0] = e[0] and pw
+            e[1] = e[1] or a.write
+    if group.gather is not None:
+        accessed.setdefault(group.gather[0].src, [True, False])
+    full_range = {id(l) for l in group.ops if l.shift == 0}
+    promoted = []
+    for v, (pw, written) in accessed.items():
+        if pw and builder.rank.get(v) == 1 and v not in direct_atomic:
+            load = not _first_access_is_full_store(group, v, full_range)
+            store = written and (v in live_after)
+            promoted.append(dict(view=v, load=load, store=store, written=written))
+    stage_cols = []
+    for loop in group.ops:
+        if loop.what == "kernel":
+            stage_cols += [(id(loop), st.index) for st in loop.sites if st.mode == "gather"]
+    return dict(promoted=promoted, stage_cols=stage_cols, max_shift=max(l.shift for l in group.ops),
+                has_user_ops=any(l.what != "apply" for l in group.ops))
+
+
+def tile_kernel(builder, group, name: str, plan: dict) -> dict:
+    b = builder
+    promoted = plan["promoted"]
+    regs = {p["view"]: f"P{b.vid(p['view'])}" for p in promoted}
+    has_stage = bool(plan["stage_cols"]) or any(l.what == "apply" for l in group.ops)
+    gather = group.gather
+    L: list = []
+    w = L.append
+    w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
+      "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
+      "unsigned int *ticket, double *red_out, int accumulate)")
+    w("{")
+    w("    const krn_i64 j0 = 4 * (blockIdx.x * (krn_i64)blockDim.x + threadIdx.x);")
+    w("    const bool full = j0 + 4 <= n_safe;")
+    w("    const bool live = j0 < n_launch;")
+    # ---- prologue ----------------------------------------------------------------
+    for k_, p in enumerate(promoted):
+        r, v = regs[p["view"]], b.vid(p["view"])
+        w(f"    double {r}[4] = {{0.0, 0.0, 0.0, 0.0}};")
+        if p["load"]:
+            w(f"    if (live && !(zero_mask & {1 << k_}u)) {{")
+            w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
+            w(f"        else {{ for (int e = 0; e < 4; ++e) if (j0 + e < E.e0[{v}] && j0 + e < n_launch) {r}[e] = E.v[{v}][j0 + e]; }}")
+            w("    }")
+    for (_, idx) in plan["stage_cols"]:
+        w(f"    double T{idx}[4] = {{0.0, 0.0, 0.0, 0.0}};")
+    # ---- body ------------------------------------------------------------------------
+    w("    if (live) {")
+    w("#pragma unroll")
+    w("    for (int e = 0; e < 4; ++e) {")
+    w("        const krn_i64 i = j0 + e;")
+    w("        bool bad = false;")
+    w("        if (i >= n_launch) continue;")
+    b.promoted = regs
+    try:
+        for loop in group.ops:
+            if loop.what == "apply":
+                view, sites, producer = loop.apply_of
+                v, r = b.vid(view), regs.get(view)
+                order = sorted(sites, key=lambda st: (-st.offset, st.index))
+                w(f"        if (i < n + {loop.shift} && i < E.e0[{v}]) {{  // deferred atomic adds landing on row i, reference order")
+                tgt = f"{r}[e]" if r else f"E.v[{v}][i]"
+                w(f"            double acc = {tgt};")
+                for st in order:
+                    guard = " && ".join(["i >= 0", "i < n"] + [b.compare(g, {producer.counter}) for g in st.guards])
+                    w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); "
+                      f"if ({guard}) acc = acc + stage[{st.index} * ld + i]; }} }}")
+                w(f"            {tgt} = acc;")
+                w("        }")
+                continue
+            sites = {id(st.stmt): st for st in loop.sites}
+            body: list = []
+            local = {loop.counter}
+            for s in loop.body:
+                b.element(s, local, body, "            ", sites, True)
+            w("        if (i < n) {" if plan["max_shift"] else "        {")
+            L.extend(body)
+            w("        }")
+    finally:
+        b.promoted = {}
+    w("    }")
+    w("    }")
+    # ---- epilogue -----------------------------------------------------------------------
+    for p in promoted:
+        if not p["store"]:
+            continue
+        r, v = regs[p["view"]], b.vid(p["view"])
+        w("    if (live) {")
+        w(f"        if (full) {{ krn_d4 q = {{{r}[0], {r}[1], {r}[2], {r}[3]}}; krn_st4(E.v[{v}] + j0, q); }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) if (j0 + e < E.e0[{v}] && j0 + e < n_launch) E.v[{v}][j0 + e] = {r}[e]; }}")
+        w("    }")
+    for (_, idx) in plan["stage_cols"]:
+        w(f"    if (live) {{ krn_d4 q = {{T{idx}[0], T{idx}[1], T{idx}[2], T{idx}[3]}}; krn_st4(stage + {idx} * ld + j0, q); }}")
+    if gather is not None:
+        src = gather[0].src
+        r = regs[src]
+        w("    {")
+        w("        double R[4];")
+        w("        for (int e = 0; e < 4; ++e) R[e] = (j0 + e < n) ? "
+          f"{r}[e] : krn_tree_pad((krn_u64)(j0 + e), (krn_u64)n);")
+        w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
+        w("        __shared__ double s_warp[8];")
+        w("        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;")
+        w("        if (lane == 0) s_warp[warp] = node;")
+        w("        __syncthreads();")
+        w("        if (warp == 0) { double v = krn_smem_tree(s_warp, 8, lane); if (lane == 0) partials[blockIdx.x] = v; }")
+        w("        if (krn_last_block(ticket, gridDim.x)) {")
+        w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
+        w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
+        w("        }")
+        w("    }")
+    w("}")
+    b.parts.append("\n".join(L))
+    return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
+                gather=gather, max_shift=plan["max_shift"])

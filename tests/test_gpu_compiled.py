@@ -1,0 +1,177 @@
+"""GPU parity, fusion pass (policy "compiled"): every corpus program and gradient
+at sizes that exercise the tile kernels' fast path, ragged tails and the
+zero-provenance / live-out decisions, against the CPU oracle, plus the cases in
+which the dry check must hand the call to the statement path."""
+
+import numpy as np
+import pytest
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import ExecutionConfig, OutOfBounds, ShapeMismatch, ViewStorage, parse
+from conftest import CORPUS, assert_bits
+
+pytestmark = pytest.mark.gpu
+CFG = ExecutionConfig(policy="compiled")
+ATOMIC_ORDER = {"gather_indirect"}
+
+
+def _inputs(fn, n, rng):
+    inputs = {}
+    for p in fn.params:
+        if not p.is_view:
+            inputs[p.name] = float(rng.uniform(0.5, 1.5))
+        elif p.name == "idx":
+            inputs[p.name] = rng.integers(0, n, size=n).astype(np.float64)
+        elif p.type.rank == 2:
+            inputs[p.name] = rng.normal(size=(n, 3))
+        else:
+            inputs[p.name] = rng.normal(size=n)
+    return inputs
+
+
+def _views(d):
+    return {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in d.items()}
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 255, 1023, 1024, 1025, 4099, 100_003])
+@pytest.mark.parametrize("stem", CORPUS)
+def test_primal_and_gradient_against_oracle(stem, n):
+    from oracle import interp
+
+    if n > 5000 and stem == "gather_indirect":
+        n = 5003  # the Python oracle's deferred-atomic queue is slow
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    rng = np.random.default_rng(1000 * n + len(stem))
+    inputs = _inputs(fn, n, rng)
+    # primal
+    if n <= 5000:
+        want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+        wv = interp.run(prog, fn.name, want)
+        got = _views(inputs)
+        assert_bits(krn.execute(prog, fn.name, got, CFG).value, wv, f"{stem} n={n} value")
+        for k, v in got.items():
+            if isinstance(v, ViewStorage):
+                assert_bits(v.buffer, want[k], f"{stem} n={n} {k}")
+    # gradient: zero shadows and pre-filled shadows
+    wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    for prefilled in (False, True):
+        if n > 5000 and prefilled:
+            continue
+        want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+        got = _views(inputs)
+        for sp, primal in zip(gfn.params[len(fn.params):], wrt):
+            shape = np.shape(inputs[primal])
+            init = rng.normal(size=shape) if prefilled else np.zeros(shape)
+            want[sp.name] = init.copy()
+            got[sp.name] = ViewStorage.from_values(sp.name, init) if prefilled else ViewStorage.zeros(sp.name, shape)
+        if n <= 5000:
+            interp.run(gp, gfn.name, want)
+        else:
+            # large case: the statement path (already checked against the oracle) is the yardstick
+            ref = _views(inputs)
+            for sp, primal in zip(gfn.params[len(fn.params):], wrt):
+                ref[sp.name] = ViewStorage.zeros(sp.name, np.shape(inputs[primal]))
+            krn.execute(gp, gfn.name, ref, ExecutionConfig(policy="statements"))
+            want = {k: (v.buffer if isinstance(v, ViewStorage) else v) for k, v in ref.items()}
+        assert krn.execute(gp, gfn.name, got, CFG).value is None
+        for k, v in got.items():
+            if not isinstance(v, ViewStorage):
+                continue
+            if stem in ATOMIC_ORDER and k.startswith("_d_"):
+                assert np.all(np.abs(v.buffer - want[k]) <= 1e-12 * np.abs(want[k])), (stem, n, k)
+            else:
+                assert_bits(v.buffer, want[k], f"{stem} n={n} prefilled={prefilled} {k}")
+
+
+def test_headline_through_the_fusion_pass_large():
+    """the generic pass on the headline objective at a bandwidth-bound size, against the C oracle"""
+    from oracle import cport
+
+    n = 3_000_017
+    rng = np.random.default_rng(4)
+    x, b = rng.normal(size=n), rng.normal(size=n)
+    lap = krn.load_program("laplacian")
+    xo = x.copy()
+    fo = cport.laplacian_primal(xo, b.copy())
+    xv = ViewStorage.from_values("x", x)
+    assert_bits(krn.execute(lap, "normRes1DLaplacianSQ", {"x": xv, "b": ViewStorage.from_values("b", b)}, CFG).value, fo, "f")
+    assert_bits(xv.buffer, xo, "x")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    dxo, dbo = np.zeros(n), np.zeros(n)
+    cport.laplacian_grad(x.copy(), b.copy(), dxo, dbo, 1.0)
+    call = {"x": ViewStorage.from_values("x", x), "b": ViewStorage.from_values("b", b),
+            "_d_x": ViewStorage.zeros("_d_x", (n,)), "_d_b": ViewStorage.zeros("_d_b", (n,))}
+    krn.execute(gp, "normRes1DLaplacianSQ_grad", call, CFG)
+    assert_bits(call["_d_x"].buffer, dxo, "_d_x")
+    assert_bits(call["_d_b"].buffer, dbo, "_d_b")
+    assert_bits(call["x"].buffer, xo, "x after grad")
+
+
+def test_views_longer_than_the_range():
+    """a kernel over extent(v) that writes a longer zero View: the rows it does not cover must
+    still read as zero afterwards (the zero shortcut may not skip materialisation)"""
+    from oracle import interp
+
+    src = """fn f(v: view<f64, 1>, w: view<f64, 1>) -> f64 {
+        parallel_for i in 0..extent(v, 0) { w(i) = v(i) * 2.0; }
+        parallel_for i in 0..extent(v, 0) { w(i) += 1.0; }
+        return parallel_sum(w); }"""
+    p = parse(src)
+    v = np.arange(1.0, 7.0)
+    want = {"v": v.copy(), "w": np.zeros(11)}
+    wv = interp.run(p, "f", want)
+    got = {"v": ViewStorage.from_values("v", v), "w": ViewStorage.zeros("w", (11,))}
+    assert_bits(krn.execute(p, "f", got, CFG).value, wv, "value")
+    assert_bits(got["w"].buffer, want["w"], "w")
+
+
+def test_dead_and_host_scalars():
+    from oracle import interp
+
+    src = """fn f(v: view<f64, 1>, c: f64) -> f64 {
+        let t: view<f64, 1> = view("t", extent(v, 0));
+        let a: f64 = c * 2.0 + 1.0;
+        a -= 0.25;
+        parallel_for i in 0..extent(v, 0) { t(i) = v(i) * a + i; }
+        unused = parallel_sum(t);
+        s = parallel_sum(t);
+        deep_copy(t, s);
+        parallel_for i in 0..extent(v, 0) { v(i) = t(i) - v(i) / a; }
+        return s * a - extent(v, 0); }"""
+    p = parse(src)
+    for n in (1, 6, 1030):
+        v = np.random.default_rng(n).normal(size=n)
+        want = {"v": v.copy(), "c": 0.75}
+        wv = interp.run(p, "f", want)
+        got = {"v": ViewStorage.from_values("v", v), "c": 0.75}
+        assert_bits(krn.execute(p, "f", got, CFG).value, wv, f"value n={n}")
+        assert_bits(got["v"].buffer, want["v"], f"v n={n}")
+
+
+def test_errors_fall_back_to_the_statement_path():
+    lap = krn.load_program("laplacian")
+    with pytest.raises(OutOfBounds, match=r"b\(2\) outside extent 2"):
+        krn.execute(lap, "normRes1DLaplacianSQ", {"x": np.ones(3), "b": np.zeros(2)}, CFG)
+    src = "fn f(v: view<f64, 1>, w: view<f64, 1>) { deep_copy(w, v); }"
+    with pytest.raises(ShapeMismatch, match="deep_copy"):
+        krn.execute(parse(src), "f", {"v": np.ones(3), "w": np.zeros(1)}, CFG)
+    oob = "fn f(v: view<f64, 1>) {\n parallel_for i in 0..extent(v, 0) {\n v(i) = v(i + 1);\n }\n}"
+    with pytest.raises(OutOfBounds, match=r"line 3: v\(2\) outside extent 2"):
+        krn.execute(parse(oob), "f", {"v": np.ones(2)}, CFG)
+
+
+def test_fewer_launches_than_statements():
+    dev = krn.Device.get()
+    lap = krn.load_program("laplacian")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    counts = {}
+    for policy in ("statements", "compiled", "fused"):
+        call = {"x": np.ones(5000), "b": np.zeros(5000), "_d_x": ViewStorage.zeros("_d_x", (5000,)),
+                "_d_b": ViewStorage.zeros("_d_b", (5000,))}
+        l0 = dev.launches()
+        krn.execute(gp, "normRes1DLaplacianSQ_grad", call, ExecutionConfig(policy=policy))
+        counts[policy] = dev.launches() - l0
+    assert counts["fused"] == 1 and counts["compiled"] == 3 and counts["statements"] >= 9, counts

@@ -20,7 +20,7 @@ def _views(inputs):
     return {k: krn.ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
 
 
-@pytest.mark.parametrize("policy", ["fused", "statements"])
+@pytest.mark.parametrize("policy", ["fused", "compiled", "statements"])
 @pytest.mark.parametrize("n", SIZES)
 @pytest.mark.parametrize("stem", CORPUS)
 def test_primal_matches_reference(corpus_golden, stem, n, policy):
@@ -35,7 +35,7 @@ def test_primal_matches_reference(corpus_golden, stem, n, policy):
             assert_bits(v.buffer, corpus_golden[f"{key}/primal/after/{name}"], f"{key} {name}")
 
 
-@pytest.mark.parametrize("policy", ["fused", "statements"])
+@pytest.mark.parametrize("policy", ["fused", "compiled", "statements"])
 @pytest.mark.parametrize("n", SIZES)
 @pytest.mark.parametrize("stem", CORPUS)
 def test_gradient_matches_reference(corpus_golden, stem, n, policy):

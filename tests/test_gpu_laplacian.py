@@ -38,7 +38,7 @@ def _cases(g):
     return sorted({k.split("/")[0] for k in g.files})
 
 
-@pytest.mark.parametrize("policy", ["fused", "statements"])
+@pytest.mark.parametrize("policy", ["fused", "compiled", "statements"])
 def test_reference_vectors(lap, laplacian_golden, policy):
     g = laplacian_golden
     for tag in _cases(g):
