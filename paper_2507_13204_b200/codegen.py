@@ -200,6 +200,8 @@ class ModuleBuilder:
         self.host_scalars = set(host_scalars)
         self.hslots: dict = {}  # host-known scalar -> slot in Env.H
         self.promoted: dict = {}  # view -> register array name, while a tile kernel is generated
+        self.elide = None  # bounds-check elision context (tile kernels only)
+        self.guards: list = []  # enclosing If conditions of the statement being generated
         self.views: list = []  # view table: name -> index
         self.rank: dict = {}
         self.slots: dict = {}  # function-scope scalar -> slot in S
@@ -255,10 +257,68 @@ class ModuleBuilder:
             return f"({self.index(e.lhs, local)} {e.op} {self.index(e.rhs, local)})"
         raise TypeError(f"cannot generate index {k}")
 
+    # ---- static bounds-check elision (tile kernels) -------------------------------------
+    # `self.elide` = dict(counter, trip, sym, views) while a fused group is generated.  The
+    # running index i satisfies L <= i <= n-1-U, refined by the enclosing guards
+    # (`i != 0`, `i != extent(x,0) - 1`, `i >= c`, `i < n + k`, ...).  An access v(i + c) is
+    # in range for every i if L + c >= 0 and c - U <= 0 PROVIDED extent(v, 0) >= n, which the
+    # host verifies before launching (otherwise the call runs on the statement path, with
+    # every check in place).
+    def _range(self):
+        el = self.elide
+        lo, up = 0, 0
+        counter_terms = ((("counter", el["counter"]), 1),)
+        for c in self.guards:
+            try:
+                (lc, lt), (rc, rt) = el["sym"](c.lhs), el["sym"](c.rhs)
+            except (TypeError, ValueError):
+                continue
+            op = c.op
+            if rt == counter_terms and lt != counter_terms:  # put the counter on the left
+                (lc, lt), (rc, rt) = (rc, rt), (lc, lt)
+                op = {"<": ">", "<=": ">=", ">": "<", ">=": "<=", "==": "==", "!=": "!="}[op]
+            if lt != counter_terms:
+                continue
+            k_const = rc - lc  # condition reads: i  op  (rt-part) + k_const
+            if not rt:  # compared with a constant
+                if op == "!=" and k_const == lo:
+                    lo += 1
+                elif op == ">":
+                    lo = max(lo, k_const + 1)
+                elif op == ">=":
+                    lo = max(lo, k_const)
+            elif (0, rt) == (0, el["trip"][1]):  # compared with n + k  (same symbolic terms as the trip count)
+                k_rel = k_const - el["trip"][0]  # rhs = n + k_rel
+                if op == "!=" and k_rel == -1 - up:
+                    up += 1
+                elif op == "<":
+                    up = max(up, -k_rel)
+                elif op == "<=":
+                    up = max(up, -k_rel - 1)
+        return lo, up
+
+    def _provably_in_range(self, acc) -> bool:
+        el = self.elide
+        if el is None or len(acc.indices) != 1 or self.rank.get(acc.view) != 1:
+            return False
+        try:
+            const, terms = normalize_index(acc.indices[0])
+        except (TypeError, ValueError):
+            return False
+        if terms != ((("counter", el["counter"]), 1),):
+            return False
+        lo, up = self._range()
+        if lo + const >= 0 and const - up <= 0:
+            el["views"].add(acc.view)
+            return True
+        return False
+
     def offset(self, acc, local) -> str:
         v = self.vid(acc.view)
         line = getattr(acc.span, "line", 0)
         idx = [self.index(i, local) for i in acc.indices]
+        if self._provably_in_range(acc):
+            return f"({idx[0]})"
         if len(idx) == 1:
             return f"off1(E, {v}, {idx[0]}, {line}, bad)"
         return f"off2(E, {v}, {idx[0]}, {idx[1]}, {line}, bad)"
@@ -346,8 +406,12 @@ class ModuleBuilder:
                 out.append(head + f"krn_red_add(&E.v[{v}][o_], t_); }}")
         elif k == "If":
             out.append(f"{pad}if {self.compare(s.cond, local)} {{")
-            for inner in s.body:
-                self.element(inner, local, out, pad + "    ", sites, in_kernel)
+            self.guards.append(s.cond)
+            try:
+                for inner in s.body:
+                    self.element(inner, local, out, pad + "    ", sites, in_kernel)
+            finally:
+                self.guards.pop()
             out.append(f"{pad}}}")
         else:
             raise TypeError(f"statement not allowed here: {k}")

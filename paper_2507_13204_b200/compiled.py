@@ -87,7 +87,7 @@ class CompiledPlan:
                 for nxt in self.schedule[idx + 1:]:
                     later |= _views_of(nxt)
                 plan = tilegen.plan_group(b, item[1], an, later)
-                self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan)))
+                self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan, an)))
             elif tag == "raw":
                 s = item[1]
                 if kind(s) == "ParallelFor":
@@ -98,14 +98,14 @@ class CompiledPlan:
                 b.slot(item[1].dst)
                 self.steps.append(("gather", item[1], item[2]))
             elif tag == "scalars":
-                self.steps.append(("scalars", b.scalar_block(item[1], f"s{idx}")))
+                self.steps.append(("scalars", b.scalar_block(item[1], f"s{idx}"), _views_of(item)))
             elif tag == "return":
                 if _host_evaluable(item[1], an.host_scalars):
                     self.steps.append(("hostreturn", item[1]))
                 elif kind(item[1]) == "ScalarVar":
                     self.steps.append(("slotreturn", b.slot(item[1].name)))  # read the slot, no kernel
                 else:
-                    self.steps.append(("return", b.return_block(item[1], f"r{idx}")))
+                    self.steps.append(("return", b.return_block(item[1], f"r{idx}"), _views_of(item)))
             else:
                 self.steps.append(item)  # declview, hostscalar
         self.source = b.source()
@@ -206,12 +206,18 @@ class _CompiledRun:
                                 return False  # would be OutOfBounds: let the statement path report it
                     if g.gather is not None and ext[g.gather[0].src][0] != n:
                         return False
+                    for v in recipe["elided_views"]:
+                        if n > ext[v][0]:
+                            return False  # the elided checks assumed extent >= range
         except (TypeError, KeyError):
             return False
         return True
 
     # ---- launching -----------------------------------------------------------------------
-    def env(self, ptrs: dict) -> bytes:
+    def env(self, ptrs: dict, needed=None) -> bytes:
+        """Kernel argument block.  `ptrs`: explicit device pointers (promoted Views);
+        `needed`: the other Views the kernel touches - only those are materialised on the
+        device (None = every View of the function, for kernels that are not analysed)."""
         b = self.b
         nv, nh = max(len(b.views), 1), max(len(b.hslots), 1)
         p, e0, e1 = [0] * nv, [0] * nv, [0] * nv
@@ -221,7 +227,10 @@ class _CompiledRun:
                 continue
             e0[i] = v.extents[0]
             e1[i] = v.extents[1] if len(v.extents) == 2 else 1
-            p[i] = ptrs[name] if name in ptrs else v.device_ptr(self.dev)
+            if name in ptrs:
+                p[i] = ptrs[name]
+            elif needed is None or name in needed:
+                p[i] = v.device_ptr(self.dev)
         h = [0.0] * nh
         for name, slot in b.hslots.items():
             h[slot] = float(self.H.get(name, 0.0))
@@ -309,10 +318,18 @@ class _CompiledRun:
         if g.gather is not None:
             stmt, accumulate = g.gather
             red_out, acc = self.S.ptr + 8 * self.b.slot(stmt.dst), int(accumulate)
-        env = self.env(ptrs)
+        needed = set()
+        for loop in g.ops:
+            if loop.what == "apply":
+                needed.add(loop.apply_of[0])
+                continue
+            staged = {st.view for st in loop.sites if st.mode == "gather"}
+            needed |= {a.view for a in loop.accesses() if not (a.atomic and a.view in staged)}
+        env = self.env(ptrs, needed - set(ptrs))
         extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
+        steps = 1 if n_launch <= (1 << 20) else 8  # must be a power of two (tree node per block)
+        nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)
         if g.gather is not None:
-            nblocks = (n_launch + 1023) // 1024
             ws = _DeviceBuffer(dev, 8 * 2 * nblocks + 64)
             tk = dev.ticket_ptr()
             extra += [C.c_void_p(ws.ptr), C.c_void_p(ws.ptr + 8 * nblocks), C.c_void_p(tk), C.c_void_p(red_out),
@@ -320,10 +337,10 @@ class _CompiledRun:
             self._keep = ws
         else:
             extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]
-        # grid: one thread per 4 iterations, whole blocks of 256 (the reduction needs every thread)
-        self.launch_tile(recipe["name"], (n_launch + 3) // 4, env, extra)
+        extra.append(C.c_int(steps))
+        self.launch_tile(recipe["name"], nblocks, env, extra)
 
-    def launch_tile(self, name, threads, env_bytes, extra):
+    def launch_tile(self, name, nblocks, env_bytes, extra):
         # krn_module_launch sizes a grid-stride grid; tile kernels need exactly ceil(threads/256) blocks
         env = C.create_string_buffer(env_bytes)
         holders, args = [env], [C.addressof(env)]
@@ -332,8 +349,7 @@ class _CompiledRun:
             holders.append(h)
             args.append(C.addressof(h))
         arr = (C.c_void_p * len(args))(*args)
-        _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(),
-                                                         (threads + 255) // 256, 256, arr))
+        _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(), nblocks, 256, arr))
 
     def do_kernel(self, loop, recipe):
         from .runtime import _DeviceBuffer, _index_value
@@ -348,11 +364,12 @@ class _CompiledRun:
                 ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
                 extra[2] = C.c_void_p(ostage.ptr)
         if n > 0:
-            self.launch_raw(recipe["name"], n, self.env({}), extra)
+            needed = _views_in_stmts([loop])
+            self.launch_raw(recipe["name"], n, self.env({}, needed), extra)
             for ap in recipe["apply"]:
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:
-                    self.launch_raw(ap["name"], count, self.env({}), extra)
+                    self.launch_raw(ap["name"], count, self.env({}, needed), extra)
 
     def do_deepcopy(self, s):
         from .runtime import ShapeMismatch
@@ -392,11 +409,11 @@ class _CompiledRun:
         out = self.S.ptr + 8 * self.b.slot(s.dst)
         self.dev.reduce_pairwise(src.device_ptr(self.dev, write=False), src.size, out, accumulate)
 
-    def do_scalars(self, recipe):
-        self.launch_raw(recipe["name"], 1, self.env({}), [])
+    def do_scalars(self, recipe, needed):
+        self.launch_raw(recipe["name"], 1, self.env({}, needed), [])
 
-    def do_return(self, recipe):
-        self.launch_raw(recipe["name"], 1, self.env({}), [])
+    def do_return(self, recipe, needed):
+        self.launch_raw(recipe["name"], 1, self.env({}, needed), [])
         self.ret_slot = recipe["slot"]
 
     def do_slotreturn(self, slot):

@@ -22,6 +22,7 @@ hand-written prelude, and is compiled with the same flags (--fmad=false).
 from __future__ import annotations
 
 from .lang import nodes as N
+from .lang.dataflow import normalize_index
 from .lang.nodes import kind, walk_statements
 
 STRIDE_PAD = 8  # staging columns are padded so that column starts stay 32-byte aligned
@@ -85,12 +86,32 @@ def plan_group(builder, group, an, live_after: set) -> dict:
     for loop in group.ops:
         if loop.what == "kernel":
             stage_cols += [(id(loop), st.index) for st in loop.sites if st.mode == "gather"]
+    # thread -> iteration mapping.  "vector": 4 consecutive iterations per thread, promoted Views
+    # move with one 256-bit access.  "strided": lane L of a warp takes iterations L, L+32, L+64,
+    # L+96 of the warp's 128, so that EVERY access of the form v(i + c) is coalesced (stencil
+    # neighbours, staging columns read by an apply loop); chosen when the group has such accesses
+    # to Views it cannot promote.
+    promoted_names = {p["view"] for p in promoted}
+    strided = any(l.what == "apply" for l in group.ops)
+    for loop in group.ops:
+        if loop.what == "apply":
+            continue
+        for a in loop.accesses():
+            if a.view in promoted_names or len(a.indices) != 1:
+                continue
+            try:
+                const, terms = normalize_index(a.indices[0])
+            except (TypeError, ValueError):
+                continue
+            if terms == ((("counter", loop.counter), 1),):
+                strided = True
     return dict(promoted=promoted, stage_cols=stage_cols, max_shift=max(l.shift for l in group.ops),
-                has_user_ops=any(l.what != "apply" for l in group.ops))
+                has_user_ops=any(l.what != "apply" for l in group.ops), strided=strided)
 
 
-def tile_kernel(builder, group, name: str, plan: dict) -> dict:
+def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b = builder
+    elided: set = set()
     promoted = plan["promoted"]
     regs = {p["view"]: f"P{b.vid(p['view'])}" for p in promoted}
     has_stage = bool(plan["stage_cols"]) or any(l.what == "apply" for l in group.ops)
@@ -99,19 +120,39 @@ def tile_kernel(builder, group, name: str, plan: dict) -> dict:
     w = L.append
     w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
       "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
-      "unsigned int *ticket, double *red_out, int accumulate)")
+      "unsigned int *ticket, double *red_out, int accumulate, int steps)")
     w("{")
-    w("    const krn_i64 j0 = 4 * (blockIdx.x * (krn_i64)blockDim.x + threadIdx.x);")
-    w("    const bool full = j0 + 4 <= n_safe;")
-    w("    const bool live = j0 < n_launch;")
+    strided = plan["strided"]
+    # a warp owns 128*steps consecutive iterations, a block 1024*steps (an aligned power-of-two
+    # chunk of the reduction tree); `steps` > 1 amortises block start-up and the block-level
+    # combine on bandwidth-bound sizes
+    w("    const int lane_ = threadIdx.x & 31;")
+    w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128 * steps;")
+    w("    double tstack[6];  // binary-counter tree over the warp's steps")
+    w("    int tdepth = 0;")
+    w("    (void)tstack; (void)tdepth;")
+    w("    for (int t = 0; t < steps; ++t) {")
+    if strided:
+        w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first iteration of this step")
+        w("    const bool full = j0 + 128 <= n_safe;")
+        w("    const bool live = j0 < n_launch;")
+        w("#define KRN_IT(e) (j0 + (e) * 32 + lane_)")
+    else:
+        w("    const krn_i64 j0 = wbase + (krn_i64)t * 128 + 4 * lane_;")
+        w("    const bool full = j0 + 4 <= n_safe;")
+        w("    const bool live = j0 < n_launch;")
+        w("#define KRN_IT(e) (j0 + (e))")
     # ---- prologue ----------------------------------------------------------------
     for k_, p in enumerate(promoted):
         r, v = regs[p["view"]], b.vid(p["view"])
         w(f"    double {r}[4] = {{0.0, 0.0, 0.0, 0.0}};")
         if p["load"]:
             w(f"    if (live && !(zero_mask & {1 << k_}u)) {{")
-            w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
-            w(f"        else {{ for (int e = 0; e < 4; ++e) if (j0 + e < E.e0[{v}] && j0 + e < n_launch) {r}[e] = E.v[{v}][j0 + e]; }}")
+            if strided:
+                w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
+            else:
+                w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
+            w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
             w("    }")
     for (_, idx) in plan["stage_cols"]:
         w(f"    double T{idx}[4] = {{0.0, 0.0, 0.0, 0.0}};")
@@ -119,7 +160,7 @@ def tile_kernel(builder, group, name: str, plan: dict) -> dict:
     w("    if (live) {")
     w("#pragma unroll")
     w("    for (int e = 0; e < 4; ++e) {")
-    w("        const krn_i64 i = j0 + e;")
+    w("        const krn_i64 i = KRN_IT(e);")
     w("        bool bad = false;")
     w("        if (i >= n_launch) continue;")
     b.promoted = regs
@@ -142,8 +183,16 @@ def tile_kernel(builder, group, name: str, plan: dict) -> dict:
             sites = {id(st.stmt): st for st in loop.sites}
             body: list = []
             local = {loop.counter}
-            for s in loop.body:
-                b.element(s, local, body, "            ", sites, True)
+            if an is not None:
+                try:
+                    b.elide = dict(counter=loop.counter, trip=an.trip(loop.upper), sym=an.trip, views=elided)
+                except (TypeError, ValueError):
+                    b.elide = None
+            try:
+                for s in loop.body:
+                    b.element(s, local, body, "            ", sites, True)
+            finally:
+                b.elide = None
             w("        if (i < n) {" if plan["max_shift"] else "        {")
             L.extend(body)
             w("        }")
@@ -157,24 +206,43 @@ def tile_kernel(builder, group, name: str, plan: dict) -> dict:
             continue
         r, v = regs[p["view"]], b.vid(p["view"])
         w("    if (live) {")
-        w(f"        if (full) {{ krn_d4 q = {{{r}[0], {r}[1], {r}[2], {r}[3]}}; krn_st4(E.v[{v}] + j0, q); }}")
-        w(f"        else {{ for (int e = 0; e < 4; ++e) if (j0 + e < E.e0[{v}] && j0 + e < n_launch) E.v[{v}][j0 + e] = {r}[e]; }}")
+        if strided:
+            w(f"        if (full) {{ for (int e = 0; e < 4; ++e) E.v[{v}][KRN_IT(e)] = {r}[e]; }}")
+        else:
+            w(f"        if (full) {{ krn_d4 q = {{{r}[0], {r}[1], {r}[2], {r}[3]}}; krn_st4(E.v[{v}] + j0, q); }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) E.v[{v}][KRN_IT(e)] = {r}[e]; }}")
         w("    }")
     for (_, idx) in plan["stage_cols"]:
-        w(f"    if (live) {{ krn_d4 q = {{T{idx}[0], T{idx}[1], T{idx}[2], T{idx}[3]}}; krn_st4(stage + {idx} * ld + j0, q); }}")
+        if strided:
+            w(f"    if (live) {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < n_launch) stage[{idx} * ld + KRN_IT(e)] = T{idx}[e]; }}")
+        else:
+            w(f"    if (live) {{ krn_d4 q = {{T{idx}[0], T{idx}[1], T{idx}[2], T{idx}[3]}}; krn_st4(stage + {idx} * ld + j0, q); }}")
     if gather is not None:
         src = gather[0].src
         r = regs[src]
         w("    {")
         w("        double R[4];")
-        w("        for (int e = 0; e < 4; ++e) R[e] = (j0 + e < n) ? "
-          f"{r}[e] : krn_tree_pad((krn_u64)(j0 + e), (krn_u64)n);")
-        w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
+        w("        for (int e = 0; e < 4; ++e) R[e] = (KRN_IT(e) < n) ? "
+          f"{r}[e] : krn_tree_pad((krn_u64)KRN_IT(e), (krn_u64)n);")
+        if strided:
+            # element e of the 32 lanes = 32 consecutive leaves: four 32-leaf subtrees, then two levels
+            w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
+            w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
+        else:
+            w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
+        w("        int m_ = t;")
+        w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
+        w("        tstack[tdepth++] = node;")
+        w("    }")
+    w("#undef KRN_IT")
+    w("    }  // steps")
+    if gather is not None:
+        w("    {")
         w("        __shared__ double s_warp[8];")
-        w("        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;")
-        w("        if (lane == 0) s_warp[warp] = node;")
+        w("        const int warp = threadIdx.x >> 5;")
+        w("        if (lane_ == 0) s_warp[warp] = tstack[0];")
         w("        __syncthreads();")
-        w("        if (warp == 0) { double v = krn_smem_tree(s_warp, 8, lane); if (lane == 0) partials[blockIdx.x] = v; }")
+        w("        if (warp == 0) { double v = krn_smem_tree(s_warp, 8, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
         w("        if (krn_last_block(ticket, gridDim.x)) {")
         w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
         w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
@@ -183,4 +251,4 @@ def tile_kernel(builder, group, name: str, plan: dict) -> dict:
     w("}")
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
-                gather=gather, max_shift=plan["max_shift"])
+                gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided))

@@ -1,0 +1,98 @@
+"""CPU tier: decisions of the fusion pass (grouping, promotion, dead code, host
+scalars, bounds-check elision) on the corpus - no device needed."""
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import compiled, fusion
+from conftest import CORPUS
+
+
+def _grad(stem):
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+    return fn, krn.differentiate(prog, fn.name, wrt).functions[-1]
+
+
+def _shape(fn):
+    an = fusion.Analysis(fn)
+    out = []
+    for item in fusion.form_groups(fusion.build_ops(fn, an), an):
+        if item[0] == "group":
+            g = item[1]
+            out.append("G[" + ",".join(o.what for o in g.ops) + ("+gather" if g.gather else "") + "]")
+        else:
+            out.append(item[0])
+    return an, out
+
+
+def test_headline_schedule():
+    fn, g = _grad("laplacian")
+    an, shape = _shape(fn)
+    # the in-place scale cannot fuse with the stencil that reads its neighbours' results
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel]", "G[kernel+gather]"]
+    an, shape = _shape(g)
+    assert an.host_scalars == {"_d_sum"}  # the seed never needs a device kernel
+    groups = [s for s in shape if s.startswith("G[")]
+    # forward stencil + seed broadcast + its reversal in one kernel; the dead forward reduction is gone;
+    # the deferred atomics' apply loop fuses with the reversal of the scale kernel
+    assert groups == ["G[kernel]", "G[kernel,suminto,kernel]", "G[apply,kernel]"]
+    assert "gather" not in shape
+
+
+def test_promotion_and_dead_stores():
+    _, g = _grad("laplacian")
+    plan = compiled.plan_for(g)
+    recipes = [s[2] for s in plan.steps if s[0] == "group"]
+    middle = {p["view"]: p for p in recipes[1]["promoted"]}
+    # y, y2, _d_y, _d_y2 live and die inside the kernel: never loaded from nor stored to memory
+    for v in ("y", "y2"):
+        assert not middle[v]["load"] and not middle[v]["store"]
+    for v in ("_d_y", "_d_y2"):
+        assert not middle[v]["store"]
+    assert middle["_d_b"]["store"] and middle["b"]["load"] and not middle["b"]["store"]
+    assert "x" not in middle and recipes[1]["elided_views"] == ["_d_x", "x"]
+    assert len(recipes[1]["stage_cols"]) == 3
+    last = {p["view"]: p for p in recipes[2]["promoted"]}
+    assert last["_d_x"]["store"]
+
+
+def test_every_corpus_function_compiles_to_a_plan():
+    for stem in CORPUS:
+        for fn in _grad(stem):
+            plan = compiled.plan_for(fn)
+            assert plan.source.count('extern "C" __global__') >= 1
+            statements = sum(1 for s in fn.body if type(s).__name__ in
+                             ("ParallelFor", "DeepCopy", "ParallelSum", "ParallelSumInto"))
+            launches = sum(1 for s in plan.steps if s[0] in ("group", "kernel", "gather", "deepcopy", "suminto"))
+            assert launches <= statements
+
+
+def test_rank2_and_unsupported_shapes_stay_unfused():
+    fn, g = _grad("rowscale_rank2")
+    _, shape = _shape(g)
+    assert "raw" in shape and not any(s.startswith("G[") for s in shape)
+
+
+def test_host_scalars_and_gather_accumulate():
+    fn, g = _grad("mean_shift")
+    an, shape = _shape(fn)
+    assert "total" not in an.host_scalars            # produced by a gather: lives on the device
+    an, shape = _shape(_grad("fill_scale")[0])
+    assert {"base", "c"} <= an.host_scalars           # c*c is evaluated on the host
+
+
+def test_bounds_check_elision_ranges():
+    p = krn.parse("""fn f(x: view<f64,1>, y: view<f64,1>) {
+        parallel_for i in 0..extent(x, 0) {
+            y(i) = x(i);
+            if (i != 0) { y(i) += x(i - 1); }
+            if (i != extent(x, 0) - 1) { y(i) += x(i + 1); }
+            if (i >= 2) { y(i) += x(i - 2); }
+            if (i < extent(x, 0) - 2) { y(i) += x(i + 2); }
+            y(i) += x(i + 1) * 0.0;
+        } }""")
+    plan = compiled.plan_for(p.functions[0])
+    src = plan.source
+    body = src[src.index('g0('):]
+    # five of the six neighbour reads are provably in range; the unguarded x(i + 1) keeps its check
+    assert body.count("off1(E") == 1
