@@ -157,11 +157,13 @@ int krn_module_destroy(krn_module *m);
 /* launch `name` over `n_iterations` (grid sized by the library: a multiple of
  * the SM count); args = array of pointers to the kernel's arguments */
 int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, size_t n_iterations,
-                      void **args);
+                      size_t shared_bytes, void **args);
 /* launch `name` with exactly `blocks` x `threads_per_block` (tile kernels of fused statement
  * groups: one thread per 4 iterations, and block-level reductions that need every thread) */
 int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_t blocks,
-                            unsigned threads_per_block, void **args);
+                            unsigned threads_per_block, size_t shared_bytes, void **args);
+/* shared_bytes: dynamic shared memory (<= 48 KB), used by the shared-memory-privatised
+ * accumulation policy of atomic_add targets with few rows */
 
 /* ---- status word: 8 x int64 {code, line, view id, index0, index1, 0, 0, 0} of the
  *      first failing access (first error wins) ---- */

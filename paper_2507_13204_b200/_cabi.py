@@ -69,8 +69,8 @@ SIGNATURES = {
     "krn_laplacian_partial_span": (_sz, [_sz]),
     "krn_module_compile": (_i, [_vp, C.c_char_p, _pp]),
     "krn_module_destroy": (_i, [_vp]),
-    "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _pp]),
-    "krn_module_launch_exact": (_i, [_vp, _vp, C.c_char_p, _sz, C.c_uint, _pp]),
+    "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),
+    "krn_module_launch_exact": (_i, [_vp, _vp, C.c_char_p, _sz, C.c_uint, _sz, _pp]),
     "krn_status_reset": (_i, [_vp]),
     "krn_status_device_ptr": (_i, [_vp, _pp]),
     "krn_status_read": (_i, [_vp, C.POINTER(C.c_longlong)]),

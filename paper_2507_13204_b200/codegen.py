@@ -151,7 +151,35 @@ struct Env {
     double *S;          // function-scope scalars that live on the device (gather results, ...)
     krn_i64 *status;
     double H[NH > 0 ? NH : 1];  // function-scope scalars the host knows, passed by value
+    krn_i64 priv_rows;  // accumulation policy of atomic_add targets (chosen by the host per launch):
+    int apol;           //   0 plain RED.ADD.F64, 1 warp-aggregated, 2 shared-memory privatised
+    int priv_vid;       //   view whose rows are privatised when apol == 2
 };
+extern __shared__ double krn_priv[];
+__device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, double t)
+{
+    if (E.apol == 2 && v == E.priv_vid) atomicAdd(&krn_priv[o], t);
+    else if (E.apol == 1) krn_red_add_aggregated(&E.v[v][o], t);
+    else krn_red_add(&E.v[v][o], t);
+}
+// -0.0 is the additive identity: a privatised row that still holds it received nothing
+__device__ __forceinline__ void krn_priv_begin(const Env &E)
+{
+    if (E.apol == 2) {
+        for (krn_i64 k = threadIdx.x; k < E.priv_rows; k += blockDim.x) krn_priv[k] = -0.0;
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ void krn_priv_end(const Env &E)
+{
+    if (E.apol == 2) {
+        __syncthreads();
+        for (krn_i64 k = threadIdx.x; k < E.priv_rows; k += blockDim.x) {
+            double s = krn_priv[k];
+            if (__double_as_longlong(s) != __double_as_longlong(-0.0)) krn_red_add(&E.v[E.priv_vid][k], s);
+        }
+    }
+}
 // bounds-checked linear offsets; on failure record {code,line,view,i,j} and flag the iteration
 __device__ __forceinline__ krn_i64 off1(const Env &E, int v, krn_i64 i, int line, bool &bad)
 {
@@ -403,7 +431,7 @@ class ModuleBuilder:
                 out.append(head + f"stage[{site.index} * n + i] = t_; "
                                   f"ostage[{site.index} * n + i] = o_; }}")
             else:
-                out.append(head + f"krn_red_add(&E.v[{v}][o_], t_); }}")
+                out.append(head + f"krn_scatter(E, {v}, o_, t_); }}")
         elif k == "If":
             out.append(f"{pad}if {self.compare(s.cond, local)} {{")
             self.guards.append(s.cond)
@@ -429,6 +457,7 @@ class ModuleBuilder:
             f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, double *stage, '
             "krn_i64 *ostage)",
             "{",
+            "    krn_priv_begin(E);" if any(st.mode == "atomic" for st in sites) else "",
             "    for (krn_i64 i = blockIdx.x * (krn_i64)blockDim.x + threadIdx.x; i < n; "
             "i += (krn_i64)gridDim.x * blockDim.x) {",
             "        bool bad = false;",
@@ -439,10 +468,11 @@ class ModuleBuilder:
             for st in staged:
                 if st.mode == "staged_atomic":
                     src.append(f"        ostage[{st.index} * n + i] = -1;")
-        src += body + ["    }", "}"]
+        src += body + ["    }", "    krn_priv_end(E);" if any(st.mode == "atomic" for st in sites) else "", "}"]
         self.parts.append("\n".join(src))
         recipe = dict(name=name, sites=sites, n_staged=len(sites) if staged else 0,
-                      needs_offsets=needs_offsets, apply=[])
+                      needs_offsets=needs_offsets, apply=[],
+                      atomic_views=sorted({st.view for st in sites if st.mode == "atomic"}))
         # apply kernels
         gather_views: dict = {}
         for st in sites:

@@ -214,7 +214,7 @@ class _CompiledRun:
         return True
 
     # ---- launching -----------------------------------------------------------------------
-    def env(self, ptrs: dict, needed=None) -> bytes:
+    def env(self, ptrs: dict, needed=None, atomic=(0, 0, 0)) -> bytes:
         """Kernel argument block.  `ptrs`: explicit device pointers (promoted Views);
         `needed`: the other Views the kernel touches - only those are materialised on the
         device (None = every View of the function, for kernels that are not analysed)."""
@@ -234,7 +234,8 @@ class _CompiledRun:
         h = [0.0] * nh
         for name, slot in b.hslots.items():
             h[slot] = float(self.H.get(name, 0.0))
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h)
+        self._shared = 8 * atomic[0] if atomic[1] == 2 else 0
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqii", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h, *atomic)
 
     def launch_raw(self, name, grid_items, env_bytes, extra):
         env = C.create_string_buffer(env_bytes)
@@ -244,7 +245,8 @@ class _CompiledRun:
             holders.append(h)
             args.append(C.addressof(h))
         arr = (C.c_void_p * len(args))(*args)
-        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), grid_items, arr))
+        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), grid_items,
+                                                   getattr(self, "_shared", 0), arr))
 
     def go(self):
         from .runtime import _DeviceBuffer
@@ -325,7 +327,10 @@ class _CompiledRun:
                 continue
             staged = {st.view for st in loop.sites if st.mode == "gather"}
             needed |= {a.view for a in loop.accesses() if not (a.atomic and a.view in staged)}
-        env = self.env(ptrs, needed - set(ptrs))
+        from .runtime import atomic_choice
+
+        env = self.env(ptrs, needed - set(ptrs),
+                       atomic_choice(self.cfg, recipe["atomic_views"], self.views, self.b, n_launch))
         extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
         steps = 1 if n_launch <= (1 << 20) else 8  # must be a power of two (tree node per block)
         nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)
@@ -349,7 +354,8 @@ class _CompiledRun:
             holders.append(h)
             args.append(C.addressof(h))
         arr = (C.c_void_p * len(args))(*args)
-        _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(), nblocks, 256, arr))
+        _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(), nblocks, 256,
+                                                         getattr(self, "_shared", 0), arr))
 
     def do_kernel(self, loop, recipe):
         from .runtime import _DeviceBuffer, _index_value
@@ -364,8 +370,11 @@ class _CompiledRun:
                 ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
                 extra[2] = C.c_void_p(ostage.ptr)
         if n > 0:
+            from .runtime import atomic_choice
+
             needed = _views_in_stmts([loop])
-            self.launch_raw(recipe["name"], n, self.env({}, needed), extra)
+            self.launch_raw(recipe["name"], n, self.env({}, needed, atomic_choice(
+                self.cfg, recipe["atomic_views"], self.views, self.b, n)), extra)
             for ap in recipe["apply"]:
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:

@@ -170,8 +170,9 @@ static int find_function(krn_module *m, const char *name, CUfunction *out)
 }
 
 extern "C" int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_t blocks,
-                                       unsigned threads_per_block, void **args)
+                                       unsigned threads_per_block, size_t shared_bytes, void **args)
 {
+    KRN_REQUIRE(shared_bytes <= 48 * 1024, "more than 48 KB of dynamic shared memory");
     KRN_REQUIRE(ctx && m && name, "null argument");
     KRN_REQUIRE(threads_per_block >= 32 && threads_per_block <= 1024, "bad block size");
     KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
@@ -179,16 +180,18 @@ extern "C" int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *
     int rc = find_function(m, name, &f);
     if (rc) return rc;
     if (blocks == 0) return KRN_OK;
-    CUresult r = api.LaunchKernel(f, unsigned(blocks), 1, 1, threads_per_block, 1, 1, 0, ctx->stream, args, nullptr);
+    CUresult r = api.LaunchKernel(f, unsigned(blocks), 1, 1, threads_per_block, 1, 1, unsigned(shared_bytes),
+                                  ctx->stream, args, nullptr);
     if (r != CUDA_SUCCESS) return driver_fail("cuLaunchKernel", r);
     ctx->launches++;
     return KRN_OK;
 }
 
 extern "C" int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, size_t n_iterations,
-                                 void **args)
+                                 size_t shared_bytes, void **args)
 {
     KRN_REQUIRE(ctx && m && name, "null argument");
+    KRN_REQUIRE(shared_bytes <= 48 * 1024, "more than 48 KB of dynamic shared memory");
     auto it = m->functions.find(name);
     if (it == m->functions.end()) {
         CUfunction f;
@@ -201,7 +204,8 @@ extern "C" int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, 
     size_t want = (n_iterations + block - 1) / block;
     size_t cap = size_t(ctx->sms) * 32;  // grid-stride loops inside; whole multiples of the SM count
     unsigned grid = unsigned(want < cap ? want : cap);
-    CUresult r = api.LaunchKernel(it->second, grid, 1, 1, block, 1, 1, 0, ctx->stream, args, nullptr);
+    CUresult r = api.LaunchKernel(it->second, grid, 1, 1, block, 1, 1, unsigned(shared_bytes), ctx->stream, args,
+                                  nullptr);
     if (r != CUDA_SUCCESS) return driver_fail("cuLaunchKernel", r);
     ctx->launches++;
     return KRN_OK;

@@ -218,10 +218,9 @@ __device__ __forceinline__ void krn_red_add(double *p, double v) { atomicAdd(p, 
 
 // warp-aggregated: lanes hitting the same address are folded first (in lane
 // order) so one RED leaves the warp per distinct address
-__device__ __forceinline__ void krn_red_add_aggregated(double *p, double v, bool active)
+__device__ __forceinline__ void krn_red_add_aggregated(double *p, double v)
 {
-    unsigned int live = __ballot_sync(KRN_FULL_MASK, active);
-    if (!active) return;
+    unsigned int live = __activemask();  // the lanes that reached this site together
     unsigned int peers = __match_any_sync(live, (krn_u64)p);
     int lane = threadIdx.x & 31;
     int leader = __ffs(peers) - 1;

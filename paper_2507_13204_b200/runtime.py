@@ -426,12 +426,18 @@ class ExecutionConfig:
     # True: when the Views of a recognised gradient call live on the host, cut the rows into
     # chunks and overlap upload / kernel / download of the shadows (fused.run_streamed)
     stream_host_io: bool = False
+    # how atomic_add contributions to non-injective targets are accumulated (generated kernels):
+    # "red" hardware fp64 reductions, "warp" warp-aggregated, "smem" block-privatised in shared
+    # memory (targets of <= 6144 elements), "auto" = smem for small hot targets, else red
+    atomic_policy: str = "auto"
 
     def __post_init__(self):
         if self.threads < 1:
             raise ValueError("threads must be >= 1")
         if self.policy not in ("fused", "compiled", "statements"):
             raise ValueError("policy must be 'fused', 'compiled' or 'statements'")
+        if self.atomic_policy not in ("auto", "red", "warp", "smem"):
+            raise ValueError("atomic_policy must be 'auto', 'red', 'warp' or 'smem'")
 
 
 def effective_threads(cfg: ExecutionConfig) -> int:
@@ -527,6 +533,25 @@ def _plan_for(fn) -> _Plan:
     return plan
 
 
+SMEM_PRIVATE_MAX = 6144  # doubles: 48 KB of dynamic shared memory
+
+
+def atomic_choice(cfg, atomic_views, views, builder, n):
+    """(rows, policy, view id) for Env: how a kernel accumulates its direct atomic_add
+    contributions.  Privatisation pays when the target is small and hit often: every block
+    folds its contributions in shared memory and issues at most one RED per row."""
+    if not atomic_views:
+        return (0, 0, 0)
+    name = atomic_views[0]
+    rows = views[name].size
+    want = cfg.atomic_policy
+    if want == "auto":
+        want = "smem" if (0 < rows <= SMEM_PRIVATE_MAX and n >= 4 * rows) else "red"
+    if want == "smem" and not (0 < rows <= SMEM_PRIVATE_MAX):
+        want = "red"
+    return (rows, {"red": 0, "warp": 1, "smem": 2}[want], builder.vid(name))
+
+
 def _scalar_src(dev, plan, S, src):
     """(host value, device pointer) for a Literal / ScalarVar bulk operand."""
     if kind(src) == "Literal":
@@ -565,7 +590,7 @@ class _Run:
         _cabi.check(dev.lib.krn_status_reset(dev.h))
         self.kernel_index = 0
 
-    def env(self) -> bytes:
+    def env(self, atomic=(0, 0, 0)) -> bytes:
         nv = max(len(self.b.views), 1)
         ptrs, e0, e1 = [0] * nv, [0] * nv, [0] * nv
         for i, name in enumerate(self.b.views):
@@ -575,11 +600,11 @@ class _Run:
                 e0[i] = v.extents[0]
                 e1[i] = v.extents[1] if len(v.extents) == 2 else 1
         nh = max(len(self.b.hslots), 1)  # Env.H: unused on the statement path, but part of the layout
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
-                           *([0.0] * nh))
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqii", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
+                           *([0.0] * nh), *atomic)
 
-    def launch(self, name: str, n: int, extra=()):
-        env = C.create_string_buffer(self.env())
+    def launch(self, name: str, n: int, extra=(), atomic=(0, 0, 0)):
+        env = C.create_string_buffer(self.env(atomic))
         holders = [env]
         args = [C.addressof(env)]
         for x in extra:
@@ -587,7 +612,8 @@ class _Run:
             holders.append(h)
             args.append(C.addressof(h))
         arr = (C.c_void_p * len(args))(*args)
-        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), n, arr))
+        shared = 8 * atomic[0] if atomic[1] == 2 else 0
+        _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), n, shared, arr))
 
     def go(self):
         for step in self.plan.steps:
@@ -620,7 +646,8 @@ class _Run:
                 ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
                 extra[2] = C.c_void_p(ostage.ptr)
         if n > 0:
-            self.launch(recipe["name"], n, extra)
+            self.launch(recipe["name"], n, extra, atomic_choice(self.cfg, recipe["atomic_views"], self.views,
+                                                                 self.b, n))
             for ap in recipe["apply"]:
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:

@@ -126,6 +126,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     # a warp owns 128*steps consecutive iterations, a block 1024*steps (an aligned power-of-two
     # chunk of the reduction tree); `steps` > 1 amortises block start-up and the block-level
     # combine on bandwidth-bound sizes
+    direct = sorted({st.view for l in group.ops for st in l.sites if st.mode == "atomic"})
+    if direct:
+        w("    krn_priv_begin(E);")
     w("    const int lane_ = threadIdx.x & 31;")
     w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128 * steps;")
     w("    double tstack[6];  // binary-counter tree over the warp's steps")
@@ -236,6 +239,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("    }")
     w("#undef KRN_IT")
     w("    }  // steps")
+    if direct:
+        w("    krn_priv_end(E);")
     if gather is not None:
         w("    {")
         w("        __shared__ double s_warp[8];")
@@ -251,4 +256,4 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     w("}")
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
-                gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided))
+                gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct)
