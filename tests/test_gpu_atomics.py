@@ -22,7 +22,7 @@ def _index_maps(n, rows, rng):
     }
 
 
-@pytest.mark.parametrize("apol", ["auto", "red", "warp", "smem"])
+@pytest.mark.parametrize("apol", ["auto", "red", "warp", "smem", "lead"])
 @pytest.mark.parametrize("policy", ["compiled", "statements"])
 def test_gather_indirect_gradient_all_policies(policy, apol):
     from oracle import interp
@@ -42,7 +42,7 @@ def test_gather_indirect_gradient_all_policies(policy, apol):
             assert np.all(err <= 1e-12 * np.abs(want["_d_x"])), (policy, apol, n, rows, label, err.max())
 
 
-@pytest.mark.parametrize("apol", ["red", "warp", "smem"])
+@pytest.mark.parametrize("apol", ["red", "warp", "smem", "lead"])
 def test_integer_contributions_are_exact(apol):
     """reference tests/test_runtime.py:150-164, generalised: sums of small integers are exact in
     any order, so every policy must return the same bits"""
