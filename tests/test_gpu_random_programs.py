@@ -1,0 +1,165 @@
+"""GPU tier, differential testing: random well-formed programs (pointwise kernels,
+guarded stencils, in-place affine updates, bulk copies/accumulates, gathers feeding
+fills, indirect reads) and their generated gradients, executed under every policy
+and compared with the CPU oracle.  Bar: bit-exact; programs whose gradient
+accumulates through hardware atomics (indirect targets) are compared at 1e-12 on
+the scale of the contributions."""
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, assume, given, settings
+from hypothesis import strategies as st
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import ExecutionConfig, ViewStorage
+from conftest import assert_bits
+
+pytestmark = pytest.mark.gpu
+
+LITS = ["0.5", "2.0", "1.25", "3.0", "0.125", "1.5"]
+
+
+@st.composite
+def programs(draw):
+    ntemps = draw(st.integers(1, 3))
+    temps = [f"t{k}" for k in range(ntemps)]
+    use_idx = draw(st.booleans())
+    use_c = draw(st.booleans())
+    params = ["a: view<f64, 1>", "b: view<f64, 1>"] + (["idx: view<f64, 1>"] if use_idx else []) + (["c: f64"] if use_c else [])
+    lines = [f'    let {t}: view<f64, 1> = view("{t}", extent(a, 0));' for t in temps]
+    scalars: list = []
+
+    def leaf(allow):
+        # gather results are not read inside kernels: the reference's transform has no reduction
+        # reversal for an active function-scope scalar used in a kernel body (it would emit an
+        # assignment to a non-local scalar, which its own validator forbids)
+        kinds = ["a", "b", "lit"] + (["c"] if use_c else []) + (["tmp"] if allow else []) + ["i"]
+        k = draw(st.sampled_from(kinds))
+        if k == "a":
+            return "a(i)"
+        if k == "b":
+            return "b(i)"
+        if k == "lit":
+            return draw(st.sampled_from(LITS))
+        if k == "c":
+            return "c"
+        if k == "tmp":
+            return f"{draw(st.sampled_from(allow))}(i)"
+        if k == "s":
+            return draw(st.sampled_from(scalars))
+        return "i"
+
+    def expr(depth, allow):
+        if depth == 0 or draw(st.integers(0, 3)) == 0:
+            return leaf(allow)
+        op = draw(st.sampled_from(["+", "-", "*", "*", "/"]))
+        lhs = expr(depth - 1, allow)
+        if op == "/":
+            d = leaf(allow)
+            return f"({lhs} / ({draw(st.sampled_from(['1.0', '2.0']))} + {d} * {d}))"
+        return f"({lhs} {op} {expr(depth - 1, allow)})"
+
+    nstmts = draw(st.integers(2, 6))
+    for _ in range(nstmts):
+        kind_ = draw(st.sampled_from(["point", "point", "stencil", "inplace", "copy", "fill", "accv", "accs", "gather"]
+                                     + (["indirect"] if use_idx else [])))
+        dst = draw(st.sampled_from(temps))
+        others = [t for t in temps if t != dst]
+        if kind_ == "point":
+            op = draw(st.sampled_from(["=", "+=", "-="]))
+            lines.append(f"    parallel_for i in 0..extent(a, 0) {{ {dst}(i) {op} {expr(2, temps)}; }}")
+        elif kind_ == "stencil":
+            src = draw(st.sampled_from(["a", "b"] + others))
+            w1, w2 = draw(st.sampled_from(LITS)), draw(st.sampled_from(LITS))
+            lines.append(f"    parallel_for i in 0..extent(a, 0) {{ {dst}(i) = {src}(i); "
+                         f"if (i != 0) {{ {dst}(i) += {w1} * {src}(i - 1); }} "
+                         f"if (i != extent(a, 0) - 1) {{ {dst}(i) -= {w2} * {src}(i + 1); }} }}")
+        elif kind_ == "inplace":
+            lines.append(f"    parallel_for i in 0..extent(a, 0) {{ a(i) = {draw(st.sampled_from(LITS))} * a(i) + b(i); }}")
+        elif kind_ == "copy" and others:
+            lines.append(f"    deep_copy({dst}, {draw(st.sampled_from(others + ['a']))});")
+        elif kind_ == "fill":
+            lines.append(f"    deep_copy({dst}, {draw(st.sampled_from(LITS + scalars))});")
+        elif kind_ == "accv":
+            lines.append(f"    parallel_sum({dst}, {draw(st.sampled_from(others + ['a', 'b']))});")
+        elif kind_ == "accs":
+            lines.append(f"    parallel_sum({dst}, {draw(st.sampled_from(LITS + scalars))});")
+        elif kind_ == "gather":
+            name = f"s{len(scalars)}"
+            lines.append(f"    {name} = parallel_sum({draw(st.sampled_from(temps + ['a']))});")
+            scalars.append(name)
+        elif kind_ == "indirect":
+            lines.append(f"    parallel_for i in 0..extent(idx, 0) {{ {dst}(i) = a(idx(i)) * {draw(st.sampled_from(LITS))} + b(i); }}")
+    ret = draw(st.sampled_from(temps))
+    tail = f"    r = parallel_sum({ret});\n    return r" + (f" + {scalars[0]} * 0.5" if scalars and draw(st.booleans()) else "") + ";"
+    text = "fn f(" + ", ".join(params) + ") -> f64 {\n" + "\n".join(lines) + "\n" + tail + "\n}\n"
+    return text, use_idx, use_c
+
+
+def _inputs(n, use_idx, use_c, seed):
+    rng = np.random.default_rng(seed)
+    d = {"a": rng.normal(size=n), "b": rng.normal(size=n)}
+    if use_idx:
+        d["idx"] = rng.integers(0, n, size=n).astype(np.float64)
+    if use_c:
+        d["c"] = 0.75
+    return d
+
+
+def _close(got, want, atomic):
+    if not atomic:
+        assert_bits(got, want)
+        return
+    scale = max(1.0, float(np.max(np.abs(want)))) if np.size(want) else 1.0
+    assert np.all(np.abs(np.asarray(got) - np.asarray(want)) <= 1e-11 * scale)
+
+
+@settings(max_examples=int(__import__("os").environ.get("KRN_FUZZ", "60")), deadline=None, suppress_health_check=list(HealthCheck))
+@given(programs(), st.sampled_from([1, 2, 5, 33, 130, 1030]), st.integers(0, 10**6))
+def test_random_programs_match_the_oracle(prog, n, seed):
+    from oracle import interp
+
+    text, use_idx, use_c = prog
+    try:
+        program = krn.parse(text)
+    except (krn.ParseError, krn.ValidationError):
+        assume(False)
+    inputs = _inputs(n, use_idx, use_c, seed)
+    want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+    with np.errstate(all="ignore"):
+        wv = interp.run(program, "f", want)
+    for policy in ("compiled", "statements"):
+        got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+        value = krn.execute(program, "f", got, ExecutionConfig(policy=policy)).value
+        assert_bits(value, wv, f"{policy} value\n{text}")
+        for k, v in got.items():
+            if isinstance(v, ViewStorage):
+                assert_bits(v.buffer, want[k], f"{policy} {k}\n{text}")
+    # gradient
+    try:
+        import warnings
+
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            gp = krn.differentiate(program, "f", ("a", "b"))
+    except krn.NotFeasible:
+        return
+    gfn = gp.functions[-1]
+    shadows = [p.name for p in gfn.params[len(program.functions[0].params):]]
+    want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+    for s in shadows:
+        want[s] = np.zeros(n)
+    with np.errstate(all="ignore"):
+        interp.run(gp, gfn.name, want)
+    atomic = use_idx and "idx(i)" in text
+    for policy in ("compiled", "statements"):
+        got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
+        for s in shadows:
+            got[s] = ViewStorage.zeros(s, (n,))
+        krn.execute(gp, gfn.name, got, ExecutionConfig(policy=policy))
+        for k, v in got.items():
+            if isinstance(v, ViewStorage):
+                try:
+                    _close(v.buffer, want[k], atomic and k.startswith("_d_"))
+                except AssertionError as e:
+                    raise AssertionError(f"{policy} grad {k} n={n}\n{text}\n{krn.emit(gfn)}\n{e}") from None
