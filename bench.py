@@ -373,6 +373,7 @@ def statements_large_n(krn, dev, torch, rows, policy="statements"):
     for v in base.values():
         v.device_ptr(dev, write=False)
     cfg = krn.ExecutionConfig(policy=policy, synchronous=False, device=dev)
+    flush = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
     tp, tg = [], []
     for rep in range(4):
         for which in ("primal", "grad"):
@@ -382,6 +383,8 @@ def statements_large_n(krn, dev, torch, rows, policy="statements"):
                 call["_d_b"] = ViewStorage.zeros("_d_b", (rows,))
             dev.sync()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(6):  # ~0.5 ms of device work ahead of e0: the host enqueues behind it
+                flush.zero_()
             e0.record()
             krn.execute(lap if which == "primal" else gp, FN if which == "primal" else FN + "_grad", call, cfg)
             e1.record()
