@@ -328,6 +328,7 @@ def main():
             "compulsory_bytes_accumulate": GRAD_BYTES_PER_ROW / PRIMAL_BYTES_PER_ROW,
             "compulsory_bytes_zero_shadows": GRAD_ZERO_BYTES_PER_ROW / PRIMAL_BYTES_PER_ROW,
         }
+        line["sweep"] = sweep(dev, torch)
         line["statements_policy_large_n"] = stm
         line["compiled_policy_large_n"] = cmp_
         line["e2e"] = end_to_end(krn, dev, rows, world)
@@ -345,6 +346,51 @@ def main():
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def sweep(dev, torch):
+    """BASELINE configs[2]: the fused kernels from 1e6 to 1e9 rows on one GPU (device time,
+    accumulate-shadow gradient = 56 B/row, primal = 24 B/row)."""
+    from paper_2507_13204_b200 import _cabi
+
+    out = []
+    peak, _ = measured_peaks()
+    for n in (1_000_000, 10_000_000, 100_000_000, 1_000_000_000):
+        free, _total = torch.cuda.mem_get_info()
+        if 5 * 8 * n + (2 << 30) > free:
+            out.append({"rows": n, "skipped": "not enough free device memory"})
+            continue
+        bufs = [torch.rand(n, dtype=torch.float64, device="cuda") * 2.0 - 1.0 for _ in range(4)]
+        x, b, dx, db = bufs
+        xo = torch.empty_like(x)
+        f = torch.zeros(1, dtype=torch.float64, device="cuda")
+        P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        flush = torch.empty(1 << 28, dtype=torch.uint8, device="cuda") if n < 20_000_000 else None
+
+        def run(fn, reps=8):
+            ts = []
+            for _ in range(reps):
+                if flush is not None:
+                    flush.zero_()  # Views below L2 size: evict them between repetitions
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return min(ts[2:])
+
+        tp = run(lambda: _cabi.check(dev.lib.krn_laplacian_primal(dev.h, P(x), P(xo), P(b), n, 0, n, None, P(f), 0)))
+        tg = run(lambda: _cabi.check(dev.lib.krn_laplacian_grad(dev.h, P(x), P(xo), P(b), P(dx), P(db), 0, 0, n, 0, n,
+                                                                 None, 1.0)))
+        out.append({"rows": n, "primal_ms": tp, "grad_ms": tg, "ratio": tg / tp,
+                    "primal_gbs": 24.0 * n / tp / 1e6, "grad_gbs": 56.0 * n / tg / 1e6,
+                    "grad_frac_of_measured_peak": 56.0 * n / tg / 1e6 / peak,
+                    "grad_entries_per_s": 2.0 * n / tg * 1e3,
+                    "l2": "flushed between repetitions" if flush is not None else "Views exceed L2"})
+        del bufs, x, b, dx, db, xo, flush
+        torch.cuda.empty_cache()
+    return out
 
 
 def profiled_traffic(rows):

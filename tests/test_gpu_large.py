@@ -1,0 +1,76 @@
+"""GPU tier, maximum size of the bandwidth sweep (BASELINE configs[2]): 10^9 rows on one
+device (40 GB of Views).  The inputs come from an integer formula that host and device
+evaluate identically, so sampled windows - both ends, block and chunk boundaries, the
+4 GiB byte-offset boundary - are checked bit for bit against the C oracle, and the
+objective against an independent device-side sum."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import _cabi
+from conftest import assert_bits
+
+pytestmark = pytest.mark.gpu
+N = 1_000_000_000
+
+
+def _formula_np(lo, hi, mult, mod):
+    j = np.arange(lo, hi, dtype=np.int64)
+    # only exact operations (integer arithmetic, scaling by a power of two, one subtraction), so
+    # numpy and torch-on-CUDA produce the same bits (torch turns `/ scalar` into `* (1/scalar)`)
+    return ((j * mult) % mod).astype(np.float64) * 2.0 ** -19 - 1.0
+
+
+def _formula_torch(n, mult, mod, out):
+    step = 1 << 26
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        j = torch.arange(lo, hi, dtype=torch.int64, device="cuda")
+        out[lo:hi] = ((j * mult) % mod).to(torch.float64) * 2.0 ** -19 - 1.0
+    return out
+
+
+def test_one_billion_rows():
+    from oracle import cport
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 56 * (1 << 30):
+        pytest.skip("needs 56 GB of free device memory")
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    dev = krn.Device(0, s.cuda_stream)
+    x = _formula_torch(N, 2654435761, 1048573, torch.empty(N, dtype=torch.float64, device="cuda"))
+    b = _formula_torch(N, 40503, 1048571, torch.empty(N, dtype=torch.float64, device="cuda"))
+    xo, dx, db = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    f = torch.zeros(1, dtype=torch.float64, device="cuda")
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _cabi.check(dev.lib.krn_laplacian_primal(dev.h, P(x), P(xo), P(b), N, 0, N, None, P(f), 0))
+    _cabi.check(dev.lib.krn_laplacian_grad(dev.h, P(x), P(xo), P(b), P(dx), P(db), 1, 1, N, 0, N, None, 1.0))
+    torch.cuda.synchronize()
+    # objective: independent evaluation with torch ops (different summation order)
+    xs = 3.0 * x
+    y = 2.0 * xs - b
+    y[1:] -= xs[:-1]
+    y[:-1] -= xs[1:]
+    f_ref = float(torch.sum(y * y).item())
+    assert abs(float(f.item()) - f_ref) <= 1e-12 * abs(f_ref)
+    assert torch.equal(xo, xs)
+    del xs, y
+    # windows, bit for bit against the oracle
+    w = 4096
+    starts = [0, N - w, (1 << 29) - w // 2, 8192 * 1000 - 7, 536_870_912 - 2, 123_456_789, N // 2 + 1]
+    for lo in starts:
+        lo = max(0, min(lo, N - w))
+        hi = lo + w
+        xa, ba = _formula_np(lo, hi, 2654435761, 1048573), _formula_np(lo, hi, 40503, 1048571)
+        assert_bits(x[lo:hi].cpu().numpy(), xa, "input formula")  # host and device agree on the inputs
+        dxo, dbo = np.zeros(w), np.zeros(w)
+        cport.laplacian_grad(xa.copy(), ba, dxo, dbo, 1.0)
+        a = 0 if lo == 0 else 2           # rows whose stencil support lies inside the window
+        z = w if hi == N else w - 2
+        assert_bits(dx[lo + a:lo + z].cpu().numpy(), dxo[a:z], f"_d_x window {lo}")
+        assert_bits(db[lo + a:lo + z].cpu().numpy(), dbo[a:z], f"_d_b window {lo}")
