@@ -196,7 +196,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=DEFAULT_ROWS, help="rows per GPU")
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=env_int("KRN_BENCH_ROWS", DEFAULT_ROWS),
+                    help="rows per GPU (under torchrun spell it --rows: its parser claims --n)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-extras", action="store_true", help="only the main line (used under ncu)")
     args = ap.parse_args()
@@ -213,12 +214,20 @@ def main():
     from paper_2507_13204_b200 import _cabi
     from paper_2507_13204_b200.sharded import ShardedLaplacian
 
+    # KRN_BENCH_BACKEND=gloo lets several ranks share one GPU (NCCL refuses that): used to rehearse
+    # the N>1 launch contract on a single-GPU box; the real runs use NCCL, one rank per GPU
+    backend = os.environ.get("KRN_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     work_stream = torch.cuda.Stream()  # non-default: handle 0 would mean "make a private stream"
     torch.cuda.set_stream(work_stream)
     stream = work_stream.cuda_stream
@@ -309,6 +318,17 @@ def main():
         "gpu_launches": grad_launches,
         "clocks": clocks,
     }
+    if not args.skip_extras:
+        # every rank moves its own shard over its own PCIe link at the same time; the slowest rank counts
+        e2e = end_to_end(krn, dev, rows, world, barrier)
+        if dist is not None:
+            t = torch.tensor([e2e["seconds_per_step"], e2e["plain"]["seconds_per_step"]], dtype=torch.float64,
+                             device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["seconds_per_step"], e2e["plain"]["seconds_per_step"] = float(t[0]), float(t[1])
+            e2e["value"] = 2.0 * rows * world / e2e["seconds_per_step"]
+            e2e["plain"]["entries_per_s"] = 2.0 * rows * world / e2e["plain"]["seconds_per_step"]
+        line["e2e"] = e2e
     if rank == 0 and not args.skip_extras:
         line["headline"] = headline(krn, dev, torch)
         stm = statements_large_n(krn, dev, torch, min(n_local, 1 << 26))
@@ -331,7 +351,6 @@ def main():
         line["sweep"] = sweep(dev, torch)
         line["statements_policy_large_n"] = stm
         line["compiled_policy_large_n"] = cmp_
-        line["e2e"] = end_to_end(krn, dev, rows, world)
         tp, tg = cpu_port_timing(min(rows, 20_000_000))
         crow = min(rows, 20_000_000)
         line["cpu_baseline"] = {"value": 2.0 * crow / tg, "unit": "entries/s", "cores": cpu_threads(),
@@ -498,7 +517,7 @@ def headline(krn, dev, torch):
     return out
 
 
-def end_to_end(krn, dev, rows, world):
+def end_to_end(krn, dev, rows, world, barrier=lambda: None):
     """Same metric through the public API with HOST buffers (pinned): every step the
     host holds fresh x and b, `execute(<fn>_grad)` runs, and _d_x, _d_b are read back
     on the host.  Two flavours:
@@ -530,6 +549,7 @@ def end_to_end(krn, dev, rows, world):
             if mode == "pipelined":
                 hdx.mark_zero()
                 hdb.mark_zero()
+            barrier()
             t0 = time.perf_counter()
             krn.execute(gp, FN + "_grad", {"x": hx, "b": hb, "_d_x": hdx, "_d_b": hdb}, cfg)
             gx, gb = hdx.peek(), hdb.peek()   # host arrays with the result
@@ -541,10 +561,13 @@ def end_to_end(krn, dev, rows, world):
     assert out["plain"]["checksum"] == out["pipelined"]["checksum"]
     return {"value": out["pipelined"]["entries_per_s"], "unit": "entries/s",
             "seconds_per_step": out["pipelined"]["seconds_per_step"],
-            "h2d_bytes_per_step": 2 * 8 * rows, "d2h_bytes_per_step": 2 * 8 * rows, "rows": rows,
-            "plain": dict(out["plain"], h2d_bytes_per_step=4 * 8 * rows, d2h_bytes_per_step=2 * 8 * rows),
+            "h2d_bytes_per_step": 2 * 8 * rows * world, "d2h_bytes_per_step": 2 * 8 * rows * world,
+            "rows": rows * world,
+            "plain": dict(out["plain"], h2d_bytes_per_step=4 * 8 * rows * world,
+                          d2h_bytes_per_step=2 * 8 * rows * world),
             "note": "execute(<fn>_grad, cfg.stream_host_io=True) on pinned host Views: chunked upload of x, b "
-                    "overlapped with the kernels and with the download of _d_x, _d_b (rank 0's shard; PCIe bound)"}
+                    "overlapped with the kernels and with the download of _d_x, _d_b (every rank its own shard at "
+                    "the same time, slowest rank counts; PCIe bound)"}
 
 
 if __name__ == "__main__":
