@@ -137,6 +137,41 @@ def plan_atomics(loop) -> list:
     return sites
 
 
+def guard_interval(guards, counter, trip, sym):
+    """(lo, up): the running index satisfies lo <= i <= n-1-up under `guards`, where n is the
+    trip count (`trip` = its canonical form, `sym` = the canonicaliser)."""
+    lo, up = 0, 0
+    counter_terms = ((("counter", counter), 1),)
+    for c in guards:
+        try:
+            (lc, lt), (rc, rt) = sym(c.lhs), sym(c.rhs)
+        except (TypeError, ValueError):
+            continue
+        op = c.op
+        if rt == counter_terms and lt != counter_terms:  # put the counter on the left
+            (lc, lt), (rc, rt) = (rc, rt), (lc, lt)
+            op = {"<": ">", "<=": ">=", ">": "<", ">=": "<=", "==": "==", "!=": "!="}[op]
+        if lt != counter_terms:
+            continue
+        k_const = rc - lc  # condition reads: i  op  (rt-part) + k_const
+        if not rt:  # compared with a constant
+            if op == "!=" and k_const == lo:
+                lo += 1
+            elif op == ">":
+                lo = max(lo, k_const + 1)
+            elif op == ">=":
+                lo = max(lo, k_const)
+        elif (0, rt) == (0, trip[1]):  # compared with n + k  (same symbolic terms as the trip count)
+            k_rel = k_const - trip[0]  # rhs = n + k_rel
+            if op == "!=" and k_rel == -1 - up:
+                up += 1
+            elif op == "<":
+                up = max(up, -k_rel)
+            elif op == "<=":
+                up = max(up, -k_rel - 1)
+    return lo, up
+
+
 # ---------------------------------------------------------------------------
 # module generation
 
@@ -229,6 +264,10 @@ class ModuleBuilder:
         self.host_scalars = set(host_scalars)
         self.hslots: dict = {}  # host-known scalar -> slot in Env.H
         self.promoted: dict = {}  # view -> register array name, while a tile kernel is generated
+        self.windows: dict = {}  # view -> warp-private shared-memory window (window kernels, tilegen.py)
+        self.stage_windows: dict = {}  # atomic site index -> window name (contribution read by a neighbour row)
+        self.in_tile = False  # a window kernel is being generated
+        self.counter = None  # AST counter of the statement being generated (window kernels)
         self.elide = None  # bounds-check elision context (tile kernels only)
         self.guards: list = []  # enclosing If conditions of the statement being generated
         self.views: list = []  # view table: name -> index
@@ -267,7 +306,18 @@ class ModuleBuilder:
         """Register holding acc's element when its view is promoted in the tile kernel
         being generated (pointwise access by construction)."""
         r = self.promoted.get(acc.view)
-        return f"{r}[e]" if r is not None else None
+        if r is not None:
+            return f"{r}[e]"
+        w = self.windows.get(acc.view)
+        if w is not None:
+            # every access to a window View is `counter + c`, proven in range when the group was formed
+            const = _unit_affine(acc.indices[0], self.counter)
+            if const is None or len(acc.indices) != 1:
+                raise TypeError(f"window view {acc.view} accessed with a non-affine index")
+            if self.elide is not None:
+                self.elide["views"].add(acc.view)
+            return f"{w}[(int)(i + ({const}) - wlo)]"
+        return None
 
     # ---- expressions -----------------------------------------------------------
 
@@ -295,36 +345,7 @@ class ModuleBuilder:
     # every check in place).
     def _range(self):
         el = self.elide
-        lo, up = 0, 0
-        counter_terms = ((("counter", el["counter"]), 1),)
-        for c in self.guards:
-            try:
-                (lc, lt), (rc, rt) = el["sym"](c.lhs), el["sym"](c.rhs)
-            except (TypeError, ValueError):
-                continue
-            op = c.op
-            if rt == counter_terms and lt != counter_terms:  # put the counter on the left
-                (lc, lt), (rc, rt) = (rc, rt), (lc, lt)
-                op = {"<": ">", "<=": ">=", ">": "<", ">=": "<=", "==": "==", "!=": "!="}[op]
-            if lt != counter_terms:
-                continue
-            k_const = rc - lc  # condition reads: i  op  (rt-part) + k_const
-            if not rt:  # compared with a constant
-                if op == "!=" and k_const == lo:
-                    lo += 1
-                elif op == ">":
-                    lo = max(lo, k_const + 1)
-                elif op == ">=":
-                    lo = max(lo, k_const)
-            elif (0, rt) == (0, el["trip"][1]):  # compared with n + k  (same symbolic terms as the trip count)
-                k_rel = k_const - el["trip"][0]  # rhs = n + k_rel
-                if op == "!=" and k_rel == -1 - up:
-                    up += 1
-                elif op == "<":
-                    up = max(up, -k_rel)
-                elif op == "<=":
-                    up = max(up, -k_rel - 1)
-        return lo, up
+        return guard_interval(self.guards, el["counter"], el["trip"], el["sym"])
 
     def _provably_in_range(self, acc) -> bool:
         el = self.elide
@@ -424,7 +445,9 @@ class ModuleBuilder:
             site = sites.get(id(s)) if sites else None
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
-            elif site.mode == "gather" and self.promoted:
+            elif site.mode == "gather" and site.index in self.stage_windows:
+                out.append(head + f"{self.stage_windows[site.index]}[(int)(i - wlo)] = t_; }}")
+            elif site.mode == "gather" and (self.promoted or self.in_tile):
                 out.append(head + f"T{site.index}[e] = t_; }}")  # tile kernel: staging column in registers
             elif site.mode == "gather":
                 out.append(head + f"stage[{site.index} * n + i] = t_; }}")

@@ -72,10 +72,11 @@ def _host_evaluable(e, host_scalars) -> bool:
 
 
 class CompiledPlan:
-    def __init__(self, fn):
+    def __init__(self, fn, windows: bool = True):
         self.fn = fn
         an = self.an = fusion.Analysis(fn)
-        self.schedule = fusion.form_groups(fusion.build_ops(fn, an), an)
+        self.schedule = fusion.form_groups(fusion.build_ops(fn, an), an, windows)
+        self.windowed = any(item[0] == "group" and item[1].windowed for item in self.schedule)
         b = self.builder = codegen.ModuleBuilder(fn, host_scalars=an.host_scalars)
         params = {p.name for p in fn.params if p.is_view}
         self.steps: list = []
@@ -86,8 +87,12 @@ class CompiledPlan:
                 later = set(params)
                 for nxt in self.schedule[idx + 1:]:
                     later |= _views_of(nxt)
-                plan = tilegen.plan_group(b, item[1], an, later)
-                self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan, an)))
+                if item[1].windowed:
+                    plan = tilegen.plan_window_group(b, item[1], an, later)
+                    self.steps.append(("group", item[1], tilegen.window_kernel(b, item[1], f"g{idx}", plan, an)))
+                else:
+                    plan = tilegen.plan_group(b, item[1], an, later)
+                    self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan, an)))
             elif tag == "raw":
                 s = item[1]
                 if kind(s) == "ParallelFor":
@@ -116,12 +121,24 @@ class CompiledPlan:
 _plans: dict = {}
 
 
-def plan_for(fn) -> CompiledPlan:
-    hit = _plans.get(id(fn))
+def plan_for(fn, windows: bool = True) -> CompiledPlan:
+    """Plan of `fn`; with `windows` the halo-recompute fusion is tried first (the plan's
+    `.windowed` says whether any group uses it)."""
+    key = (id(fn), bool(windows))
+    hit = _plans.get(key)
     if hit is not None and hit[0] is fn:
         return hit[1]
-    plan = CompiledPlan(fn)
-    _plans[id(fn)] = (fn, plan)
+    plan = None
+    if windows:
+        try:
+            plan = CompiledPlan(fn, True)
+        except ValueError:
+            plan = None  # shape outside the window kernel: plain tile kernels
+        if plan is not None and not plan.windowed:
+            _plans[(id(fn), False)] = (fn, plan)
+    if plan is None:
+        plan = CompiledPlan(fn, False)
+    _plans[key] = (fn, plan)
     return plan
 
 
@@ -147,8 +164,13 @@ def run(dev, fn, views: dict, scalars: dict, cfg):
     group cannot preserve the reference's error behaviour."""
     from .runtime import _Run, _plan_for
 
-    plan = plan_for(fn)
+    plan = plan_for(fn, cfg.fuse_neighbours)
     r = _CompiledRun(dev, plan, views, scalars, cfg)
+    if not r.dry_check() and plan.windowed:
+        r = _CompiledRun(dev, plan_for(fn, False), views, scalars, cfg)
+        if r.dry_check():
+            return r.go()
+        return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
     if not r.dry_check():
         return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
     return r.go()
@@ -176,6 +198,10 @@ class _CompiledRun:
         def trip(e):
             return int(_index_value(e, {k: _V(v) for k, v in ext.items()}))
 
+        # one storage object bound to two names: registers/windows would hide the aliasing
+        objs = [id(v) for v in self.views.values()]
+        if len(set(objs)) != len(objs):
+            return False
         try:
             for step in self.plan.steps:
                 tag = step[0]
@@ -209,6 +235,9 @@ class _CompiledRun:
                     for v in recipe["elided_views"]:
                         if n > ext[v][0]:
                             return False  # the elided checks assumed extent >= range
+                    for v in recipe.get("alt", ()):
+                        if ext[v][0] > n + recipe["max_shift"]:
+                            return False  # rows the kernel does not cover would be lost in the buffer swap
         except (TypeError, KeyError):
             return False
         return True
@@ -288,11 +317,23 @@ class _CompiledRun:
                 self.do_gather(*g.gather)
             return
         ptrs, zero_mask, n_safe = {}, 0, n
+        alt_bufs: dict = {}
+        alt_views = set(recipe.get("alt", ()))
         for k_, p in enumerate(recipe["promoted"]):
             v = self.views[p["view"]]
             rows = v.extents[0]
             n_safe = min(n_safe, rows)
             zero = bool(v._zero)
+            if p["view"] in alt_views:
+                # out of place: the kernel reads the old buffer (neighbouring warps included) and
+                # writes a fresh one, which the View adopts afterwards
+                alt_bufs[p["view"]] = _DeviceBuffer(dev, v.nbytes)
+                if zero:
+                    zero_mask |= 1 << k_
+                    ptrs[p["view"]] = 0
+                else:
+                    ptrs[p["view"]] = v.device_ptr(dev, write=False)
+                continue
             if zero and p["store"] and rows > n_launch:
                 zero = False  # rows the kernel does not cover must really hold zeros
             if zero:
@@ -312,8 +353,8 @@ class _CompiledRun:
             self.stage[producer] = (buf, ld)
             stage_ptr = buf.ptr
         for loop in g.ops:
-            if loop.what == "apply":
-                buf, ld = self.stage[id(loop.apply_of[2])]
+            if loop.what == "apply" and id(loop.apply_of[2]) in self.stage:
+                buf, ld = self.stage[id(loop.apply_of[2])]  # contributions staged by an earlier launch
                 stage_ptr = buf.ptr
         blocks_items = n_launch
         red_out, acc, partials, scratch, ticket = 0, 0, 0, 0, 0
@@ -343,7 +384,12 @@ class _CompiledRun:
         else:
             extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]
         extra.append(C.c_int(steps))
+        if recipe.get("window"):
+            order = list(recipe["alt"]) + [None] * (fusion.MAX_ALT - len(recipe["alt"]))
+            extra += [C.c_void_p(alt_bufs[v].ptr if v is not None else 0) for v in order]
         self.launch_tile(recipe["name"], nblocks, env, extra)
+        for name, buf in alt_bufs.items():
+            self.views[name]._adopt(buf)
 
     def launch_tile(self, name, nblocks, env_bytes, extra):
         # krn_module_launch sizes a grid-stride grid; tile kernels need exactly ceil(threads/256) blocks

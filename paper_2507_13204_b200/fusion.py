@@ -108,6 +108,199 @@ class LoopOp:
         return out
 
 
+def guarded_accesses(loop: "LoopOp") -> list:
+    """(Access, guards) for every access of a user loop: the enclosing If conditions decide
+    which neighbour reads are provably in range."""
+    out: list = []
+
+    def reads(e, guards):
+        for n in walk_expr(e):
+            if kind(n) == "ViewAccess":
+                out.append((Access(n.view, tuple(n.indices), False), guards))
+
+    def walk(body, guards):
+        for s in body:
+            k = kind(s)
+            if k == "If":
+                walk(s.body, guards + (s.cond,))
+            elif k == "AssignView":
+                out.append((Access(s.target.view, tuple(s.target.indices), True), guards))
+                if s.op != "=":
+                    out.append((Access(s.target.view, tuple(s.target.indices), False), guards))
+                for i in s.target.indices:
+                    reads(i, guards)
+                reads(s.rhs, guards)
+            elif k == "AtomicAdd":
+                out.append((Access(s.target.view, tuple(s.target.indices), True, True), guards))
+                for i in s.target.indices:
+                    reads(i, guards)
+                reads(s.value, guards)
+            elif k == "DeclScalar":
+                reads(s.init, guards)
+            elif k == "AssignScalar":
+                reads(s.rhs, guards)
+
+    walk(loop.body, ())
+    return out
+
+
+def stage_name(index: int, producer) -> str:
+    return f"__stage{index}@{id(producer)}"
+
+
+MAX_HALO = 32      # halo iterations of a warp step are handled by the 32 lanes in one extra slot
+MAX_WINDOWS = 5    # 8 warps x (128 + halo) doubles each: 5 windows stay under 48 KB of static shared memory
+MAX_ALT = 4        # out-of-place output pointers a window kernel accepts
+
+
+@_dc.dataclass
+class Facts:
+    """How one loop (or a whole group) touches one View."""
+
+    pw: bool = True        # every access at exactly the running index
+    wr: bool = False
+    at: bool = False       # direct (non-staged) atomic target
+    affine: bool = True    # every access is `counter + c` on a rank-1 View, writes at c = 0, reads proven in range
+    offsets: frozenset = frozenset()
+    rd: bool = False
+
+    def merged(self, o: "Facts") -> "Facts":
+        return Facts(self.pw and o.pw, self.wr or o.wr, self.at or o.at, self.affine and o.affine,
+                     self.offsets | o.offsets, self.rd or o.rd)
+
+
+def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
+    """view -> Facts; staging columns of gather-mode atomics appear as pseudo views
+    (`stage_name`): written pointwise by the producer, read at -offset by the apply loop."""
+    out: dict = {}
+
+    def note(view, pw, wr, at, affine, c, rd):
+        f = out.get(view, Facts())
+        offs = f.offsets | ({c} if c is not None else set())
+        out[view] = Facts(f.pw and pw, f.wr or wr, f.at or at, f.affine and affine, frozenset(offs), f.rd or rd)
+
+    if loop.what == "apply":
+        view, sites, producer = loop.apply_of
+        note(view, True, True, False, an.rank.get(view) == 1, 0, True)
+        for st in sites:
+            note(stage_name(st.index, producer), st.offset == 0, False, False, True, -st.offset, True)
+        return out
+    try:
+        trip = an.trip(loop.upper)
+    except (TypeError, ValueError):
+        trip = None
+    staged_views = {st.view for st in loop.sites if st.mode == "gather"}
+    for st in loop.sites:
+        if st.mode == "gather":
+            note(stage_name(st.index, loop), True, True, False, True, 0, False)
+    for a, guards in guarded_accesses(loop):
+        if a.atomic and a.view in staged_views:
+            continue
+        pw = _is_pointwise(a, loop.counter)
+        c = codegen._unit_affine(a.indices[0], loop.counter) if len(a.indices) == 1 else None
+        affine = c is not None and an.rank.get(a.view, 1) == 1
+        if affine and c != 0:
+            if a.write or trip is None:
+                affine = False
+            else:
+                lo, up = codegen.guard_interval(guards, loop.counter, trip, an.trip)
+                affine = lo + c >= 0 and c - up <= 0
+        note(a.view, pw, a.write, a.atomic, affine, c if affine else None, not a.write)
+    return out
+
+
+@_dc.dataclass
+class WindowPlan:
+    halo: list            # per op: (lo, hi) iterations it runs beyond the warp's own 128
+    hlo: int              # window geometry: positions [j0 - hlo, j0 + 128 + hhi)
+    hhi: int
+    windowed: list        # Views kept in warp-private shared-memory windows
+    stage_windows: list   # staging pseudo views kept in windows (read by a neighbour row)
+    stage_regs: list      # staging pseudo views kept in registers (read by the same row)
+    halo_views: set       # Views touched by an op that runs on halo iterations
+    phases: list          # op indices, split where a window written by one op is read at an offset by the next
+    facts: dict           # group-level Facts
+
+    @property
+    def needed(self) -> bool:
+        return bool(self.windowed or self.stage_windows or self.stage_regs)
+
+
+def window_plan(ops: list, an: "Analysis"):
+    """Halo-recompute plan for running `ops` back to back in ONE kernel although some View
+    written by one of them is read at a neighbouring index by a later one (stencil after an
+    in-place update, deferred atomics gathered by the rows they land on).  Every warp owns
+    128 consecutive iterations per step and recomputes the few iterations of its neighbours
+    whose results it reads, so no value crosses a warp and no grid-wide barrier is needed.
+    None when the shape is outside what the window kernel supports."""
+    per = [loop_facts(o, an) for o in ops]
+    G: dict = {}
+    for f in per:
+        for v, x in f.items():
+            G[v] = G[v].merged(x) if v in G else x
+    windowed = [v for v, f in G.items() if f.wr and not f.pw and not v.startswith("__stage")]
+    for v in windowed:
+        f = G[v]
+        if not f.affine or f.at or an.rank.get(v) != 1:
+            return None
+    stage_w, stage_r = [], []
+    for v, f in G.items():
+        if v.startswith("__stage") and f.wr and f.rd:   # producer and apply loop in the same group
+            (stage_r if f.pw else stage_w).append(v)
+    promoted = {v for v, f in G.items() if f.pw and not f.at and an.rank.get(v, 1) == 1}
+    in_kernel = promoted | set(windowed) | set(stage_w) | set(stage_r)
+    m = len(ops)
+    H = [[0, 0] for _ in ops]
+    for k in range(m - 1, -1, -1):
+        hlo, hhi = H[k]
+        for v, f in per[k].items():
+            if not f.rd or v not in in_kernel:
+                continue
+            for c in (f.offsets or {0}):
+                for p in range(k):
+                    if v in per[p] and per[p][v].wr:
+                        H[p][0] = max(H[p][0], hlo - c)
+                        H[p][1] = max(H[p][1], hhi + c)
+    HLO = max(h[0] for h in H)
+    HHI = max(h[1] for h in H)
+    halo_views: set = set()
+    for k, (hlo, hhi) in enumerate(H):
+        if hlo == 0 and hhi == 0:
+            continue
+        # an op that runs on halo iterations must leave no trace outside registers and windows
+        if any(st.mode != "gather" for st in ops[k].sites):
+            return None
+        for v, f in per[k].items():
+            if f.wr and v not in in_kernel:
+                return None
+            if False:
+                return None  # its apply loop runs in another launch: contributions must be stored exactly once
+            halo_views.add(v)
+    for k, (hlo, hhi) in enumerate(H):
+        for v, f in per[k].items():
+            if v in windowed or v in stage_w:
+                for c in f.offsets:
+                    HLO, HHI = max(HLO, hlo - c), max(HHI, hhi + c)
+    if HLO + HHI > MAX_HALO or len(windowed) + len(stage_w) > MAX_WINDOWS:
+        return None
+    # phases: a __syncwarp() separates an op from an earlier one when a window carries a value
+    # between different lanes (read-after-write or write-after-read at a non-zero offset)
+    phases, cur, written, read_off = [], [], set(), set()
+    for k in range(m):
+        reads_k = {v for v, f in per[k].items() if (v in windowed or v in stage_w) and f.rd and any(c != 0 for c in f.offsets)}
+        writes_k = {v for v, f in per[k].items() if (v in windowed or v in stage_w) and f.wr}
+        if cur and ((reads_k & written) or (writes_k & read_off)):
+            phases.append(cur)
+            cur, written, read_off = [], set(), set()
+        cur.append(k)
+        written |= writes_k
+        read_off |= reads_k
+    if cur:
+        phases.append(cur)
+    return WindowPlan([tuple(h) for h in H], HLO, HHI, sorted(windowed), sorted(stage_w), sorted(stage_r),
+                      halo_views, phases, G)
+
+
 def _is_pointwise(acc: Access, counter: str) -> bool:
     return len(acc.indices) == 1 and kind(acc.indices[0]) == "Counter" and acc.indices[0].name == counter
 
@@ -118,6 +311,7 @@ class Group:
     gather: object = None  # (ParallelSum stmt, accumulate) fused at the end
     promoted: dict = _dc.field(default_factory=dict)  # view -> dict(load=, store=, written=)
     name: str = ""
+    windowed: bool = False  # formed through window_plan: runs as a window kernel (tilegen.window_kernel)
 
 
 class Analysis:
@@ -298,9 +492,10 @@ def _reads_scalar(group: "Group", name: str) -> bool:
     return False
 
 
-def form_groups(ops: list, an: Analysis) -> list:
+def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
     """Greedy left-to-right grouping.  Returns a schedule of
-    ('group', Group) | the non-loop ops unchanged."""
+    ('group', Group) | the non-loop ops unchanged.  `windows`: also merge across
+    neighbour dependencies when a halo-recompute plan exists (window_plan)."""
     schedule: list = []
     cur = None  # (Group, trip, access summary)
 
@@ -377,19 +572,31 @@ def form_groups(ops: list, an: Analysis) -> list:
             producer = loop.what == "kernel" and any(st.mode == "gather" for st in loop.sites)
             has_producer = any(o.what == "kernel" and any(st.mode == "gather" for st in o.sites) for o in g.ops)
             has_apply = any(o.what == "apply" for o in g.ops)
+            classic = ok and not g.windowed
             if (producer and (has_producer or has_apply)) or (loop.what == "apply" and (has_producer or has_apply)):
-                ok = False
-            if ok:
+                classic = False
+            if classic:
                 for v, (pw, wr, at) in acc.items():
                     if v in gacc:
                         gpw, gwr, gat = gacc[v]
                         if at or gat:
-                            ok = False
+                            classic = False
                         elif (wr or gwr) and not (pw and gpw):
-                            ok = False
-                    if not ok:
+                            classic = False
+                    if not classic:
                         break
-            if ok:
+            merged = classic
+            if ok and not classic and windows:
+                # halo recompute: the contributions of a producer reach their apply loop through
+                # warp-private windows, so the pair may share a kernel; still one producer per group,
+                # and an apply loop only next to its own producer
+                allowed = not (producer and (has_producer or has_apply))
+                if loop.what == "apply" and (has_producer or has_apply):
+                    allowed = any(o is loop.apply_of[2] for o in g.ops)
+                if allowed and window_plan(g.ops + [loop], an) is not None:
+                    merged = True
+                    g.windowed = True
+            if merged:
                 g.ops.append(loop)
                 for v, (pw, wr, at) in acc.items():
                     e = gacc.setdefault(v, [True, False, False])

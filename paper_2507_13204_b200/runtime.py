@@ -430,6 +430,10 @@ class ExecutionConfig:
     # "red" hardware fp64 reductions, "warp" warp-aggregated, "smem" block-privatised in shared
     # memory (targets of <= 6144 elements), "auto" = smem for small hot targets, else red
     atomic_policy: str = "auto"
+    # fusion pass: also merge statements across neighbour dependencies (a stencil after an in-place
+    # update, deferred atomics and the rows they land on) by recomputing the few halo iterations
+    # each warp needs (tilegen.window_kernel); False = only pointwise fusion
+    fuse_neighbours: bool = True
 
     def __post_init__(self):
         if self.threads < 1:

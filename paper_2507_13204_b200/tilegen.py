@@ -257,3 +257,267 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
                 gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct)
+
+
+# ---------------------------------------------------------------------------------------
+# window kernels: groups whose statements exchange values between NEIGHBOURING iterations
+# (fusion.window_plan).  Same decomposition as the strided tile kernel - a warp owns 128
+# consecutive iterations per step, lane L takes L, L+32, L+64, L+96 - plus one extra slot
+# (e = 4) in which the first HLO + HHI lanes re-run the iterations just outside the warp's
+# 128 whose results the warp reads.  Views written by one statement and read at i + c by a
+# later one live in a warp-private shared-memory window [j0 - HLO, j0 + 128 + HHI); pointwise
+# Views stay in registers (5 per lane instead of 4).  No value crosses a warp, so there is no
+# block or grid barrier: __syncwarp() between phases is all.  A View that is loaded on halo
+# positions and stored by the kernel is written OUT OF PLACE (`alt` pointers; the host swaps
+# the buffers afterwards) because the neighbouring warp may still need the old contents.
+
+
+def plan_window_group(builder, group, an, live_after: set) -> dict:
+    from . import fusion
+
+    wp = fusion.window_plan(group.ops, an)
+    if wp is None:
+        raise ValueError("group has no window plan")
+    G = wp.facts
+    full_range = {id(l) for l in group.ops if l.shift == 0}
+    if group.gather is not None and group.gather[0].src not in G:
+        G[group.gather[0].src] = fusion.Facts(rd=True)
+    promoted, windows = [], []
+    for v, f in G.items():
+        if v.startswith("__stage"):
+            continue
+        is_window = v in wp.windowed
+        if not is_window and not (f.pw and builder.rank.get(v) == 1 and not f.at):
+            continue
+        load = not _first_access_is_full_store(group, v, full_range)
+        store = f.wr and (v in live_after)
+        halo = v in wp.halo_views
+        rec = dict(view=v, load=load, store=store, written=f.wr, halo=halo,
+                   alt=bool(load and store and (halo or is_window)))
+        (windows if is_window else promoted).append(rec)
+    if sum(1 for r in promoted + windows if r["alt"]) > fusion.MAX_ALT:
+        raise ValueError("too many out-of-place outputs")
+    stage_cols = []  # columns that travel through global memory (apply loop in another launch)
+    for loop in group.ops:
+        if loop.what == "kernel":
+            for st in loop.sites:
+                name = fusion.stage_name(st.index, loop)
+                if st.mode == "gather" and name not in wp.stage_windows and name not in wp.stage_regs:
+                    stage_cols.append((id(loop), st.index))
+    return dict(promoted=promoted, windows=windows, stage_cols=stage_cols, wp=wp,
+                max_shift=max(l.shift for l in group.ops), strided=True, window=True)
+
+
+def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
+    from . import fusion
+
+    b, wp = builder, plan["wp"]
+    promoted, windows = plan["promoted"], plan["windows"]
+    elided: set = set()
+    HLO, HHI = wp.hlo, wp.hhi
+    WN = 128 + HLO + HHI
+    regs = {p["view"]: f"P{b.vid(p['view'])}" for p in promoted}
+    wins = {p["view"]: f"W{b.vid(p['view'])}" for p in windows}
+    # zero_mask bits / alt pointers: promoted first, then windows
+    bit = {p["view"]: k for k, p in enumerate(promoted + windows)}
+    alts = [p["view"] for p in promoted + windows if p["alt"]]
+    outp = {v: f"alt{k}" for k, v in enumerate(alts)}
+    stage_win, stage_reg_sites, stage_win_sites = {}, set(), {}
+    for loop in group.ops:
+        if loop.what != "kernel":
+            continue
+        for st in loop.sites:
+            nm = fusion.stage_name(st.index, loop)
+            if nm in wp.stage_windows:
+                stage_win_sites[st.index] = f"TW{st.index}"
+            elif nm in wp.stage_regs or (id(loop), st.index) in plan["stage_cols"]:
+                stage_reg_sites.add(st.index)
+    gather = group.gather
+    direct = sorted({st.view for l in group.ops for st in l.sites if st.mode == "atomic"})
+    L: list = []
+    w = L.append
+    w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
+      "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
+      "unsigned int *ticket, double *red_out, int accumulate, int steps, double *alt0, double *alt1, "
+      "double *alt2, double *alt3)")
+    w("{")
+    w("    (void)alt0; (void)alt1; (void)alt2; (void)alt3;")
+    w("    const int lane_ = threadIdx.x & 31, warp_ = threadIdx.x >> 5;")
+    for v, wn in list(wins.items()) + [(None, t) for t in stage_win_sites.values()]:
+        w(f"    __shared__ double {wn}_[8][{WN}];")
+        w(f"    double *{wn} = {wn}_[warp_];")
+    if direct:
+        w("    krn_priv_begin(E);")
+    w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + warp_) * 128 * steps;")
+    w("    double tstack[6];  // binary-counter tree over the warp's steps")
+    w("    int tdepth = 0;")
+    w("    (void)tstack; (void)tdepth;")
+    w("    for (int t = 0; t < steps; ++t) {")
+    w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first own iteration of this step")
+    w(f"    const krn_i64 wlo = j0 - {HLO};                // iteration held by window position 0")
+    w("    const bool full = j0 + 128 <= n_safe;")
+    w("    const bool live = j0 < n_launch;")
+    w("    krn_i64 it_[5]; bool act_[5];")
+    w("    for (int e = 0; e < 4; ++e) { it_[e] = j0 + e * 32 + lane_; act_[e] = live && it_[e] < n_launch; }")
+    w(f"    it_[4] = lane_ < {HLO} ? wlo + lane_ : j0 + 128 + (lane_ - {HLO});")
+    w(f"    act_[4] = live && lane_ < {HLO + HHI} && it_[4] >= 0 && it_[4] < n_launch;")
+    w("#define KRN_IT(e) it_[e]")
+    # ---- prologue: registers ------------------------------------------------------------
+    for p in promoted:
+        r, v = regs[p["view"]], b.vid(p["view"])
+        slots = 5 if p["halo"] else 4
+        w(f"    double {r}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
+        if p["load"]:
+            w(f"    if (live && !(zero_mask & {1 << bit[p['view']]}u)) {{")
+            w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][it_[e]]; }}")
+            w(f"        else {{ for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {r}[e] = E.v[{v}][it_[e]]; }}")
+            if slots == 5:
+                w(f"        if (act_[4] && it_[4] < E.e0[{v}]) {r}[4] = E.v[{v}][it_[4]];")
+            w("    }")
+    for idx in sorted(stage_reg_sites):
+        w(f"    double T{idx}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
+    # ---- prologue: windows ------------------------------------------------------------------
+    any_window_load = False
+    for p in windows:
+        if not p["load"]:
+            continue
+        any_window_load = True
+        wn, v = wins[p["view"]], b.vid(p["view"])
+        w(f"    if (live) {{")
+        w(f"        const bool z_ = (zero_mask & {1 << bit[p['view']]}u) != 0u;")
+        w(f"        for (int q = lane_; q < {WN}; q += 32) {{")
+        w("            const krn_i64 g_ = wlo + q;")
+        w(f"            {wn}[q] = (!z_ && g_ >= 0 && g_ < E.e0[{v}] && g_ < n_launch) ? E.v[{v}][g_] : 0.0;")
+        w("        }")
+        w("    }")
+    if any_window_load:
+        w("    __syncwarp();")
+    # ---- phases ---------------------------------------------------------------------------------
+    b.promoted, b.windows, b.stage_windows, b.in_tile = regs, wins, stage_win_sites, True
+    try:
+        for phase in wp.phases:
+            slots = 5 if any(wp.halo[k] != (0, 0) for k in phase) else 4
+            w("    if (live) {")
+            w("#pragma unroll")
+            w(f"    for (int e = 0; e < {slots}; ++e) {{")
+            w("        if (!act_[e]) continue;")
+            w("        const krn_i64 i = it_[e];")
+            w("        bool bad = false;")
+            for k in phase:
+                loop = group.ops[k]
+                hlo, hhi = wp.halo[k]
+                conds = []
+                if slots == 5:
+                    conds.append("(e < 4 || (i >= j0 - %d && i < j0 + 128 + %d))" % (hlo, hhi) if (hlo or hhi)
+                                 else "e < 4")
+                if loop.what == "apply":
+                    view, sites, producer = loop.apply_of
+                    v = b.vid(view)
+                    order = sorted(sites, key=lambda st: (-st.offset, st.index))
+                    conds += [f"i < n + {loop.shift}", f"i < E.e0[{v}]"]
+                    w(f"        if ({' && '.join(conds)}) {{  // deferred atomic adds landing on row i, reference order")
+                    if view in regs:
+                        tgt = f"{regs[view]}[e]"
+                    elif view in wins:
+                        tgt = f"{wins[view]}[(int)(i - wlo)]"
+                    else:
+                        tgt = f"E.v[{v}][i]"
+                    w(f"            double acc = {tgt};")
+                    for st in order:
+                        guard = " && ".join(["i >= 0", "i < n"] + [b.compare(g, {producer.counter}) for g in st.guards])
+                        nm = fusion.stage_name(st.index, producer)
+                        if nm in wp.stage_windows:
+                            src = f"TW{st.index}[(int)(i - wlo)]"
+                        elif nm in wp.stage_regs:
+                            src = f"T{st.index}[e]"
+                        else:
+                            src = f"stage[{st.index} * ld + i]"
+                        w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); "
+                          f"if ({guard}) acc = acc + {src}; }} }}")
+                    w(f"            {tgt} = acc;")
+                    w("        }")
+                    continue
+                sites = {id(st.stmt): st for st in loop.sites}
+                body: list = []
+                local = {loop.counter}
+                b.counter = loop.counter
+                try:
+                    b.elide = dict(counter=loop.counter, trip=an.trip(loop.upper), sym=an.trip, views=elided)
+                except (TypeError, ValueError):
+                    b.elide = None
+                try:
+                    for s in loop.body:
+                        b.element(s, local, body, "            ", sites, True)
+                finally:
+                    b.elide = None
+                    b.counter = None
+                if plan["max_shift"]:
+                    conds.append("i < n")
+                # `continue` inside the body must only leave this statement's block
+                w(f"        if ({' && '.join(conds) if conds else 'true'}) do {{")
+                L.extend(x.replace("continue;", "break;") for x in body)
+                w("        } while (0);")
+                w("        if (bad) continue;")
+            w("    }")
+            w("    }")
+            w("    __syncwarp();")
+    finally:
+        b.promoted, b.windows, b.stage_windows, b.in_tile = {}, {}, {}, False
+    # ---- epilogue ---------------------------------------------------------------------------------
+    for p in promoted:
+        if not p["store"]:
+            continue
+        r, v = regs[p["view"]], b.vid(p["view"])
+        dst = outp.get(p["view"], f"E.v[{v}]")
+        w("    if (live) {")
+        w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {dst}[it_[e]] = {r}[e]; }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {dst}[it_[e]] = {r}[e]; }}")
+        w("    }")
+    for p in windows:
+        if not p["store"]:
+            continue
+        wn, v = wins[p["view"]], b.vid(p["view"])
+        dst = outp.get(p["view"], f"E.v[{v}]")
+        w("    if (live) {")
+        w(f"        for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {dst}[it_[e]] = {wn}[(int)(it_[e] - wlo)];")
+        w("    }")
+    for (_, idx) in plan["stage_cols"]:
+        w(f"    if (live) {{ for (int e = 0; e < 4; ++e) if (act_[e]) stage[{idx} * ld + it_[e]] = T{idx}[e]; }}")
+    if gather is not None:
+        src = gather[0].src
+        w("    {")
+        w("        double R[4];")
+        if src in regs:
+            val = f"{regs[src]}[e]"
+        else:
+            val = f"{wins[src]}[(int)(it_[e] - wlo)]"
+        w(f"        for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n);")
+        w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
+        w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
+        w("        int m_ = t;")
+        w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
+        w("        tstack[tdepth++] = node;")
+        w("    }")
+    w("#undef KRN_IT")
+    w("    __syncwarp();")
+    w("    }  // steps")
+    if direct:
+        w("    krn_priv_end(E);")
+    if gather is not None:
+        w("    {")
+        w("        __shared__ double s_warp[8];")
+        w("        if (lane_ == 0) s_warp[warp_] = tstack[0];")
+        w("        __syncthreads();")
+        w("        if (warp_ == 0) { double v = krn_smem_tree(s_warp, 8, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
+        w("        if (krn_last_block(ticket, gridDim.x)) {")
+        w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
+        w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
+        w("        }")
+        w("    }")
+    w("}")
+    b.parts.append("\n".join(L))
+    every = promoted + windows
+    return dict(name=name, promoted=every, stage_cols=plan["stage_cols"], has_stage=bool(plan["stage_cols"]),
+                gather=gather, max_shift=plan["max_shift"],
+                elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct,
+                window=True, alt=alts, hlo=HLO, hhi=HHI)

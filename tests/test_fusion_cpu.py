@@ -13,10 +13,10 @@ def _grad(stem):
     return fn, krn.differentiate(prog, fn.name, wrt).functions[-1]
 
 
-def _shape(fn):
+def _shape(fn, windows=False):
     an = fusion.Analysis(fn)
     out = []
-    for item in fusion.form_groups(fusion.build_ops(fn, an), an):
+    for item in fusion.form_groups(fusion.build_ops(fn, an), an, windows):
         if item[0] == "group":
             g = item[1]
             out.append("G[" + ",".join(o.what for o in g.ops) + ("+gather" if g.gather else "") + "]")
@@ -39,9 +39,51 @@ def test_headline_schedule():
     assert "gather" not in shape
 
 
+def test_headline_schedule_with_halo_recompute():
+    """window_plan: the in-place scale, the stencil, the seed broadcast, the stencil's reversal,
+    the deferred atomics' apply loop and the scale's reversal become ONE kernel; every warp
+    re-runs 2 iterations either side for the scale and 1 for the stencil and its reversal."""
+    fn, g = _grad("laplacian")
+    _, shape = _shape(fn, True)
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel,kernel+gather]"]
+    an, shape = _shape(g, True)
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel,kernel,suminto,kernel,apply,kernel]"]
+    group = [i[1] for i in fusion.form_groups(fusion.build_ops(g, an), an, True) if i[0] == "group"][0]
+    wp = fusion.window_plan(group.ops, an)
+    assert wp.halo == [(2, 2), (1, 1), (1, 1), (1, 1), (0, 0), (0, 0)] and (wp.hlo, wp.hhi) == (2, 2)
+    assert wp.windowed == ["x"]
+    # contributions to _d_x(j +- 1) cross lanes (windows); the one to _d_x(j) stays in a register
+    assert len(wp.stage_windows) == 2 and len(wp.stage_regs) == 1
+    assert wp.phases == [[0], [1, 2, 3], [4, 5]]
+    plan = compiled.plan_for(g, True)
+    assert plan.windowed and plan.launch_count == 1
+    recipe = [s[2] for s in plan.steps if s[0] == "group"][0]
+    views = {p["view"]: p for p in recipe["promoted"]}
+    # x is read on halo rows and stored: out of place; so is _d_b (touched by a halo statement)
+    assert sorted(recipe["alt"]) == ["_d_b", "x"] and not views["_d_x"]["alt"]
+    for v in ("y", "y2", "_d_y", "_d_y2"):
+        assert not views[v]["store"]
+    assert not recipe["stage_cols"]  # nothing staged through global memory
+
+
+def test_window_plan_refuses_side_effects_on_halo_iterations():
+    # the first kernel would have to re-run on halo iterations, but it scatters with hardware atomics
+    p = krn.parse("""fn f(x: view<f64,1>, idx: view<f64,1>, acc: view<f64,1>, y: view<f64,1>) {
+        parallel_for i in 0..extent(x, 0) { x(i) = 2.0 * x(i); atomic_add(acc(idx(i)), 1.0); }
+        parallel_for i in 0..extent(x, 0) { if (i != 0) { y(i) = x(i - 1); } } }""")
+    _, shape = _shape(p.functions[0], True)
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel]", "G[kernel]"]
+    # an unguarded neighbour read cannot be proven in range: no window, two launches, checks kept
+    p = krn.parse("""fn f(x: view<f64,1>, y: view<f64,1>) {
+        parallel_for i in 0..extent(x, 0) { x(i) = 2.0 * x(i); }
+        parallel_for i in 0..extent(x, 0) { y(i) = x(i + 1); } }""")
+    _, shape = _shape(p.functions[0], True)
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel]", "G[kernel]"]
+
+
 def test_promotion_and_dead_stores():
     _, g = _grad("laplacian")
-    plan = compiled.plan_for(g)
+    plan = compiled.plan_for(g, False)
     recipes = [s[2] for s in plan.steps if s[0] == "group"]
     middle = {p["view"]: p for p in recipes[1]["promoted"]}
     # y, y2, _d_y, _d_y2 live and die inside the kernel: never loaded from nor stored to memory

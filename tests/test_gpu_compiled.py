@@ -11,7 +11,8 @@ from paper_2507_13204_b200 import ExecutionConfig, OutOfBounds, ShapeMismatch, V
 from conftest import CORPUS, assert_bits
 
 pytestmark = pytest.mark.gpu
-CFG = ExecutionConfig(policy="compiled")
+CFG = ExecutionConfig(policy="compiled")  # halo-recompute fusion on (the default)
+CFG_POINTWISE = ExecutionConfig(policy="compiled", fuse_neighbours=False)
 ATOMIC_ORDER = {"gather_indirect"}
 
 
@@ -33,9 +34,10 @@ def _views(d):
     return {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in d.items()}
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 255, 1023, 1024, 1025, 4099, 100_003])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 8, 126, 127, 128, 129, 130, 131, 255, 1023, 1024, 1025, 4099, 100_003])
 @pytest.mark.parametrize("stem", CORPUS)
-def test_primal_and_gradient_against_oracle(stem, n):
+@pytest.mark.parametrize("CFG", [CFG, CFG_POINTWISE], ids=["windows", "pointwise"])
+def test_primal_and_gradient_against_oracle(stem, n, CFG):
     from oracle import interp
 
     if n > 5000 and stem == "gather_indirect":
@@ -86,11 +88,12 @@ def test_primal_and_gradient_against_oracle(stem, n):
                 assert_bits(v.buffer, want[k], f"{stem} n={n} prefilled={prefilled} {k}")
 
 
-def test_headline_through_the_fusion_pass_large():
+@pytest.mark.parametrize("CFG", [CFG, CFG_POINTWISE], ids=["windows", "pointwise"])
+@pytest.mark.parametrize("n", [3_000_017, 1 << 20, (1 << 20) + 1, 1_048_704])
+def test_headline_through_the_fusion_pass_large(CFG, n):
     """the generic pass on the headline objective at a bandwidth-bound size, against the C oracle"""
     from oracle import cport
 
-    n = 3_000_017
     rng = np.random.default_rng(4)
     x, b = rng.normal(size=n), rng.normal(size=n)
     lap = krn.load_program("laplacian")
@@ -168,10 +171,13 @@ def test_fewer_launches_than_statements():
     lap = krn.load_program("laplacian")
     gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
     counts = {}
-    for policy in ("statements", "compiled", "fused"):
+    for policy in ("statements", "compiled", "pointwise", "fused"):
         call = {"x": np.ones(5000), "b": np.zeros(5000), "_d_x": ViewStorage.zeros("_d_x", (5000,)),
                 "_d_b": ViewStorage.zeros("_d_b", (5000,))}
         l0 = dev.launches()
-        krn.execute(gp, "normRes1DLaplacianSQ_grad", call, ExecutionConfig(policy=policy))
+        cfg = CFG_POINTWISE if policy == "pointwise" else ExecutionConfig(policy=policy)
+        krn.execute(gp, "normRes1DLaplacianSQ_grad", call, cfg)
         counts[policy] = dev.launches() - l0
-    assert counts["fused"] == 1 and counts["compiled"] == 3 and counts["statements"] >= 9, counts
+    # halo recompute turns the whole generated gradient into one launch, like the hand-written kernel
+    assert counts["fused"] == 1 and counts["compiled"] == 1 and counts["pointwise"] == 3, counts
+    assert counts["statements"] >= 9, counts

@@ -106,6 +106,12 @@ def _inputs(n, use_idx, use_c, seed):
     return d
 
 
+def _cfg(policy):
+    if policy == "pointwise":  # fusion pass without halo recompute
+        return ExecutionConfig(policy="compiled", fuse_neighbours=False)
+    return ExecutionConfig(policy=policy)
+
+
 def _close(got, want, atomic):
     if not atomic:
         assert_bits(got, want)
@@ -128,9 +134,9 @@ def test_random_programs_match_the_oracle(prog, n, seed):
     want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
     with np.errstate(all="ignore"):
         wv = interp.run(program, "f", want)
-    for policy in ("compiled", "statements"):
+    for policy in ("compiled", "pointwise", "statements"):
         got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
-        value = krn.execute(program, "f", got, ExecutionConfig(policy=policy)).value
+        value = krn.execute(program, "f", got, _cfg(policy)).value
         assert_bits(value, wv, f"{policy} value\n{text}")
         for k, v in got.items():
             if isinstance(v, ViewStorage):
@@ -152,11 +158,11 @@ def test_random_programs_match_the_oracle(prog, n, seed):
     with np.errstate(all="ignore"):
         interp.run(gp, gfn.name, want)
     atomic = use_idx and "idx(i)" in text
-    for policy in ("compiled", "statements"):
+    for policy in ("compiled", "pointwise", "statements"):
         got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
         for s in shadows:
             got[s] = ViewStorage.zeros(s, (n,))
-        krn.execute(gp, gfn.name, got, ExecutionConfig(policy=policy))
+        krn.execute(gp, gfn.name, got, _cfg(policy))
         for k, v in got.items():
             if isinstance(v, ViewStorage):
                 try:

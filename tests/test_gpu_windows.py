@@ -1,0 +1,183 @@
+"""GPU parity, halo-recompute fusion (tilegen.window_kernel): statements that exchange
+values between neighbouring iterations run in one kernel, each warp re-running the few
+iterations either side of its own 128 whose results it reads.  Checked bit for bit
+against the CPU oracle at sizes around the warp-step (128), block (1024) and multi-step
+(2^20) boundaries, and against the statement path at bandwidth-bound sizes."""
+
+import numpy as np
+import pytest
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import ExecutionConfig, ViewStorage, compiled, parse
+from conftest import assert_bits
+
+pytestmark = pytest.mark.gpu
+WIN = ExecutionConfig(policy="compiled")
+STMT = ExecutionConfig(policy="statements")
+
+WIDE = """fn f(a: view<f64, 1>, b: view<f64, 1>, c: view<f64, 1>) -> f64 {
+    let t: view<f64, 1> = view("t", extent(a, 0));
+    let u: view<f64, 1> = view("u", extent(a, 0));
+    parallel_for i in 0..extent(a, 0) { a(i) = 0.5 * a(i) + b(i); }
+    parallel_for i in 0..extent(a, 0) {
+        t(i) = a(i);
+        if (i >= 3) { t(i) += 0.25 * a(i - 3); }
+        if (i < extent(a, 0) - 2) { t(i) -= 1.5 * a(i + 2); }
+    }
+    parallel_for i in 0..extent(a, 0) {
+        u(i) = t(i) * t(i);
+        if (i != 0) { u(i) += t(i - 1) * b(i); }
+        if (i != extent(a, 0) - 1) { u(i) -= t(i + 1); }
+    }
+    parallel_for i in 0..extent(a, 0) { c(i) = u(i) - b(i); }
+    return parallel_sum(u);
+}"""
+
+# a window View that is only partly rewritten (guarded), read at an offset, rewritten again
+PARTIAL = """fn f(a: view<f64, 1>, b: view<f64, 1>) -> f64 {
+    let t: view<f64, 1> = view("t", extent(a, 0));
+    parallel_for i in 0..extent(a, 0) { if (i >= 2) { a(i) = a(i) * 3.0; } }
+    parallel_for i in 0..extent(a, 0) { t(i) = b(i); if (i != 0) { t(i) += a(i - 1); } }
+    parallel_for i in 0..extent(a, 0) { a(i) = a(i) - t(i); }
+    parallel_for i in 0..extent(a, 0) { b(i) = t(i); if (i != extent(a, 0) - 1) { b(i) += a(i + 1); } }
+    return parallel_sum(t);
+}"""
+
+# write-after-read across iterations: the stencil must see the OLD neighbours
+WAR = """fn f(a: view<f64, 1>, b: view<f64, 1>) {
+    parallel_for i in 0..extent(a, 0) { b(i) = a(i); if (i != 0) { b(i) += a(i - 1); } }
+    parallel_for i in 0..extent(a, 0) { a(i) = 2.0 * b(i); }
+    parallel_for i in 0..extent(a, 0) { if (i != extent(a, 0) - 1) { b(i) -= a(i + 1); } }
+}"""
+
+# scatter with offsets on both sides, applied to a View the next statement rescales
+SCATTER = """fn f(a: view<f64, 1>, acc: view<f64, 1>) {
+    parallel_for i in 0..extent(a, 0) {
+        if (i >= 2) { atomic_add(acc(i - 2), a(i) * 0.5); }
+        atomic_add(acc(i), a(i));
+        if (i != extent(a, 0) - 1) { atomic_add(acc(i + 1), -a(i)); }
+        atomic_add(acc(i), 0.125);
+    }
+    parallel_for i in 0..extent(a, 0) { acc(i) = acc(i) * a(i); }
+}"""
+
+CASES = {"wide": WIDE, "partial": PARTIAL, "war": WAR, "scatter": SCATTER}
+SIZES = [1, 2, 3, 4, 5, 6, 31, 32, 33, 127, 128, 129, 130, 131, 132, 255, 256, 257, 1023, 1024, 1025, 1027, 2500]
+
+
+def _views(fn, n, rng):
+    return {p.name: rng.normal(size=n) for p in fn.params if p.is_view}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_plan_uses_one_window_kernel(name):
+    fn = parse(CASES[name]).functions[0]
+    plan = compiled.plan_for(fn, True)
+    assert plan.windowed
+    assert sum(1 for s in plan.steps if s[0] in ("group", "kernel")) == 1
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_window_kernels_against_oracle(name, n):
+    from oracle import interp
+
+    prog = parse(CASES[name])
+    fn = prog.functions[0]
+    data = _views(fn, n, np.random.default_rng(7 * n + len(name)))
+    want = {k: v.copy() for k, v in data.items()}
+    wv = interp.run(prog, "f", want)
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"{name} n={n} value")
+    for k in data:
+        assert_bits(got[k].buffer, want[k], f"{name} n={n} {k}")
+
+
+@pytest.mark.parametrize("n", [5, 129, 1030])
+@pytest.mark.parametrize("name", ["wide", "partial"])
+def test_gradients_of_window_programs(name, n):
+    from oracle import interp
+
+    prog = parse(CASES[name])
+    gp = krn.differentiate(prog, "f", ("a", "b"))
+    gfn = gp.functions[-1]
+    data = _views(prog.functions[0], n, np.random.default_rng(n))
+    want = {k: v.copy() for k, v in data.items()}
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    for p in gfn.params[len(prog.functions[0].params):]:
+        want[p.name] = np.zeros(n)
+        got[p.name] = ViewStorage.zeros(p.name, (n,))
+    interp.run(gp, gfn.name, want)
+    krn.execute(gp, gfn.name, got, WIN)
+    for k in want:
+        assert_bits(got[k].buffer, want[k], f"{name} grad n={n} {k}")
+
+
+@pytest.mark.parametrize("n", [(1 << 20) - 1, 1 << 20, (1 << 20) + 1, (1 << 20) + 1024 * 8 + 5, 3_000_017])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_window_kernels_large_against_statement_path(name, n):
+    """multi-step warps (8 steps of 128 rows above 2^20 iterations): the statement path, itself
+    checked against the oracle, is the yardstick"""
+    prog = parse(CASES[name])
+    data = _views(prog.functions[0], n, np.random.default_rng(n % 1000))
+    ref = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    rv = krn.execute(prog, "f", ref, STMT).value
+    gv = krn.execute(prog, "f", got, WIN).value
+    assert_bits(gv, rv, f"{name} n={n} value")
+    for k in data:
+        assert_bits(got[k].buffer, ref[k].buffer, f"{name} n={n} {k}")
+
+
+def test_prefilled_and_longer_views_take_the_safe_route():
+    """a View longer than the range cannot be swapped out of place: the call must still be right
+    (the dry check hands it to the pointwise plan)"""
+    from oracle import interp
+
+    prog = parse(WAR)
+    n = 300
+    rng = np.random.default_rng(3)
+    a, b = rng.normal(size=n), rng.normal(size=n + 7)
+    want = {"a": a.copy(), "b": b.copy()}
+    interp.run(prog, "f", want)
+    got = {"a": ViewStorage.from_values("a", a), "b": ViewStorage.from_values("b", b)}
+    krn.execute(prog, "f", got, WIN)
+    assert_bits(got["a"].buffer, want["a"], "a")
+    assert_bits(got["b"].buffer, want["b"], "b")
+
+
+def test_aliased_arguments_keep_reference_semantics():
+    """one storage object bound to two parameters: registers and windows would hide the aliasing
+    (a = 3a instead of 4a here), so the call runs on the statement path"""
+    from oracle import interp
+
+    src = """fn f(a: view<f64, 1>, b: view<f64, 1>) {
+        parallel_for i in 0..extent(a, 0) { b(i) = a(i) * 2.0; }
+        parallel_for i in 0..extent(a, 0) { a(i) = a(i) + b(i); } }"""
+    prog = parse(src)
+    v = np.random.default_rng(5).normal(size=200)
+    shared = v.copy()
+    interp.run(prog, "f", {"a": shared, "b": shared})
+    assert_bits(shared, 4.0 * v, "oracle aliases")
+    s = ViewStorage.from_values("a", v)
+    krn.execute(prog, "f", {"a": s, "b": s}, WIN)
+    assert_bits(s.buffer, shared, "aliased")
+
+
+def test_repeated_calls_accumulate_like_the_reference():
+    """out-of-place outputs are adopted by the View: a second call must see the first call's result"""
+    from oracle import interp
+
+    lap = krn.load_program("laplacian")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    n = 777
+    rng = np.random.default_rng(9)
+    x, b = rng.normal(size=n), rng.normal(size=n)
+    want = {"x": x.copy(), "b": b.copy(), "_d_x": np.zeros(n), "_d_b": np.zeros(n)}
+    got = {"x": ViewStorage.from_values("x", x), "b": ViewStorage.from_values("b", b),
+           "_d_x": ViewStorage.zeros("_d_x", (n,)), "_d_b": ViewStorage.zeros("_d_b", (n,))}
+    for _ in range(2):
+        interp.run(gp, "normRes1DLaplacianSQ_grad", want)
+        krn.execute(gp, "normRes1DLaplacianSQ_grad", got, WIN)
+    for k in want:
+        assert_bits(got[k].buffer, want[k], k)
