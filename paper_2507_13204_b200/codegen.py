@@ -267,6 +267,7 @@ class ModuleBuilder:
         self.windows: dict = {}  # view -> warp-private shared-memory window (window kernels, tilegen.py)
         self.stage_windows: dict = {}  # atomic site index -> window name (contribution read by a neighbour row)
         self.in_tile = False  # a window kernel is being generated
+        self.interior = None  # dict(counter, trip, sym, lo, up) while an interior warp step is generated
         self.counter = None  # AST counter of the statement being generated (window kernels)
         self.elide = None  # bounds-check elision context (tile kernels only)
         self.guards: list = []  # enclosing If conditions of the statement being generated
@@ -316,7 +317,7 @@ class ModuleBuilder:
                 raise TypeError(f"window view {acc.view} accessed with a non-affine index")
             if self.elide is not None:
                 self.elide["views"].add(acc.view)
-            return f"{w}[(int)(i + ({const}) - wlo)]"
+            return f"{w}[wq + ({const})]"
         return None
 
     # ---- expressions -----------------------------------------------------------
@@ -405,6 +406,14 @@ class ModuleBuilder:
         raise TypeError(f"cannot generate value {k}")
 
     def compare(self, c, local) -> str:
+        if self.interior is not None:
+            # interior warp step (window kernels): every iteration the warp touches lies at least
+            # `lo` rows from the start and `up` rows from the end of the range, so guards of the
+            # forms the interval analysis understands are known to hold
+            el = self.interior
+            lo, up = guard_interval([c], el["counter"], el["trip"], el["sym"])
+            if (lo or up) and lo <= el["lo"] and up <= el["up"]:
+                return "(true)"
         return f"({self.index(c.lhs, local)} {c.op} {self.index(c.rhs, local)})"
 
     # ---- statements ----------------------------------------------------------------
@@ -446,7 +455,7 @@ class ModuleBuilder:
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
             elif site.mode == "gather" and site.index in self.stage_windows:
-                out.append(head + f"{self.stage_windows[site.index]}[(int)(i - wlo)] = t_; }}")
+                out.append(head + f"{self.stage_windows[site.index]}[wq] = t_; }}")
             elif site.mode == "gather" and (self.promoted or self.in_tile):
                 out.append(head + f"T{site.index}[e] = t_; }}")  # tile kernel: staging column in registers
             elif site.mode == "gather":

@@ -81,12 +81,19 @@ class CompiledPlan:
         params = {p.name for p in fn.params if p.is_view}
         self.steps: list = []
         bound = set()
+        fresh: set = set()  # local Views declared so far that no statement has touched: all +0.0
         for idx, item in enumerate(self.schedule):
             tag = item[0]
+            if tag == "declview":
+                fresh.add(item[1].name)
+            elif tag != "group":
+                fresh -= _views_of(item)
             if tag == "group":
                 later = set(params)
                 for nxt in self.schedule[idx + 1:]:
                     later |= _views_of(nxt)
+                item[1].fresh = frozenset(fresh)
+                fresh -= _views_of(item)
                 if item[1].windowed:
                     plan = tilegen.plan_window_group(b, item[1], an, later)
                     self.steps.append(("group", item[1], tilegen.window_kernel(b, item[1], f"g{idx}", plan, an)))

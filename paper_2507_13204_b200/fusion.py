@@ -311,6 +311,7 @@ class Group:
     gather: object = None  # (ParallelSum stmt, accumulate) fused at the end
     promoted: dict = _dc.field(default_factory=dict)  # view -> dict(load=, store=, written=)
     name: str = ""
+    fresh: frozenset = frozenset()  # local Views still untouched (all +0.0) when the group starts
     windowed: bool = False  # formed through window_plan: runs as a window kernel (tilegen.window_kernel)
 
 

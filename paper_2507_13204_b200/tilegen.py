@@ -79,7 +79,8 @@ def plan_group(builder, group, an, live_after: set) -> dict:
     promoted = []
     for v, (pw, written) in accessed.items():
         if pw and builder.rank.get(v) == 1 and v not in direct_atomic:
-            load = not _first_access_is_full_store(group, v, full_range)
+            # a local View nothing has touched yet is +0.0 everywhere: nothing to load
+            load = not _first_access_is_full_store(group, v, full_range) and v not in group.fresh
             store = written and (v in live_after)
             promoted.append(dict(view=v, load=load, store=store, written=written))
     stage_cols = []
@@ -289,7 +290,7 @@ def plan_window_group(builder, group, an, live_after: set) -> dict:
         is_window = v in wp.windowed
         if not is_window and not (f.pw and builder.rank.get(v) == 1 and not f.at):
             continue
-        load = not _first_access_is_full_store(group, v, full_range)
+        load = not _first_access_is_full_store(group, v, full_range) and v not in group.fresh
         store = f.wr and (v in live_after)
         halo = v in wp.halo_views
         rec = dict(view=v, load=load, store=store, written=f.wr, halo=halo,
@@ -308,6 +309,34 @@ def plan_window_group(builder, group, an, live_after: set) -> dict:
                 max_shift=max(l.shift for l in group.ops), strided=True, window=True)
 
 
+def _guard_margins(group, an) -> tuple:
+    """(lo, up): the largest margins any guard of the group needs to be decided statically
+    (`i != 0` -> lo 1, `i < n - 2` -> up 2, ...)."""
+    from . import codegen
+
+    lo = up = 0
+    for loop in group.ops:
+        conds = []
+        if loop.what == "apply":
+            producer = loop.apply_of[2]
+            counter, upper = producer.counter, producer.upper
+            for st in loop.apply_of[1]:
+                conds += list(st.guards)
+        else:
+            counter, upper = loop.counter, loop.upper
+            for s_ in walk_statements(loop.body):
+                if kind(s_) == "If":
+                    conds.append(s_.cond)
+        try:
+            trip = an.trip(upper)
+        except (TypeError, ValueError):
+            continue
+        for c in conds:
+            l, u = codegen.guard_interval([c], counter, trip, an.trip)
+            lo, up = max(lo, l), max(up, u)
+    return lo, up
+
+
 def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     from . import fusion
 
@@ -318,11 +347,12 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     WN = 128 + HLO + HHI
     regs = {p["view"]: f"P{b.vid(p['view'])}" for p in promoted}
     wins = {p["view"]: f"W{b.vid(p['view'])}" for p in windows}
+    in_kernel_views = set(regs) | set(wins)
     # zero_mask bits / alt pointers: promoted first, then windows
     bit = {p["view"]: k for k, p in enumerate(promoted + windows)}
     alts = [p["view"] for p in promoted + windows if p["alt"]]
     outp = {v: f"alt{k}" for k, v in enumerate(alts)}
-    stage_win, stage_reg_sites, stage_win_sites = {}, set(), {}
+    stage_reg_sites, stage_win_sites = set(), {}
     for loop in group.ops:
         if loop.what != "kernel":
             continue
@@ -334,6 +364,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 stage_reg_sites.add(st.index)
     gather = group.gather
     direct = sorted({st.view for l in group.ops for st in l.sites if st.mode == "atomic"})
+    LO, UP = _guard_margins(group, an)
     L: list = []
     w = L.append
     w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
@@ -343,126 +374,187 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     w("{")
     w("    (void)alt0; (void)alt1; (void)alt2; (void)alt3;")
     w("    const int lane_ = threadIdx.x & 31, warp_ = threadIdx.x >> 5;")
-    for v, wn in list(wins.items()) + [(None, t) for t in stage_win_sites.values()]:
+    for wn in list(wins.values()) + list(stage_win_sites.values()):
         w(f"    __shared__ double {wn}_[8][{WN}];")
         w(f"    double *{wn} = {wn}_[warp_];")
+    # which lanes of the halo slot run statement k (it covers [j0 - hlo_k, j0 + 128 + hhi_k))
+    for k, (hlo, hhi) in enumerate(wp.halo):
+        if hlo or hhi:
+            w(f"    const bool h{k}_ = lane_ >= {HLO - hlo} && lane_ < {HLO + hhi};")
     if direct:
         w("    krn_priv_begin(E);")
     w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + warp_) * 128 * steps;")
     w("    double tstack[6];  // binary-counter tree over the warp's steps")
     w("    int tdepth = 0;")
     w("    (void)tstack; (void)tdepth;")
+    w("    int wq_[5];  // window position of each slot's iteration")
+    w(f"    for (int e = 0; e < 4; ++e) wq_[e] = e * 32 + lane_ + {HLO};")
+    w(f"    wq_[4] = lane_ < {HLO} ? lane_ : 128 + lane_;")
     w("    for (int t = 0; t < steps; ++t) {")
     w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first own iteration of this step")
     w(f"    const krn_i64 wlo = j0 - {HLO};                // iteration held by window position 0")
     w("    const bool full = j0 + 128 <= n_safe;")
     w("    const bool live = j0 < n_launch;")
+    w("    // interior step: the whole window lies inside the range, far enough from both ends for every")
+    w("    // index guard to be decided at compile time")
+    w(f"    const bool interior = full && wlo >= {LO} && j0 + {128 + HHI + UP} <= n;")
     w("    krn_i64 it_[5]; bool act_[5];")
     w("    for (int e = 0; e < 4; ++e) { it_[e] = j0 + e * 32 + lane_; act_[e] = live && it_[e] < n_launch; }")
     w(f"    it_[4] = lane_ < {HLO} ? wlo + lane_ : j0 + 128 + (lane_ - {HLO});")
     w(f"    act_[4] = live && lane_ < {HLO + HHI} && it_[4] >= 0 && it_[4] < n_launch;")
-    w("#define KRN_IT(e) it_[e]")
     # ---- prologue: registers ------------------------------------------------------------
     for p in promoted:
         r, v = regs[p["view"]], b.vid(p["view"])
-        slots = 5 if p["halo"] else 4
         w(f"    double {r}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
         if p["load"]:
             w(f"    if (live && !(zero_mask & {1 << bit[p['view']]}u)) {{")
             w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][it_[e]]; }}")
             w(f"        else {{ for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {r}[e] = E.v[{v}][it_[e]]; }}")
-            if slots == 5:
+            if p["halo"]:
                 w(f"        if (act_[4] && it_[4] < E.e0[{v}]) {r}[4] = E.v[{v}][it_[4]];")
             w("    }")
     for idx in sorted(stage_reg_sites):
         w(f"    double T{idx}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
-    # ---- prologue: windows ------------------------------------------------------------------
-    any_window_load = False
+    # window contents: fetched into registers here so that every global load of the step is in
+    # flight before the first one is consumed
+    NQ = (WN + 31) // 32
     for p in windows:
         if not p["load"]:
             continue
-        any_window_load = True
         wn, v = wins[p["view"]], b.vid(p["view"])
-        w(f"    if (live) {{")
-        w(f"        const bool z_ = (zero_mask & {1 << bit[p['view']]}u) != 0u;")
-        w(f"        for (int q = lane_; q < {WN}; q += 32) {{")
-        w("            const krn_i64 g_ = wlo + q;")
-        w(f"            {wn}[q] = (!z_ && g_ >= 0 && g_ < E.e0[{v}] && g_ < n_launch) ? E.v[{v}][g_] : 0.0;")
+        w(f"    double {wn}r[{NQ}];")
+        w("#pragma unroll")
+        w(f"    for (int u = 0; u < {NQ}; ++u) {wn}r[u] = 0.0;")
+        w(f"    if (live && !(zero_mask & {1 << bit[p['view']]}u)) {{")
+        w("        if (interior) {")
+        w("#pragma unroll")
+        w(f"            for (int u = 0; u < {NQ}; ++u) if (lane_ + 32 * u < {WN}) {wn}r[u] = E.v[{v}][wlo + lane_ + 32 * u];")
+        w("        } else {")
+        w("#pragma unroll")
+        w(f"            for (int u = 0; u < {NQ}; ++u) {{ const krn_i64 g_ = wlo + lane_ + 32 * u; "
+          f"if (lane_ + 32 * u < {WN} && g_ >= 0 && g_ < E.e0[{v}] && g_ < n_launch) {wn}r[u] = E.v[{v}][g_]; }}")
         w("        }")
         w("    }")
-    if any_window_load:
-        w("    __syncwarp();")
-    # ---- phases ---------------------------------------------------------------------------------
-    b.promoted, b.windows, b.stage_windows, b.in_tile = regs, wins, stage_win_sites, True
-    try:
-        for phase in wp.phases:
-            slots = 5 if any(wp.halo[k] != (0, 0) for k in phase) else 4
-            w("    if (live) {")
+
+    def emit_step(interior: bool):
+        # ---- windows in (values were fetched into registers by the prologue, all loads in flight at once)
+        loaded = False
+        for p in windows:
+            if not p["load"]:
+                continue
+            loaded = True
+            wn = wins[p["view"]]
             w("#pragma unroll")
-            w(f"    for (int e = 0; e < {slots}; ++e) {{")
-            w("        if (!act_[e]) continue;")
-            w("        const krn_i64 i = it_[e];")
-            w("        bool bad = false;")
-            for k in phase:
-                loop = group.ops[k]
-                hlo, hhi = wp.halo[k]
-                conds = []
-                if slots == 5:
-                    conds.append("(e < 4 || (i >= j0 - %d && i < j0 + 128 + %d))" % (hlo, hhi) if (hlo or hhi)
-                                 else "e < 4")
-                if loop.what == "apply":
-                    view, sites, producer = loop.apply_of
-                    v = b.vid(view)
-                    order = sorted(sites, key=lambda st: (-st.offset, st.index))
-                    conds += [f"i < n + {loop.shift}", f"i < E.e0[{v}]"]
-                    w(f"        if ({' && '.join(conds)}) {{  // deferred atomic adds landing on row i, reference order")
-                    if view in regs:
-                        tgt = f"{regs[view]}[e]"
-                    elif view in wins:
-                        tgt = f"{wins[view]}[(int)(i - wlo)]"
-                    else:
-                        tgt = f"E.v[{v}][i]"
-                    w(f"            double acc = {tgt};")
-                    for st in order:
-                        guard = " && ".join(["i >= 0", "i < n"] + [b.compare(g, {producer.counter}) for g in st.guards])
-                        nm = fusion.stage_name(st.index, producer)
-                        if nm in wp.stage_windows:
-                            src = f"TW{st.index}[(int)(i - wlo)]"
-                        elif nm in wp.stage_regs:
-                            src = f"T{st.index}[e]"
-                        else:
-                            src = f"stage[{st.index} * ld + i]"
-                        w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); "
-                          f"if ({guard}) acc = acc + {src}; }} }}")
-                    w(f"            {tgt} = acc;")
-                    w("        }")
-                    continue
-                sites = {id(st.stmt): st for st in loop.sites}
-                body: list = []
-                local = {loop.counter}
-                b.counter = loop.counter
-                try:
-                    b.elide = dict(counter=loop.counter, trip=an.trip(loop.upper), sym=an.trip, views=elided)
-                except (TypeError, ValueError):
-                    b.elide = None
-                try:
-                    for s in loop.body:
-                        b.element(s, local, body, "            ", sites, True)
-                finally:
-                    b.elide = None
-                    b.counter = None
-                if plan["max_shift"]:
-                    conds.append("i < n")
-                # `continue` inside the body must only leave this statement's block
-                w(f"        if ({' && '.join(conds) if conds else 'true'}) do {{")
-                L.extend(x.replace("continue;", "break;") for x in body)
-                w("        } while (0);")
-                w("        if (bad) continue;")
-            w("    }")
-            w("    }")
+            w(f"    for (int u = 0; u < {NQ}; ++u) if (lane_ + 32 * u < {WN}) {wn}[lane_ + 32 * u] = {wn}r[u];")
+        if loaded:
             w("    __syncwarp();")
-    finally:
-        b.promoted, b.windows, b.stage_windows, b.in_tile = {}, {}, {}, False
+        # ---- phases ----------------------------------------------------------------------------
+        b.promoted, b.windows, b.stage_windows, b.in_tile = regs, wins, stage_win_sites, True
+        try:
+            for phase in wp.phases:
+                slots = 5 if any(wp.halo[k] != (0, 0) for k in phase) else 4
+                w("#pragma unroll")
+                w(f"    for (int e = 0; e < {slots}; ++e) {{")
+                if interior:
+                    if slots == 5:
+                        w(f"        if (e == 4 && lane_ >= {HLO + HHI}) continue;")
+                else:
+                    w("        if (!act_[e]) continue;")
+                w("        const krn_i64 i = it_[e];")
+                w("        const int wq = wq_[e]; (void)wq;")
+                w("        bool bad = false;")
+                for k in phase:
+                    loop = group.ops[k]
+                    hlo, hhi = wp.halo[k]
+                    conds = []
+                    if slots == 5:
+                        conds.append(f"(e < 4 || h{k}_)" if (hlo or hhi) else "e < 4")
+                    if loop.what == "apply":
+                        view, sites, producer = loop.apply_of
+                        v = b.vid(view)
+                        order = sorted(sites, key=lambda st: (-st.offset, st.index))
+                        if not interior:
+                            conds.append(f"i < n + {loop.shift}")
+                        if not (interior and view in in_kernel_views):
+                            conds.append(f"i < E.e0[{v}]")
+                        w(f"        if ({' && '.join(conds) if conds else 'true'}) {{  // deferred atomic adds landing on row i, reference order")
+                        if view in regs:
+                            tgt = f"{regs[view]}[e]"
+                        elif view in wins:
+                            tgt = f"{wins[view]}[wq]"
+                        else:
+                            tgt = f"E.v[{v}][i]"
+                        w(f"            double acc = {tgt};")
+                        try:
+                            ptrip = an.trip(producer.upper)
+                        except (TypeError, ValueError):
+                            ptrip = None
+                        if interior and ptrip is not None:
+                            b.interior = dict(counter=producer.counter, trip=ptrip, sym=an.trip, lo=LO, up=UP)
+                        try:
+                            for st in order:
+                                parts = ([] if interior else ["i >= 0", "i < n"]) + \
+                                        [b.compare(g, {producer.counter}) for g in st.guards]
+                                guard = " && ".join(x for x in parts if x != "(true)") or "true"
+                                nm = fusion.stage_name(st.index, producer)
+                                if nm in wp.stage_windows:
+                                    src = f"TW{st.index}[wq - ({st.offset})]"
+                                elif nm in wp.stage_regs:
+                                    src = f"T{st.index}[e]"
+                                else:
+                                    src = f"stage[{st.index} * ld + i]"
+                                w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); (void)i; "
+                                  f"if ({guard}) acc = acc + {src}; }} }}")
+                        finally:
+                            b.interior = None
+                        w(f"            {tgt} = acc;")
+                        w("        }")
+                        continue
+                    sites = {id(st.stmt): st for st in loop.sites}
+                    body: list = []
+                    local = {loop.counter}
+                    b.counter = loop.counter
+                    try:
+                        trip = an.trip(loop.upper)
+                        b.elide = dict(counter=loop.counter, trip=trip, sym=an.trip, views=elided)
+                        if interior:
+                            b.interior = dict(counter=loop.counter, trip=trip, sym=an.trip, lo=LO, up=UP)
+                    except (TypeError, ValueError):
+                        b.elide = None
+                    try:
+                        for s_ in loop.body:
+                            b.element(s_, local, body, "            ", sites, True)
+                    finally:
+                        b.elide = None
+                        b.interior = None
+                        b.counter = None
+                    if plan["max_shift"] and not interior:
+                        conds.append("i < n")
+                    # `continue` inside the body must only leave this statement's block
+                    w(f"        if ({' && '.join(conds) if conds else 'true'}) do {{")
+                    L.extend(x.replace("continue;", "break;") for x in body)
+                    w("        } while (0);")
+                    w("        if (bad) continue;")
+                w("    }")
+                w("    __syncwarp();")
+        finally:
+            b.promoted, b.windows, b.stage_windows, b.in_tile = {}, {}, {}, False
+        # ---- windows out ---------------------------------------------------------------------------
+        for p in windows:
+            if not p["store"]:
+                continue
+            wn, v = wins[p["view"]], b.vid(p["view"])
+            dst = outp.get(p["view"], f"E.v[{v}]")
+            if interior:
+                w(f"    for (int e = 0; e < 4; ++e) {dst}[it_[e]] = {wn}[wq_[e]];")
+            else:
+                w(f"    for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {dst}[it_[e]] = {wn}[wq_[e]];")
+
+    w("    if (interior) {")
+    emit_step(True)
+    w("    } else if (live) {")
+    emit_step(False)
+    w("    }")
     # ---- epilogue ---------------------------------------------------------------------------------
     for p in promoted:
         if not p["store"]:
@@ -473,24 +565,13 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {dst}[it_[e]] = {r}[e]; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {dst}[it_[e]] = {r}[e]; }}")
         w("    }")
-    for p in windows:
-        if not p["store"]:
-            continue
-        wn, v = wins[p["view"]], b.vid(p["view"])
-        dst = outp.get(p["view"], f"E.v[{v}]")
-        w("    if (live) {")
-        w(f"        for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {dst}[it_[e]] = {wn}[(int)(it_[e] - wlo)];")
-        w("    }")
     for (_, idx) in plan["stage_cols"]:
         w(f"    if (live) {{ for (int e = 0; e < 4; ++e) if (act_[e]) stage[{idx} * ld + it_[e]] = T{idx}[e]; }}")
     if gather is not None:
         src = gather[0].src
         w("    {")
         w("        double R[4];")
-        if src in regs:
-            val = f"{regs[src]}[e]"
-        else:
-            val = f"{wins[src]}[(int)(it_[e] - wlo)]"
+        val = f"{regs[src]}[e]" if src in regs else f"{wins[src]}[wq_[e]]"
         w(f"        for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n);")
         w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
         w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
@@ -498,7 +579,6 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
         w("        tstack[tdepth++] = node;")
         w("    }")
-    w("#undef KRN_IT")
     w("    __syncwarp();")
     w("    }  // steps")
     if direct:
