@@ -308,6 +308,8 @@ class ModuleBuilder:
         being generated (pointwise access by construction)."""
         r = self.promoted.get(acc.view)
         if r is not None:
+            if len(acc.indices) == 2:  # rank-2 row at the running index: one register column per literal column
+                return f"{r}c{_constant(acc.indices[1])}[e]"
             return f"{r}[e]"
         w = self.windows.get(acc.view)
         if w is not None:

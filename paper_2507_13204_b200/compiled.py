@@ -75,7 +75,7 @@ class CompiledPlan:
     def __init__(self, fn, windows: bool = True):
         self.fn = fn
         an = self.an = fusion.Analysis(fn)
-        self.schedule = fusion.form_groups(fusion.build_ops(fn, an), an, windows)
+        self.schedule = fusion.form_groups(fusion.build_ops(fn, an, windows), an, windows)
         self.windowed = any(item[0] == "group" and item[1].windowed for item in self.schedule)
         b = self.builder = codegen.ModuleBuilder(fn, host_scalars=an.host_scalars)
         params = {p.name for p in fn.params if p.is_view}
@@ -237,6 +237,12 @@ class _CompiledRun:
                         for v in fusion_views(loop) & promoted:
                             if n > ext[v][0]:
                                 return False  # would be OutOfBounds: let the statement path report it
+                        for v, ncols in loop.need_cols.items():
+                            if ext[v][1] != ncols:
+                                return False  # a bulk statement unrolled over the columns the function names
+                    for p in recipe["promoted"]:
+                        if "cols" in p and p["cols"] and max(p["cols"]) >= ext[p["view"]][1]:
+                            return False  # a literal column outside the View: the statement path reports it
                     if g.gather is not None and ext[g.gather[0].src][0] != n:
                         return False
                     for v in recipe["elided_views"]:

@@ -73,6 +73,7 @@ class LoopOp:
     sites: list = _dc.field(default_factory=list)  # atomic sites of a kernel
     apply_of: object = None  # (view, sites) for an apply loop
     shift: int = 0  # apply loops run over upper + shift rows
+    need_cols: dict = _dc.field(default_factory=dict)  # rank-2 bulk statements: view -> exact extent 1 assumed
 
     def accesses(self) -> list:
         out: list = []
@@ -181,7 +182,7 @@ def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
 
     if loop.what == "apply":
         view, sites, producer = loop.apply_of
-        note(view, True, True, False, an.rank.get(view) == 1, 0, True)
+        note(view, True, True, False, True, 0, True)
         for st in sites:
             note(stage_name(st.index, producer), st.offset == 0, False, False, True, -st.offset, True)
         return out
@@ -199,6 +200,8 @@ def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
         pw = _is_pointwise(a, loop.counter)
         c = codegen._unit_affine(a.indices[0], loop.counter) if len(a.indices) == 1 else None
         affine = c is not None and an.rank.get(a.view, 1) == 1
+        if pw and len(a.indices) == 2:
+            affine, c = True, 0  # rank-2 row at the running index, literal column: register columns
         if affine and c != 0:
             if a.write or trip is None:
                 affine = False
@@ -220,10 +223,11 @@ class WindowPlan:
     halo_views: set       # Views touched by an op that runs on halo iterations
     phases: list          # op indices, split where a window written by one op is read at an offset by the next
     facts: dict           # group-level Facts
+    rank2: list = _dc.field(default_factory=list)  # rank-2 Views kept as register columns
 
     @property
     def needed(self) -> bool:
-        return bool(self.windowed or self.stage_windows or self.stage_regs)
+        return bool(self.windowed or self.stage_windows or self.stage_regs or self.rank2)
 
 
 def window_plan(ops: list, an: "Analysis"):
@@ -243,11 +247,15 @@ def window_plan(ops: list, an: "Analysis"):
         f = G[v]
         if not f.affine or f.at or an.rank.get(v) != 1:
             return None
+    # read-only Views read at neighbouring rows: one coalesced window load instead of one load per
+    # neighbour (optional: dropped first when the kernel runs out of windows)
+    readonly = [v for v, f in G.items() if not f.wr and not f.pw and f.affine and not f.at
+                and an.rank.get(v, 1) == 1 and not v.startswith("__stage")]
     stage_w, stage_r = [], []
     for v, f in G.items():
         if v.startswith("__stage") and f.wr and f.rd:   # producer and apply loop in the same group
             (stage_r if f.pw else stage_w).append(v)
-    promoted = {v for v, f in G.items() if f.pw and not f.at and an.rank.get(v, 1) == 1}
+    promoted = {v for v, f in G.items() if f.pw and not f.at}
     in_kernel = promoted | set(windowed) | set(stage_w) | set(stage_r)
     m = len(ops)
     H = [[0, 0] for _ in ops]
@@ -281,8 +289,17 @@ def window_plan(ops: list, an: "Analysis"):
             if v in windowed or v in stage_w:
                 for c in f.offsets:
                     HLO, HHI = max(HLO, hlo - c), max(HHI, hhi + c)
-    if HLO + HHI > MAX_HALO or len(windowed) + len(stage_w) > MAX_WINDOWS:
+    if len(windowed) + len(stage_w) > MAX_WINDOWS:
         return None
+    readonly = sorted(readonly)[:MAX_WINDOWS - len(windowed) - len(stage_w)]
+    for k, (hlo, hhi) in enumerate(H):
+        for v, f in per[k].items():
+            if v in readonly:
+                for c in f.offsets:
+                    HLO, HHI = max(HLO, hlo - c), max(HHI, hhi + c)
+    if HLO + HHI > MAX_HALO:
+        return None
+    windowed = windowed + readonly
     # phases: a __syncwarp() separates an op from an earlier one when a window carries a value
     # between different lanes (read-after-write or write-after-read at a non-zero offset)
     phases, cur, written, read_off = [], [], set(), set()
@@ -297,12 +314,18 @@ def window_plan(ops: list, an: "Analysis"):
         read_off |= reads_k
     if cur:
         phases.append(cur)
+    rank2 = sorted(v for v in promoted if an.rank.get(v, 1) == 2)
     return WindowPlan([tuple(h) for h in H], HLO, HHI, sorted(windowed), sorted(stage_w), sorted(stage_r),
-                      halo_views, phases, G)
+                      halo_views, phases, G, rank2)
 
 
 def _is_pointwise(acc: Access, counter: str) -> bool:
-    return len(acc.indices) == 1 and kind(acc.indices[0]) == "Counter" and acc.indices[0].name == counter
+    """the running row: v(i), or v(i, c) with a literal column c >= 0"""
+    if not acc.indices or kind(acc.indices[0]) != "Counter" or acc.indices[0].name != counter:
+        return False
+    if len(acc.indices) == 1:
+        return True
+    return len(acc.indices) == 2 and kind(acc.indices[1]) == "IntLiteral" and acc.indices[1].value >= 0
 
 
 @_dc.dataclass
@@ -326,13 +349,25 @@ class Analysis:
         for s in walk_statements(fn.body):
             if kind(s) == "DeclView":
                 self.rank[s.name] = s.descriptor.rank
-                if s.descriptor.rank == 1 and len(s.dyn_args) == 1:
+                # extent(local, 0) is the expression the View was declared with
+                first_dynamic = kind(s.descriptor.extents[0]) != "StaticExtent"
+                if first_dynamic and len(s.dyn_args) >= 1:
                     try:
                         self.extent_alias[s.name] = self.trip(s.dyn_args[0])
                     except (TypeError, ValueError):
                         pass
         self.host_scalars = self._host_scalars()
         self.live_scalars = self._live_scalars()
+        # literal columns with which each rank-2 View is accessed anywhere in the function
+        self.columns: dict = {}
+        for s in walk_statements(fn.body):
+            for e in N.statement_exprs(s):
+                for n in walk_expr(e):
+                    if kind(n) == "ViewAccess" and len(n.indices) == 2 and kind(n.indices[1]) == "IntLiteral":
+                        self.columns.setdefault(n.view, set()).add(n.indices[1].value)
+            if kind(s) in ("AssignView", "AtomicAdd") and len(s.target.indices) == 2 \
+                    and kind(s.target.indices[1]) == "IntLiteral":
+                self.columns.setdefault(s.target.view, set()).add(s.target.indices[1].value)
 
     # symbolic trip counts ------------------------------------------------------
     def trip(self, e):
@@ -401,24 +436,39 @@ class Analysis:
         return live
 
 
-def _bulk_as_loop(stmt, an: Analysis):
-    """deep_copy / accumulate parallel_sum over rank-1 views as an equivalent loop."""
+def _bulk_as_loop(stmt, an: Analysis, rank2: bool = False):
+    """deep_copy / accumulate parallel_sum as an equivalent loop over the rows.  Rank-2 Views
+    (`rank2`): one statement per column, for the columns 0..C-1 the function names literally;
+    the host checks extent(dst, 1) == C before launching (LoopOp.need_cols)."""
     k = kind(stmt)
-    if an.rank.get(stmt.dst) != 1:
-        return None
-    tgt = N.ViewAccess(stmt.dst, (N.Counter(K),))
-    if isinstance(stmt.src, str):
-        if an.rank.get(stmt.src) != 1:
-            return None
-        rhs = N.ViewAccess(stmt.src, (N.Counter(K),))
-    else:
-        rhs = stmt.src
     op = "=" if k == "DeepCopy" else "+="
-    body = (N.AssignView(tgt, op, rhs),)
-    return LoopOp(K, N.Extent(stmt.dst, 0), body, stmt, "deepcopy" if k == "DeepCopy" else "suminto")
+    what = "deepcopy" if k == "DeepCopy" else "suminto"
+    rank = an.rank.get(stmt.dst)
+    if isinstance(stmt.src, str) and an.rank.get(stmt.src) != rank:
+        return None
+    if rank == 1:
+        tgt = N.ViewAccess(stmt.dst, (N.Counter(K),))
+        rhs = N.ViewAccess(stmt.src, (N.Counter(K),)) if isinstance(stmt.src, str) else stmt.src
+        return LoopOp(K, N.Extent(stmt.dst, 0), (N.AssignView(tgt, op, rhs),), stmt, what)
+    if rank != 2 or not rank2:
+        return None
+    cols = set(an.columns.get(stmt.dst, ()))
+    if isinstance(stmt.src, str):
+        cols |= set(an.columns.get(stmt.src, ()))
+    if not cols or cols != set(range(len(cols))) or len(cols) > 8:
+        return None
+    body = []
+    for c in sorted(cols):
+        tgt = N.ViewAccess(stmt.dst, (N.Counter(K), N.IntLiteral(c)))
+        rhs = N.ViewAccess(stmt.src, (N.Counter(K), N.IntLiteral(c))) if isinstance(stmt.src, str) else stmt.src
+        body.append(N.AssignView(tgt, op, rhs))
+    need = {stmt.dst: len(cols)}
+    if isinstance(stmt.src, str):
+        need[stmt.src] = len(cols)
+    return LoopOp(K, N.Extent(stmt.dst, 0), tuple(body), stmt, what, need_cols=need)
 
 
-def build_ops(fn, an: Analysis) -> list:
+def build_ops(fn, an: Analysis, windows: bool = True) -> list:
     """Statement list -> op list.  Ops are ('loop', LoopOp) | ('gather', stmt, acc) |
     ('scalars', [stmts]) | ('hostscalar', stmt) | ('declview', stmt) | ('return', expr) |
     ('raw', stmt) for statements the fusion pass does not model."""
@@ -449,7 +499,11 @@ def build_ops(fn, an: Analysis) -> list:
         elif k == "ParallelFor":
             sites = codegen.plan_atomics(s)
             modes = {st.mode for st in sites}
-            rank2 = any(an.rank.get(a.view, 1) != 1 for a in LoopOp(s.counter, s.upper, s.body, s, "kernel").accesses())
+            # rank-2 Views: only rows at the running index with literal columns, and only in the
+            # window generator (register columns); anything else stays an unfused statement
+            probe = LoopOp(s.counter, s.upper, s.body, s, "kernel")
+            rank2 = any(an.rank.get(a.view, 1) != 1 and not (windows and _is_pointwise(a, s.counter))
+                        for a in probe.accesses())
             if rank2 or "staged_atomic" in modes:
                 ops.append(("raw", s))
                 continue
@@ -463,7 +517,7 @@ def build_ops(fn, an: Analysis) -> list:
                 shift = max(0, max(st.offset for st in group))
                 ops.append(("loop", LoopOp(K, s.upper, (), s, "apply", apply_of=(view, group, loop), shift=shift)))
         elif k in ("DeepCopy", "ParallelSumInto"):
-            loop = _bulk_as_loop(s, an)
+            loop = _bulk_as_loop(s, an, windows)
             ops.append(("loop", loop) if loop is not None else ("raw", s))
         elif k == "ParallelSum":
             if s.dst not in an.live_scalars:
@@ -503,7 +557,14 @@ def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
     def close():
         nonlocal cur
         if cur is not None:
-            schedule.append(("group", cur[0]))
+            g = cur[0]
+            if windows and not g.windowed:
+                # the window generator is also the one that keeps rank-2 rows in register columns and
+                # serves neighbour reads of read-only Views from a window instead of repeated loads
+                wp = window_plan(g.ops, an)
+                if wp is not None and wp.needed:
+                    g.windowed = True
+            schedule.append(("group", g))
             cur = None
 
     def summary(loop: LoopOp):
@@ -562,7 +623,8 @@ def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
             trip = an.trip(loop.upper)
         except (TypeError, ValueError):
             close()
-            schedule.append(("group", Group([loop])))
+            cur = (Group([loop]), None, {})
+            close()
             continue
         acc = summary(loop)
         if cur is not None:

@@ -28,10 +28,15 @@ from .lang.nodes import kind, walk_statements
 STRIDE_PAD = 8  # staging columns are padded so that column starts stay 32-byte aligned
 
 
-def _first_access_is_full_store(group, view, ops_with_full_range) -> bool:
+def _first_access_is_full_store(group, view, ops_with_full_range, col=None) -> bool:
     """True when, in program order, the first statement of the group touching `view`
-    is an unguarded top-level `view(i) = rhs` whose rhs does not read `view`, in a
-    statement that runs over the whole range of the group."""
+    (column `col` of it, for a rank-2 View) is an unguarded top-level `view(i) = rhs` whose
+    rhs does not read it, in a statement that runs over the whole range of the group."""
+    def hit(n):
+        if kind(n) != "ViewAccess" or n.view != view:
+            return False
+        return col is None or (len(n.indices) == 2 and kind(n.indices[1]) == "IntLiteral" and n.indices[1].value == col)
+
     for loop in group.ops:
         if loop.what == "apply":
             if loop.apply_of[0] == view:
@@ -42,15 +47,31 @@ def _first_access_is_full_store(group, view, ops_with_full_range) -> bool:
             for inner in walk_statements([s]):
                 for e in N.statement_exprs(inner):
                     for n in N.walk_expr(e):
-                        if kind(n) == "ViewAccess" and n.view == view:
+                        if hit(n):
                             touches = True
             if not touches:
                 continue
-            if (kind(s) == "AssignView" and s.op == "=" and s.target.view == view and id(loop) in ops_with_full_range
-                    and not any(kind(n) == "ViewAccess" and n.view == view for n in N.walk_expr(s.rhs))):
+            if (kind(s) == "AssignView" and s.op == "=" and hit(s.target) and id(loop) in ops_with_full_range
+                    and not any(hit(n) for n in N.walk_expr(s.rhs))):
                 return True
             return False
     return False
+
+
+def _columns(group, view) -> dict:
+    """rank-2 View -> {column: written?} over the statements of the group"""
+    cols: dict = {}
+    for loop in group.ops:
+        if loop.what == "apply":
+            if loop.apply_of[0] == view:
+                for st in loop.apply_of[1]:
+                    cols[st.column] = True
+            continue
+        for a in loop.accesses():
+            if a.view == view and len(a.indices) == 2 and kind(a.indices[1]) == "IntLiteral":
+                c = a.indices[1].value
+                cols[c] = cols.get(c, False) or (a.write and not a.atomic)
+    return cols
 
 
 def plan_group(builder, group, an, live_after: set) -> dict:
@@ -288,13 +309,25 @@ def plan_window_group(builder, group, an, live_after: set) -> dict:
         if v.startswith("__stage"):
             continue
         is_window = v in wp.windowed
-        if not is_window and not (f.pw and builder.rank.get(v) == 1 and not f.at):
+        if not is_window and not (f.pw and not f.at):
             continue
         load = not _first_access_is_full_store(group, v, full_range) and v not in group.fresh
         store = f.wr and (v in live_after)
         halo = v in wp.halo_views
         rec = dict(view=v, load=load, store=store, written=f.wr, halo=halo,
                    alt=bool(load and store and (halo or is_window)))
+        # an untouched local kept in a window: the window itself must read as +0.0
+        rec["zero_init"] = is_window and v in group.fresh and not _first_access_is_full_store(group, v, full_range)
+        if builder.rank.get(v) == 2:
+            # register columns: each literal column is loaded unless its first access overwrites it,
+            # and stored when the group wrote it
+            cols = _columns(group, v)
+            fresh = v in group.fresh
+            rec["cols"] = sorted(cols)
+            rec["col_load"] = {c: not fresh and not _first_access_is_full_store(group, v, full_range, c) for c in cols}
+            rec["col_store"] = {c: bool(cols[c]) and store for c in cols}
+            rec["load"] = any(rec["col_load"].values())
+            rec["alt"] = False
         (windows if is_window else promoted).append(rec)
     if sum(1 for r in promoted + windows if r["alt"]) > fusion.MAX_ALT:
         raise ValueError("too many out-of-place outputs")
@@ -405,6 +438,23 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     # ---- prologue: registers ------------------------------------------------------------
     for p in promoted:
         r, v = regs[p["view"]], b.vid(p["view"])
+        if "cols" in p:
+            # rank-2 View, rows at the running index: one register column per literal column; the
+            # lanes of a warp read rows 24 B (n1 = 3) apart, the columns of a row share its sectors (L1)
+            for c in p["cols"]:
+                w(f"    double {r}c{c}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
+            lc = [c for c in p["cols"] if p["col_load"][c]]
+            if lc:
+                w(f"    if (live && !(zero_mask & {1 << bit[p['view']]}u)) {{")
+                w(f"        const krn_i64 ld_ = E.e1[{v}];")
+                w("        for (int e = 0; e < 4; ++e) {")
+                w(f"            if (full || (act_[e] && it_[e] < E.e0[{v}])) {{")
+                for c in lc:
+                    w(f"                {r}c{c}[e] = E.v[{v}][it_[e] * ld_ + {c}];")
+                w("            }")
+                w("        }")
+                w("    }")
+            continue
         w(f"    double {r}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
         if p["load"]:
             w(f"    if (live && !(zero_mask & {1 << bit[p['view']]}u)) {{")
@@ -440,6 +490,9 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         # ---- windows in (values were fetched into registers by the prologue, all loads in flight at once)
         loaded = False
         for p in windows:
+            if p["zero_init"]:
+                loaded = True
+                w(f"    for (int q = lane_; q < {WN}; q += 32) {wins[p['view']]}[q] = 0.0;")
             if not p["load"]:
                 continue
             loaded = True
@@ -478,21 +531,35 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                         if not (interior and view in in_kernel_views):
                             conds.append(f"i < E.e0[{v}]")
                         w(f"        if ({' && '.join(conds) if conds else 'true'}) {{  // deferred atomic adds landing on row i, reference order")
-                        if view in regs:
-                            tgt = f"{regs[view]}[e]"
-                        elif view in wins:
-                            tgt = f"{wins[view]}[wq]"
-                        else:
-                            tgt = f"E.v[{v}][i]"
-                        w(f"            double acc = {tgt};")
                         try:
                             ptrip = an.trip(producer.upper)
                         except (TypeError, ValueError):
                             ptrip = None
-                        if interior and ptrip is not None:
-                            b.interior = dict(counter=producer.counter, trip=ptrip, sym=an.trip, lo=LO, up=UP)
-                        try:
+                        rank2 = b.rank.get(view) == 2
+                        columns = sorted({st.column for st in sites}) if rank2 else [None]
+                        for col in columns:
+                          if rank2 and view in regs:
+                              tgt = f"{regs[view]}c{col}[e]"
+                              w("            {")
+                          elif rank2:
+                              tgt = f"E.v[{v}][i * E.e1[{v}] + {col}]"
+                              w(f"            if ({col} < E.e1[{v}]) {{")
+                          elif view in regs:
+                              tgt = f"{regs[view]}[e]"
+                              w("            {")
+                          elif view in wins:
+                              tgt = f"{wins[view]}[wq]"
+                              w("            {")
+                          else:
+                              tgt = f"E.v[{v}][i]"
+                              w("            {")
+                          w(f"            double acc = {tgt};")
+                          if interior and ptrip is not None:
+                              b.interior = dict(counter=producer.counter, trip=ptrip, sym=an.trip, lo=LO, up=UP)
+                          try:
                             for st in order:
+                                if rank2 and st.column != col:
+                                    continue
                                 parts = ([] if interior else ["i >= 0", "i < n"]) + \
                                         [b.compare(g, {producer.counter}) for g in st.guards]
                                 guard = " && ".join(x for x in parts if x != "(true)") or "true"
@@ -505,9 +572,10 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                                     src = f"stage[{st.index} * ld + i]"
                                 w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); (void)i; "
                                   f"if ({guard}) acc = acc + {src}; }} }}")
-                        finally:
+                          finally:
                             b.interior = None
-                        w(f"            {tgt} = acc;")
+                          w(f"            {tgt} = acc;")
+                          w("            }")
                         w("        }")
                         continue
                     sites = {id(st.stmt): st for st in loop.sites}
@@ -560,6 +628,19 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         if not p["store"]:
             continue
         r, v = regs[p["view"]], b.vid(p["view"])
+        if "cols" in p:
+            sc = [c for c in p["cols"] if p["col_store"][c]]
+            if sc:
+                w("    if (live) {")
+                w(f"        const krn_i64 ld_ = E.e1[{v}];")
+                w("        for (int e = 0; e < 4; ++e) {")
+                w(f"            if (full || (act_[e] && it_[e] < E.e0[{v}])) {{")
+                for c in sc:
+                    w(f"                E.v[{v}][it_[e] * ld_ + {c}] = {r}c{c}[e];")
+                w("            }")
+                w("        }")
+                w("    }")
+            continue
         dst = outp.get(p["view"], f"E.v[{v}]")
         w("    if (live) {")
         w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {dst}[it_[e]] = {r}[e]; }}")

@@ -16,7 +16,7 @@ def _grad(stem):
 def _shape(fn, windows=False):
     an = fusion.Analysis(fn)
     out = []
-    for item in fusion.form_groups(fusion.build_ops(fn, an), an, windows):
+    for item in fusion.form_groups(fusion.build_ops(fn, an, windows), an, windows):
         if item[0] == "group":
             g = item[1]
             out.append("G[" + ",".join(o.what for o in g.ops) + ("+gather" if g.gather else "") + "]")
@@ -48,7 +48,7 @@ def test_headline_schedule_with_halo_recompute():
     assert [s for s in shape if s.startswith("G[")] == ["G[kernel,kernel+gather]"]
     an, shape = _shape(g, True)
     assert [s for s in shape if s.startswith("G[")] == ["G[kernel,kernel,suminto,kernel,apply,kernel]"]
-    group = [i[1] for i in fusion.form_groups(fusion.build_ops(g, an), an, True) if i[0] == "group"][0]
+    group = [i[1] for i in fusion.form_groups(fusion.build_ops(g, an, True), an, True) if i[0] == "group"][0]
     wp = fusion.window_plan(group.ops, an)
     assert wp.halo == [(2, 2), (1, 1), (1, 1), (1, 1), (0, 0), (0, 0)] and (wp.hlo, wp.hhi) == (2, 2)
     assert wp.windowed == ["x"]
@@ -109,10 +109,35 @@ def test_every_corpus_function_compiles_to_a_plan():
             assert launches <= statements
 
 
-def test_rank2_and_unsupported_shapes_stay_unfused():
+def test_rank2_rows_become_register_columns():
     fn, g = _grad("rowscale_rank2")
-    _, shape = _shape(g)
+    _, shape = _shape(g)  # pointwise-only fusion leaves rank-2 statements alone
     assert "raw" in shape and not any(s.startswith("G[") for s in shape)
+    # the window generator keeps m(i, c), q(i, c), _d_q(i, c), _d_m(i, c) in register columns: the
+    # forward kernel, the seed broadcast (unrolled over the 3 columns), the reversal and the apply
+    # loops of its (conservatively flagged, in fact injective) atomics are one launch
+    an, shape = _shape(g, True)
+    assert [s for s in shape if s.startswith("G[")] == ["G[kernel,suminto,kernel,apply,apply]"]
+    plan = compiled.plan_for(g, True)
+    recipe = [s[2] for s in plan.steps if s[0] == "group"][0]
+    views = {p["view"]: p for p in recipe["promoted"]}
+    assert views["m"]["cols"] == [0, 1, 2] and not views["m"]["store"]
+    assert not any(views["q"]["col_load"].values()) and not views["q"]["store"]       # dead intermediate
+    assert not any(views["_d_q"]["col_load"].values())                                   # fresh local: +0.0
+    assert all(views["_d_m"]["col_store"].values()) and views["_d_r"]["store"]
+    assert not recipe["stage_cols"] and plan.launch_count == 1
+    # primal: q must exist for the flat reduction (its tree interleaves the columns)
+    _, shape = _shape(fn, True)
+    assert shape == ["declview", "G[kernel]", "gather", "return"]
+
+
+def test_read_only_neighbour_reads_use_a_window():
+    fn, _ = _grad("stencil_smooth")
+    an = fusion.Analysis(fn)
+    group = [i[1] for i in fusion.form_groups(fusion.build_ops(fn, an, True), an, True) if i[0] == "group"][0]
+    wp = fusion.window_plan(group.ops, an)
+    assert group.windowed and wp.windowed == ["u"] and (wp.hlo, wp.hhi) == (1, 1)
+    assert wp.halo == [(0, 0), (0, 0)]  # nothing is recomputed: the window only replaces repeated loads
 
 
 def test_host_scalars_and_gather_accumulate():

@@ -181,3 +181,104 @@ def test_repeated_calls_accumulate_like_the_reference():
         krn.execute(gp, "normRes1DLaplacianSQ_grad", got, WIN)
     for k in want:
         assert_bits(got[k].buffer, want[k], k)
+
+
+# ---- rank-2 Views: rows at the running index, literal columns -> register columns --------------------
+
+RANK2 = """fn f(m: view<f64, 2>, r: view<f64, 1>, out: view<f64, 2>) -> f64 {
+    let q: view<f64, 2> = view("q", extent(m, 0), extent(m, 1));
+    deep_copy(q, 0.5);
+    parallel_for i in 0..extent(m, 0) {
+        q(i, 0) += r(i) * m(i, 0);
+        q(i, 2) = q(i, 0) - m(i, 1);
+        if (i != 0) { q(i, 1) = m(i, 2) * r(i - 1); }
+    }
+    parallel_sum(out, q);
+    parallel_for i in 0..extent(m, 0) { out(i, 1) -= r(i); m(i, 0) = q(i, 2); }
+    return parallel_sum(out);
+}"""
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 127, 128, 129, 1025, 4100])
+def test_rank2_register_columns_against_oracle(n):
+    from oracle import interp
+
+    prog = parse(RANK2)
+    plan = compiled.plan_for(prog.functions[0], True)
+    # every rank-2 statement (bulk ones included) runs in a generated window kernel, none through the library
+    assert plan.windowed and not any(s[0] in ("kernel", "deepcopy", "suminto") for s in plan.steps)
+    rng = np.random.default_rng(n)
+    data = {"m": rng.normal(size=(n, 3)), "r": rng.normal(size=n), "out": rng.normal(size=(n, 3))}
+    want = {k: v.copy() for k, v in data.items()}
+    wv = interp.run(prog, "f", want)
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"n={n} value")
+    for k in data:
+        assert_bits(got[k].buffer, want[k], f"n={n} {k}")
+
+
+def test_rank2_with_more_columns_than_the_program_names():
+    """deep_copy / parallel_sum over a rank-2 View are unrolled over the columns the function names;
+    a View with MORE columns must take the general route and still be right"""
+    from oracle import interp
+
+    prog = parse(RANK2)
+    n = 300
+    rng = np.random.default_rng(1)
+    data = {"m": rng.normal(size=(n, 5)), "r": rng.normal(size=n), "out": rng.normal(size=(n, 5))}
+    want = {k: v.copy() for k, v in data.items()}
+    wv = interp.run(prog, "f", want)
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    assert_bits(krn.execute(prog, "f", got, WIN).value, wv, "value")
+    for k in data:
+        assert_bits(got[k].buffer, want[k], k)
+
+
+def test_rank2_column_out_of_bounds_is_reported_like_the_reference():
+    prog = parse(RANK2)
+    n = 10
+    rng = np.random.default_rng(2)
+    data = {"m": rng.normal(size=(n, 2)), "r": rng.normal(size=n), "out": rng.normal(size=(n, 2))}
+    with pytest.raises(krn.OutOfBounds, match=r"outside extents 10x2"):
+        krn.execute(prog, "f", {k: ViewStorage.from_values(k, v) for k, v in data.items()}, WIN)
+
+
+@pytest.mark.parametrize("n", [3, 1000, 1 << 21])
+def test_rowscale_gradient_prefilled_shadows(n):
+    """the shipped 2-D case with accumulating shadows, against the statement path (itself checked
+    against the oracle in test_gpu_corpus)"""
+    prog = krn.load_program("rowscale_rank2")
+    gp = krn.differentiate(prog, "rowScaleEnergy", ("m", "r"))
+    rng = np.random.default_rng(n)
+    data = {"m": rng.normal(size=(n, 3)), "r": rng.normal(size=n), "_d_m": rng.normal(size=(n, 3)),
+            "_d_r": rng.normal(size=n)}
+    ref = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+    krn.execute(gp, "rowScaleEnergy_grad", ref, STMT)
+    krn.execute(gp, "rowScaleEnergy_grad", got, WIN)
+    for k in data:
+        assert_bits(got[k].buffer, ref[k].buffer, f"n={n} {k}")
+
+
+def test_untouched_local_read_at_neighbours_reads_as_zero():
+    """found by the random-program test: a fresh local (all +0.0) read at i - 1 / i + 1 lives in a
+    window that nothing loads - the window itself must be zero filled"""
+    from oracle import interp
+
+    src = """fn f(a: view<f64, 1>, b: view<f64, 1>) -> f64 {
+        let t0: view<f64, 1> = view("t0", extent(a, 0));
+        let t1: view<f64, 1> = view("t1", extent(a, 0));
+        parallel_for i in 0..extent(a, 0) { t0(i) = t1(i) + a(i); if (i != 0) { t0(i) += 0.5 * t1(i - 1); }
+                                            if (i != extent(a, 0) - 1) { t0(i) -= 0.5 * t1(i + 1); } }
+        parallel_for i in 0..extent(a, 0) { a(i) = 0.5 * a(i) + b(i); }
+        r = parallel_sum(t0);
+        return r; }"""
+    prog = parse(src)
+    for n in (2, 130, 1030):
+        rng = np.random.default_rng(n)
+        data = {"a": rng.normal(size=n), "b": rng.normal(size=n)}
+        want = {k: v.copy() for k, v in data.items()}
+        wv = interp.run(prog, "f", want)
+        got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
+        assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"n={n} value")
+        assert_bits(got["a"].buffer, want["a"], f"n={n} a")
