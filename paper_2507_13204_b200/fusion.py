@@ -152,6 +152,10 @@ def stage_name(index: int, producer) -> str:
 MAX_HALO = 32      # halo iterations of a warp step are handled by the 32 lanes in one extra slot
 MAX_WINDOWS = 5    # 8 warps x (128 + halo) doubles each: 5 windows stay under 48 KB of static shared memory
 MAX_ALT = 4        # out-of-place output pointers a window kernel accepts
+# Also serve neighbour reads of READ-ONLY Views from a window.  Measured on B200 (stencil_smooth,
+# 67 M rows): no gain for the primal, -10% for the gradient - the three L1-cached loads per row are
+# all in flight at once, the window adds a shared-memory round trip - so it stays off.
+READONLY_WINDOWS = False
 
 
 @_dc.dataclass
@@ -250,7 +254,7 @@ def window_plan(ops: list, an: "Analysis"):
     # read-only Views read at neighbouring rows: one coalesced window load instead of one load per
     # neighbour (optional: dropped first when the kernel runs out of windows)
     readonly = [v for v, f in G.items() if not f.wr and not f.pw and f.affine and not f.at
-                and an.rank.get(v, 1) == 1 and not v.startswith("__stage")]
+                and an.rank.get(v, 1) == 1 and not v.startswith("__stage")] if READONLY_WINDOWS else []
     stage_w, stage_r = [], []
     for v, f in G.items():
         if v.startswith("__stage") and f.wr and f.rd:   # producer and apply loop in the same group

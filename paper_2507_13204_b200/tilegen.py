@@ -156,74 +156,134 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     w("    double tstack[6];  // binary-counter tree over the warp's steps")
     w("    int tdepth = 0;")
     w("    (void)tstack; (void)tdepth;")
-    w("    for (int t = 0; t < steps; ++t) {")
+    # Memory-level parallelism: the loads of B consecutive steps are issued before the first of them
+    # is consumed (a kernel with one or two operand streams otherwise keeps a single 1 KB request per
+    # warp in flight; measured on B200: 4.5 -> 6 TB/s for a one-stream reduction).  B shrinks with
+    # the number of loaded Views so the register file still holds 3+ blocks per SM.
+    nload = sum(1 for p in promoted if p["load"])
+    B = 2 if 1 <= nload <= 2 else 1  # measured on B200: 2 gains 1-3%, deeper batches cost occupancy
     if strided:
-        w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first iteration of this step")
-        w("    const bool full = j0 + 128 <= n_safe;")
-        w("    const bool live = j0 < n_launch;")
         w("#define KRN_IT(e) (j0 + (e) * 32 + lane_)")
     else:
-        w("    const krn_i64 j0 = wbase + (krn_i64)t * 128 + 4 * lane_;")
-        w("    const bool full = j0 + 4 <= n_safe;")
-        w("    const bool live = j0 < n_launch;")
         w("#define KRN_IT(e) (j0 + (e))")
-    # ---- prologue ----------------------------------------------------------------
+
+    def geometry():
+        w("    const int t = t0 + b_;")
+        w("    if (t >= steps) break;")
+        if strided:
+            w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first iteration of this step")
+            w("    const bool full = j0 + 128 <= n_safe;")
+        else:
+            w("    const krn_i64 j0 = wbase + (krn_i64)t * 128 + 4 * lane_;")
+            w("    const bool full = j0 + 4 <= n_safe;")
+        w("    const bool live = j0 < n_launch;")
+
+    w(f"    for (int t0 = 0; t0 < steps; t0 += {B}) {{")
+    # ---- prologue: loads of the whole batch -------------------------------------------
     for k_, p in enumerate(promoted):
-        r, v = regs[p["view"]], b.vid(p["view"])
-        w(f"    double {r}[4] = {{0.0, 0.0, 0.0, 0.0}};")
         if p["load"]:
-            w(f"    if (live && !(zero_mask & {1 << k_}u)) {{")
-            if strided:
-                w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
-            else:
-                w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
-            w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
-            w("    }")
+            w(f"    double {regs[p['view']]}b_[{B}][4];")
+    w("#pragma unroll")
+    w(f"    for (int b_ = 0; b_ < {B}; ++b_) {{")
+    geometry()
+    for k_, p in enumerate(promoted):
+        if not p["load"]:
+            continue
+        r, v = regs[p["view"]] + "b_[b_]", b.vid(p["view"])
+        w(f"    for (int e = 0; e < 4; ++e) {r}[e] = 0.0;")
+        w(f"    if (live && !(zero_mask & {1 << k_}u)) {{")
+        if strided:
+            w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
+        else:
+            w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
+        w("    }")
+    w("    }")
+    # ---- the steps of the batch, one after the other ------------------------------------------
+    w("#pragma unroll")
+    w(f"    for (int b_ = 0; b_ < {B}; ++b_) {{")
+    geometry()
+    for p in promoted:
+        if p["load"]:
+            w(f"    double (&{regs[p['view']]})[4] = {regs[p['view']]}b_[b_];")
+        else:
+            w(f"    double {regs[p['view']]}[4] = {{0.0, 0.0, 0.0, 0.0}};")
     for (_, idx) in plan["stage_cols"]:
         w(f"    double T{idx}[4] = {{0.0, 0.0, 0.0, 0.0}};")
     # ---- body ------------------------------------------------------------------------
-    w("    if (live) {")
-    w("#pragma unroll")
-    w("    for (int e = 0; e < 4; ++e) {")
-    w("        const krn_i64 i = KRN_IT(e);")
-    w("        bool bad = false;")
-    w("        if (i >= n_launch) continue;")
-    b.promoted = regs
-    try:
-        for loop in group.ops:
-            if loop.what == "apply":
-                view, sites, producer = loop.apply_of
-                v, r = b.vid(view), regs.get(view)
-                order = sorted(sites, key=lambda st: (-st.offset, st.index))
-                w(f"        if (i < n + {loop.shift} && i < E.e0[{v}]) {{  // deferred atomic adds landing on row i, reference order")
-                tgt = f"{r}[e]" if r else f"E.v[{v}][i]"
-                w(f"            double acc = {tgt};")
-                for st in order:
-                    guard = " && ".join(["i >= 0", "i < n"] + [b.compare(g, {producer.counter}) for g in st.guards])
-                    w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); "
-                      f"if ({guard}) acc = acc + stage[{st.index} * ld + i]; }} }}")
-                w(f"            {tgt} = acc;")
-                w("        }")
-                continue
-            sites = {id(st.stmt): st for st in loop.sites}
-            body: list = []
-            local = {loop.counter}
-            if an is not None:
+    # interior step: every iteration of the warp (and every iteration an apply loop looks back or
+    # ahead to) lies far enough inside the range for the index guards to be decided at compile time
+    LO, UP = _guard_margins(group, an) if an is not None else (0, 0)
+    OFF = max([abs(st.offset) for l in group.ops if l.what == "apply" for st in l.apply_of[1]] + [0])
+    span = 128 if strided else 4
+    w(f"    const bool interior = full && j0 >= {LO + OFF} && j0 + {span + UP + OFF} <= n;")
+
+    def emit_body(interior: bool):
+        w("#pragma unroll")
+        w("    for (int e = 0; e < 4; ++e) {")
+        w("        const krn_i64 i = KRN_IT(e);")
+        w("        bool bad = false;")
+        if not interior:
+            w("        if (i >= n_launch) continue;")
+        b.promoted = regs
+        try:
+            for loop in group.ops:
+                if loop.what == "apply":
+                    view, sites, producer = loop.apply_of
+                    v, r = b.vid(view), regs.get(view)
+                    order = sorted(sites, key=lambda st: (-st.offset, st.index))
+                    conds = [f"i < E.e0[{v}]"] if not (interior and r) else []
+                    if not interior:
+                        conds.append(f"i < n + {loop.shift}")
+                    w(f"        if ({' && '.join(conds) if conds else 'true'}) {{  // deferred atomic adds landing on row i, reference order")
+                    tgt = f"{r}[e]" if r else f"E.v[{v}][i]"
+                    w(f"            double acc = {tgt};")
+                    if interior and an is not None:
+                        try:
+                            b.interior = dict(counter=producer.counter, trip=an.trip(producer.upper), sym=an.trip,
+                                              lo=LO, up=UP)
+                        except (TypeError, ValueError):
+                            b.interior = None
+                    try:
+                        for st in order:
+                            parts = ([] if interior else ["i >= 0", "i < n"]) + \
+                                    [b.compare(g, {producer.counter}) for g in st.guards]
+                            guard = " && ".join(x for x in parts if x != "(true)") or "true"
+                            w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); "
+                              f"if ({guard}) acc = acc + stage[{st.index} * ld + i]; }} }}")
+                    finally:
+                        b.interior = None
+                    w(f"            {tgt} = acc;")
+                    w("        }")
+                    continue
+                sites = {id(st.stmt): st for st in loop.sites}
+                body: list = []
+                local = {loop.counter}
+                if an is not None:
+                    try:
+                        trip = an.trip(loop.upper)
+                        b.elide = dict(counter=loop.counter, trip=trip, sym=an.trip, views=elided)
+                        if interior:
+                            b.interior = dict(counter=loop.counter, trip=trip, sym=an.trip, lo=LO, up=UP)
+                    except (TypeError, ValueError):
+                        b.elide = None
                 try:
-                    b.elide = dict(counter=loop.counter, trip=an.trip(loop.upper), sym=an.trip, views=elided)
-                except (TypeError, ValueError):
+                    for s in loop.body:
+                        b.element(s, local, body, "            ", sites, True)
+                finally:
                     b.elide = None
-            try:
-                for s in loop.body:
-                    b.element(s, local, body, "            ", sites, True)
-            finally:
-                b.elide = None
-            w("        if (i < n) {" if plan["max_shift"] else "        {")
-            L.extend(body)
-            w("        }")
-    finally:
-        b.promoted = {}
-    w("    }")
+                    b.interior = None
+                w("        if (i < n) {" if (plan["max_shift"] and not interior) else "        {")
+                L.extend(body)
+                w("        }")
+        finally:
+            b.promoted = {}
+        w("    }")
+
+    w("    if (interior) {")
+    emit_body(True)
+    w("    } else if (live) {")
+    emit_body(False)
     w("    }")
     # ---- epilogue -----------------------------------------------------------------------
     for p in promoted:
@@ -247,8 +307,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         r = regs[src]
         w("    {")
         w("        double R[4];")
-        w("        for (int e = 0; e < 4; ++e) R[e] = (KRN_IT(e) < n) ? "
-          f"{r}[e] : krn_tree_pad((krn_u64)KRN_IT(e), (krn_u64)n);")
+        w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = {r}[e]; }}")
+        w("        else { for (int e = 0; e < 4; ++e) R[e] = (KRN_IT(e) < n) ? "
+          f"{r}[e] : krn_tree_pad((krn_u64)KRN_IT(e), (krn_u64)n); }}")
         if strided:
             # element e of the 32 lanes = 32 consecutive leaves: four 32-leaf subtrees, then two levels
             w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
@@ -259,8 +320,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
         w("        tstack[tdepth++] = node;")
         w("    }")
-    w("#undef KRN_IT")
+    w("    }  // step of the batch")
     w("    }  // steps")
+    w("#undef KRN_IT")
     if direct:
         w("    krn_priv_end(E);")
     if gather is not None:
@@ -653,7 +715,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("    {")
         w("        double R[4];")
         val = f"{regs[src]}[e]" if src in regs else f"{wins[src]}[wq_[e]]"
-        w(f"        for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n);")
+        w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = {val}; }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n); }}")
         w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
         w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
         w("        int m_ = t;")
