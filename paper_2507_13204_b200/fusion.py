@@ -481,9 +481,15 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
     run: list = []
 
     def flush():
-        if run:
-            ops.append(("scalars", list(run)))
-            run.clear()
+        # `let s: f64 = 0.0;` of a device-resident scalar needs no kernel: the slot array is zero
+        # filled at the start of every run (compiled._CompiledRun.go)
+        import math
+
+        live = [x for x in run if not (kind(x) == "DeclScalar" and kind(x.init) == "Literal"
+                                       and x.init.value == 0.0 and math.copysign(1.0, x.init.value) > 0)]
+        if live:
+            ops.append(("scalars", live))
+        run.clear()
 
     for s in fn.body:
         k = kind(s)
@@ -534,7 +540,95 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
         else:
             raise TypeError(f"cannot execute {k}")
     flush()
-    return ops
+    return _drop_dead_fills(ops, fn)
+
+
+def _op_views(op) -> set:
+    tag = op[0]
+    out: set = set()
+
+    def of_stmt(s):
+        k = kind(s)
+        if k in ("DeepCopy", "ParallelSumInto"):
+            out.add(s.dst)
+            if isinstance(s.src, str):
+                out.add(s.src)
+        elif k == "ParallelSum":
+            out.add(s.src)
+        for inner in walk_statements([s]):
+            for e in N.statement_exprs(inner):
+                for n in walk_expr(e):
+                    if kind(n) in ("ViewAccess", "Extent"):
+                        out.add(n.view)
+
+    if tag == "loop":
+        loop = op[1]
+        if loop.what == "apply":
+            out.add(loop.apply_of[0])
+        else:
+            for s in loop.body:
+                of_stmt(s)
+            of_stmt(loop.origin) if loop.what in ("deepcopy", "suminto") else None
+    elif tag in ("raw", "gather", "hostscalar", "declview"):
+        of_stmt(op[1])
+    elif tag == "scalars":
+        for s in op[1]:
+            of_stmt(s)
+    elif tag == "return":
+        for n in walk_expr(op[1]):
+            if kind(n) in ("ViewAccess", "Extent"):
+                out.add(n.view)
+    return out
+
+
+def _drop_dead_fills(ops: list, fn) -> list:
+    """`deep_copy(local, scalar)` whose destination nothing reads afterwards is dead: locals die
+    at the return (runtime.py: DeclView storage is dropped), and a fill cannot raise.  The
+    generated gradients end with such fills (the reversal of `deep_copy(t, 0.0)` zeroes the
+    shadow of a View that is never used again)."""
+    local = {s.name for s in walk_statements(fn.body) if kind(s) == "DeclView"}
+    needed: set = set()
+    needed_scalars: set = set()
+    kept: list = []
+
+    def scalar_reads(op) -> set:
+        out: set = set()
+        stmts = op[1] if op[0] == "scalars" else [op[1].origin] + list(op[1].body) if op[0] == "loop" else \
+            [op[1]] if op[0] in ("raw", "gather", "hostscalar", "declview") else []
+        exprs = [op[1]] if op[0] == "return" else []
+        for s in walk_statements([x for x in stmts if x is not None and kind(x) != "ParallelFor"] +
+                                 [x for x in stmts if x is not None and kind(x) == "ParallelFor"]):
+            exprs += list(N.statement_exprs(s))
+            if kind(s) == "AssignScalar" and s.op != "=":
+                out.add(s.name)
+        for e in exprs:
+            for n in walk_expr(e):
+                if kind(n) == "ScalarVar":
+                    out.add(n.name)
+        return out
+
+    for op in reversed(ops):
+        if op[0] == "scalars":
+            # function-scope scalar statements nothing reads afterwards (the tail of a generated
+            # gradient reverses scalars that are never used again): dead unless they touch a View
+            stmts = list(walk_statements(op[1]))
+            pure = all(kind(x) in ("DeclScalar", "AssignScalar", "If") for x in stmts) and not any(
+                kind(n) == "ViewAccess" for x in stmts for e in N.statement_exprs(x) for n in walk_expr(e))
+            written = {x.name for x in stmts if kind(x) in ("DeclScalar", "AssignScalar")}
+            if pure and not (written & needed_scalars):
+                continue
+        needed_scalars |= scalar_reads(op)
+        stmt = op[1].origin if op[0] == "loop" and op[1].what == "deepcopy" else op[1] if op[0] == "raw" else None
+        if stmt is not None and kind(stmt) == "DeepCopy" and not isinstance(stmt.src, str):
+            if stmt.dst in local and stmt.dst not in needed:
+                continue  # dead
+            needed.discard(stmt.dst)  # fully overwritten here: earlier contents are not needed
+            kept.append(op)
+            continue
+        needed |= _op_views(op)
+        kept.append(op)
+    kept.reverse()
+    return kept
 
 
 def _reads_scalar(group: "Group", name: str) -> bool:
@@ -633,6 +727,16 @@ def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
         acc = summary(loop)
         if cur is not None:
             g, gtrip, gacc = cur
+            if gtrip != trip and loop.what in ("deepcopy", "suminto") and isinstance(loop.origin.src, str):
+                # `dst op= src` over whole Views raises unless their extents are equal (runtime.py:632-635,
+                # 658-660; the host checks it before launching), so the loop may as well be counted
+                # over the source's extent when that is the open group's range
+                try:
+                    alt = an.trip(N.Extent(loop.origin.src, 0))
+                except (TypeError, ValueError):
+                    alt = None
+                if alt == gtrip:
+                    loop.upper, trip = N.Extent(loop.origin.src, 0), alt
             ok = gtrip == trip
             # one staging buffer per kernel: a group holds at most one producer of staged
             # contributions, and never a producer together with an apply loop

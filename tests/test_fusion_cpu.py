@@ -142,3 +142,35 @@ def test_read_only_neighbour_reads_can_use_a_window(monkeypatch):
     wp = fusion.window_plan(group.ops, an)
     assert group.windowed and wp.windowed == ["u"] and (wp.hlo, wp.hhi) == (1, 1)
     assert wp.halo == [(0, 0), (0, 0)]  # nothing is recomputed: the window only replaces repeated loads
+
+
+def test_dead_fills_and_scalars_disappear():
+    """the tail of a generated gradient zeroes shadows of locals nobody reads again and reverses
+    scalars that are never used: no kernels for those; `dst += src` over whole Views counts over
+    the source's extent when that is the open group's range (their extents must agree anyway)"""
+    _, g = _grad("copy_chain")
+    plan = compiled.plan_for(g)
+    groups = [s for s in plan.steps if s[0] == "group"]
+    assert plan.launch_count == 1 and len(groups) == 1
+    assert [o.what for o in groups[0][1].ops] == ["deepcopy", "deepcopy", "kernel", "suminto", "kernel", "suminto"]
+    stored = [p["view"] for p in groups[0][2]["promoted"] if p["store"]]
+    assert stored == ["_d_src"]  # 16 B/row: read src, write _d_src
+    fn, g = _grad("mean_shift")
+    assert compiled.plan_for(fn).launch_count == 2       # gather, then fill + kernel + gather
+    plan = compiled.plan_for(g)
+    assert plan.launch_count == 3 and not any(s[0] == "scalars" for s in plan.steps)
+
+
+def test_a_fill_that_is_read_later_is_kept():
+    p = krn.parse("""fn f(v: view<f64,1>) -> f64 {
+        let t: view<f64,1> = view("t", extent(v, 0));
+        deep_copy(t, 2.0);
+        parallel_for i in 0..extent(v, 0) { v(i) = v(i) * t(i); }
+        deep_copy(t, 3.0);
+        s = parallel_sum(t);
+        deep_copy(t, 4.0);
+        return s; }""")
+    an = fusion.Analysis(p.functions[0])
+    ops = fusion.build_ops(p.functions[0], an, True)
+    fills = [op[1].origin.src.value for op in ops if op[0] == "loop" and op[1].what == "deepcopy"]
+    assert fills == [2.0, 3.0]  # the last one is dead, the others are read
