@@ -126,6 +126,11 @@ class _Bound:
 
     # rows per chunk of the pipelined host path: 4 Mi rows = 32 MB per View and chunk,
     # ~0.6 ms of PCIe time, large against launch/event overheads, small against the whole
+    # Measured on this pool (tools/pcie_probe.py, 2 GB each way at once, PCIe 5 x16): 40.0 ms in one
+    # piece (50 GB/s per direction), 43.0 ms in 4 Mi-row pieces, 40.8 ms in 16 Mi-row pieces.  In the
+    # pipeline the download of a chunk waits for its upload, so a call costs about
+    # chunk/bandwidth + whole download + per-chunk overheads: larger or ramped chunks were slower
+    # (46.3 ms with 16 Mi-row chunks and 1-2-4-8 ramps vs 44.0 ms with uniform 4 Mi rows).
     STREAM_CHUNK = 1 << 22
     STREAM_MIN_ROWS = 1 << 23
 
