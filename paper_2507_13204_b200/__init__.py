@@ -66,6 +66,10 @@ PROGRAMS_DIR = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "prog
 
 
 def load_program(stem: str):
-    """Parse one of the shipped corpus programs (``programs/<stem>.krn``)."""
-    with open(_os.path.join(PROGRAMS_DIR, stem + ".krn"), encoding="utf-8") as f:
+    """Parse one of the shipped programs: the reference's corpus (``programs/<stem>.krn``) or
+    an additional one (``extra_programs/<stem>.krn``, see the README there)."""
+    path = _os.path.join(PROGRAMS_DIR, stem + ".krn")
+    if not _os.path.exists(path):
+        path = _os.path.join(_os.path.dirname(PROGRAMS_DIR), "extra_programs", stem + ".krn")
+    with open(path, encoding="utf-8") as f:
         return parse(f.read())

@@ -141,8 +141,6 @@ def plan_for(fn, windows: bool = True) -> CompiledPlan:
             plan = CompiledPlan(fn, True)
         except ValueError:
             plan = None  # shape outside the window kernel: plain tile kernels
-        if plan is not None and not plan.windowed:
-            _plans[(id(fn), False)] = (fn, plan)
     if plan is None:
         plan = CompiledPlan(fn, False)
     _plans[key] = (fn, plan)

@@ -511,9 +511,10 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
             modes = {st.mode for st in sites}
             # rank-2 Views: only rows at the running index with literal columns, and only in the
             # window generator (register columns); anything else stays an unfused statement
+            # (a rank-2 View indexed any other way - m(idx(i), c) - is accessed in global memory
+            # through the checked accessors, like an indirectly indexed rank-1 View)
             probe = LoopOp(s.counter, s.upper, s.body, s, "kernel")
-            rank2 = any(an.rank.get(a.view, 1) != 1 and not (windows and _is_pointwise(a, s.counter))
-                        for a in probe.accesses())
+            rank2 = not windows and any(an.rank.get(a.view, 1) != 1 for a in probe.accesses())
             if rank2 or "staged_atomic" in modes:
                 ops.append(("raw", s))
                 continue
