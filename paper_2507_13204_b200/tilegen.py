@@ -178,7 +178,15 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w("    const bool full = j0 + 4 <= n_safe;")
         w("    const bool live = j0 < n_launch;")
 
-    w(f"    for (int t0 = 0; t0 < steps; t0 += {B}) {{")
+    if gather is not None:
+        # steps is 1 or 8 (compiled.py): unrolled, so that the step index - and with it the shape of
+        # the binary-counter tree over the steps - is known at compile time (registers, no local memory)
+        w("#pragma unroll")
+        w(f"    for (int tt_ = 0; tt_ < {8 // B}; ++tt_) {{")
+        w(f"    const int t0 = tt_ * {B};")
+        w("    if (t0 >= steps) break;")
+    else:
+        w(f"    for (int t0 = 0; t0 < steps; t0 += {B}) {{")
     # ---- prologue: loads of the whole batch -------------------------------------------
     for k_, p in enumerate(promoted):
         if p["load"]:
@@ -195,7 +203,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         if strided:
             w(f"        if (full) {{ for (int e = 0; e < 4; ++e) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
         else:
-            w(f"        if (full) {{ krn_d4 q = krn_ld4_rmw(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
+            # read-only operands take the non-coherent path (LDG.E.256.CONSTANT), read-modify-write ones may not
+            ld = "krn_ld4_rmw" if p["written"] else "krn_ld4_stream"
+            w(f"        if (full) {{ krn_d4 q = {ld}(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
         w("    }")
     w("    }")

@@ -21,6 +21,9 @@ BYTES = {
     "laplacian": (24, 40), "sum_squares": (8, 16), "affine_weighted": (16, 16), "safe_divide": (8, 16),
     "inplace_axpy": (24, 40), "copy_chain": (8, 16), "fill_scale": (8, 8), "mean_shift": (16, 24),
     "gather_indirect": (16, 24), "stencil_smooth": (8, 16), "rowscale_rank2": (32, 64),
+    # extra_programs/: 2-D View through a non-injective index map (BASELINE.json configs[3]):
+    # idx, w, 3 gathered columns; gradient adds _d_w and read-modify-write of 3 scattered columns
+    "gather_rows_rank2": (40, 96),
 }
 
 
