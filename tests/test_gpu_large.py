@@ -74,3 +74,33 @@ def test_one_billion_rows():
         z = w if hi == N else w - 2
         assert_bits(dx[lo + a:lo + z].cpu().numpy(), dxo[a:z], f"_d_x window {lo}")
         assert_bits(db[lo + a:lo + z].cpu().numpy(), dbo[a:z], f"_d_b window {lo}")
+
+
+def test_generated_window_kernels_beyond_4gib_offsets():
+    """The headline through the fusion pass (ONE generated window kernel per side) at 2^29 + 5 rows:
+    byte offsets exceed 4 GiB, 65 k blocks of 8 steps.  Checked bit for bit against the hand-written
+    kernels (themselves pinned to the oracle above): objective, scaled x, both shadows."""
+    from paper_2507_13204_b200 import ExecutionConfig, ViewStorage
+
+    free, _ = torch.cuda.mem_get_info()
+    n = (1 << 29) + 5
+    if free < 14 * 8 * n:
+        pytest.skip("needs ~60 GB of free device memory")
+    lap = krn.load_program("laplacian")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    xh, bh = _formula_np(0, n, 2654435761, 1048573), _formula_np(0, n, 40503, 1048571)
+    results = {}
+    for policy in ("fused", "compiled"):
+        cfg = ExecutionConfig(policy=policy)
+        call = {"x": ViewStorage.from_values("x", xh), "b": ViewStorage.from_values("b", bh)}
+        f = krn.execute(lap, "normRes1DLaplacianSQ", call, cfg).value
+        g = {"x": ViewStorage.from_values("x", xh), "b": ViewStorage.from_values("b", bh),
+             "_d_x": ViewStorage.zeros("_d_x", (n,)), "_d_b": ViewStorage.zeros("_d_b", (n,))}
+        krn.execute(gp, "normRes1DLaplacianSQ_grad", g, cfg)
+        results[policy] = (f, call["x"].peek().copy(), g["_d_x"].peek().copy(), g["_d_b"].peek().copy(),
+                           g["x"].peek().copy())
+        del call, g
+    a, c = results["fused"], results["compiled"]
+    assert_bits(c[0], a[0], "objective")
+    for k, name in ((1, "x after primal"), (2, "_d_x"), (3, "_d_b"), (4, "x after gradient")):
+        assert np.array_equal(c[k].view(np.uint64), a[k].view(np.uint64)), name
