@@ -148,6 +148,14 @@ int krn_laplacian_grad(krn_ctx *ctx, const double *d_x_in, double *d_x_out, cons
  * at this problem size (a power of two) */
 size_t krn_laplacian_partial_span(size_t n_global);
 
+/* Copies the per-block tree partials of the LAST krn_laplacian_primal launch on this
+ * context - ceil(n_local / span) doubles in block order, each the exact node of the
+ * reference's tree (pairwise_sum, runtime.py:166-177) over its aligned span of rows - to
+ * d_out (device memory), on the context's stream.  Sharded mode: the partials of all shards,
+ * concatenated in rank order and folded with krn_reduce_pairwise, give the objective
+ * bit-identical to the single-device (and the reference's) result for any number of shards. */
+int krn_laplacian_partials(krn_ctx *ctx, double *d_out, size_t count);
+
 /* ---- generated kernels (parallel_for bodies compiled from the program tree;
  *      replaces _Compiler/_Interpreter.parallel_for, runtime.py:230-447, 567-624)
  * `cuda_source` is CUDA C++ for sm_100a; it may #include "krn_prelude.cuh"

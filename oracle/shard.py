@@ -69,3 +69,24 @@ def laplacian_shard(x, b, dx, db, halo, offset, n_global, seed=1.0):
             dx[i] = acc
             db[i] = db[i] + (-r1[k])
     return xs[2:-2], (y * y)[2:-2]
+
+
+def tree_pad(j: int, n: int) -> float:
+    """Leaf value of a missing leaf j >= n of the blocked tree (csrc/krn_prelude.cuh:krn_tree_pad):
+    +0.0 where the reference pads an odd level (runtime.py:166-177), the identity -0.0 elsewhere."""
+    low = j & (-j)
+    return 0.0 if (j - low < n and j != low) else -0.0
+
+
+def block_partials(y2, offset: int, n_global: int, span: int) -> np.ndarray:
+    """The per-block tree nodes one shard's primal kernel produces: block k covers global rows
+    [offset + k*span, offset + (k+1)*span) as a complete binary tree, leaves past n_global padded."""
+    n = len(y2)
+    out = []
+    for start in range(0, n, span):
+        leaves = np.array([y2[start + j] if start + j < n else tree_pad(offset + start + j, n_global)
+                           for j in range(span)], dtype=np.float64)
+        while len(leaves) > 1:
+            leaves = leaves[0::2] + leaves[1::2]
+        out.append(leaves[0])
+    return np.array(out, dtype=np.float64)

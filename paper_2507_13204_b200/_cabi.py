@@ -67,6 +67,7 @@ SIGNATURES = {
     "krn_laplacian_primal": (_i, [_vp, _dp, _dp, _dp, _sz, _sz, _sz, _dp, _dp, _i]),
     "krn_laplacian_grad": (_i, [_vp, _dp, _dp, _dp, _dp, _dp, _i, _i, _sz, _sz, _sz, _dp, _d]),
     "krn_laplacian_partial_span": (_sz, [_sz]),
+    "krn_laplacian_partials": (_i, [_vp, _dp, _sz]),
     "krn_module_compile": (_i, [_vp, C.c_char_p, _pp]),
     "krn_module_destroy": (_i, [_vp]),
     "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),

@@ -459,3 +459,13 @@ extern "C" int krn_laplacian_grad(krn_ctx *ctx, const double *d_x_in, double *d_
     return launch<true>(ctx, d_x_in, d_x_out, d_b, d_dx, d_db, dx_zero, db_zero, n_local, offset,
                         n_global, d_halo, seed, nullptr, 0);
 }
+
+extern "C" int krn_laplacian_partials(krn_ctx *ctx, double *d_out, size_t count)
+{
+    KRN_REQUIRE(ctx != nullptr, "null context");
+    KRN_REQUIRE(count <= ctx->partial_capacity, "more partials requested than the last launch produced");
+    if (count == 0) return KRN_OK;
+    KRN_REQUIRE(d_out != nullptr, "null output pointer");
+    KRN_CUDA(cudaMemcpyAsync(d_out, ctx->d_partials, count * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    return KRN_OK;
+}

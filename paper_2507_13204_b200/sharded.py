@@ -10,8 +10,14 @@ shard boundary and the summation order of every ``_d_x`` entry is the
 reference's.  Collectives, both latency bound:
 
 * one all_gather of 6 doubles per rank (the halo rows)
-* one all_reduce(SUM) of 1 double for the objective value (primal only; the
-  gradient does not depend on it)
+* for the objective value (primal only; the gradient does not depend on it) one
+  all_gather of the per-block tree partials (one double per 1024 or 8192 rows;
+  122 KB per rank at 125 M rows), folded by every rank with the reference's tree:
+  shard cuts are multiples of the partial span, so the partials of all ranks in
+  rank order ARE the nodes of the single-device tree and the result is
+  bit-identical to the single-device and to the reference's value for any number
+  of GPUs (``exact=False``: a plain all_reduce(SUM) of 1 double instead, exact
+  only up to reassociation)
 
 ``torch.distributed`` is the plumbing (NCCL on GPUs; gloo for the CPU tests of
 the partition/halo logic).  Device memory here is torch tensors whose
@@ -34,6 +40,22 @@ def partition(n_global: int, world: int, align: int = 1) -> list:
         cuts.append(max(c, cuts[-1]))
     cuts.append(n_global)
     return [(cuts[r], cuts[r + 1] - cuts[r]) for r in range(world)]
+
+
+def partial_count(n_local: int, span: int) -> int:
+    """Tree partials one shard produces (one per started span of rows)."""
+    return (n_local + span - 1) // span
+
+
+def combine_partials(gathered, counts):
+    """The all-gathered partial matrix (world x width, rows padded) as ONE vector in rank order:
+    because every cut is a multiple of the span these are exactly the per-block nodes a single
+    device would have produced, so the reference's tree over them is the reference's value."""
+    import torch
+
+    if all(c == gathered.shape[1] for c in counts):
+        return gathered.reshape(-1)  # equal shards: already one contiguous vector
+    return torch.cat([gathered[r, :c] for r, c in enumerate(counts)]).contiguous()
 
 
 def pack_boundary(x, b):
@@ -72,8 +94,10 @@ class ShardedLaplacian:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.dev = device
         self.n_global = n_global
-        span = int(device.lib.krn_laplacian_partial_span(n_global))
-        self.offset, self.n_local = partition(n_global, self.world, span)[self.rank]
+        self.span = int(device.lib.krn_laplacian_partial_span(n_global))
+        self.parts = partition(n_global, self.world, self.span)
+        self.offset, self.n_local = self.parts[self.rank]
+        self.block_counts = [partial_count(length, self.span) for _, length in self.parts]
 
     def exchange_halo(self, x, b):
         import torch
@@ -85,17 +109,32 @@ class ShardedLaplacian:
         self.dist.all_gather_into_tensor(gathered, mine, group=self.group)
         return assemble_halo(gathered.view(self.world, 6), self.rank, self.world)
 
-    def primal(self, x, x_out, b, f_out):
+    def primal(self, x, x_out, b, f_out, *, exact: bool = True):
         """f_out (1-element tensor) <- global objective; x_out <- 3x (local rows)."""
+        import torch
+
         from . import _cabi
 
+        lib = self.dev.lib
         halo = self.exchange_halo(x, b)
-        _cabi.check(self.dev.lib.krn_laplacian_primal(
+        _cabi.check(lib.krn_laplacian_primal(
             self.dev.h, C.c_void_p(x.data_ptr()), C.c_void_p(x_out.data_ptr()), C.c_void_p(b.data_ptr()),
             self.n_local, self.offset, self.n_global,
             C.c_void_p(halo.data_ptr()) if halo is not None else None, C.c_void_p(f_out.data_ptr()), 0))
-        if self.world > 1:
+        if self.world == 1:
+            return f_out
+        if not exact:
             self.dist.all_reduce(f_out, group=self.group)
+            return f_out
+        # every rank contributes max(block counts) doubles (the tail is padding that is cut off again)
+        width = max(self.block_counts)
+        mine = torch.zeros(width, dtype=x.dtype, device=x.device)
+        _cabi.check(lib.krn_laplacian_partials(self.dev.h, C.c_void_p(mine.data_ptr()), self.block_counts[self.rank]))
+        gathered = torch.empty(self.world * width, dtype=x.dtype, device=x.device)
+        self.dist.all_gather_into_tensor(gathered, mine, group=self.group)
+        nodes = combine_partials(gathered.view(self.world, width), self.block_counts)
+        _cabi.check(lib.krn_reduce_pairwise(self.dev.h, C.c_void_p(nodes.data_ptr()), nodes.numel(),
+                                            C.c_void_p(f_out.data_ptr()), 0))
         return f_out
 
     def grad(self, x, x_out, b, dx, db, *, seed=1.0, dx_zero=False, db_zero=False):

@@ -86,3 +86,39 @@ def test_single_rank_object(dev):
     assert_bits(dx.cpu().numpy(), dxo, "_d_x")
     assert_bits(db.cpu().numpy(), dbo, "_d_b")
     assert_bits(xo_t.cpu().numpy(), xo, "3x")
+
+
+@pytest.mark.parametrize("world,n", [(2, 5000), (3, 100_003), (8, (1 << 21) + 12345), (4, (1 << 20) + 1), (7, 3 * 8192 * 7)])
+def test_sharded_objective_is_bit_identical(dev, world, n):
+    """per-block tree partials of every shard, concatenated in rank order and folded with the
+    reference's tree (what ShardedLaplacian.primal does after its all_gather), equal the
+    single-device objective - and the oracle's - bit for bit, for any number of shards"""
+    from oracle import cport
+    from paper_2507_13204_b200.sharded import combine_partials, partial_count
+
+    rng = np.random.default_rng(world + n)
+    x, b = rng.normal(size=n), rng.normal(size=n)
+    fo = cport.laplacian_primal(x.copy(), b.copy())
+    span = int(dev.lib.krn_laplacian_partial_span(n))
+    parts = partition(n, world, span)
+    xt = [torch.from_numpy(x[o:o + l].copy()).cuda() for o, l in parts]
+    bt = [torch.from_numpy(b[o:o + l].copy()).cuda() for o, l in parts]
+    gathered = torch.stack([pack_boundary(xi, bi) for xi, bi in zip(xt, bt)])
+    counts = [partial_count(l, span) for _, l in parts]
+    width = max(counts)
+    rows = torch.zeros(world, width, dtype=torch.float64, device="cuda")
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    plain = 0.0
+    for r, (o, l) in enumerate(parts):
+        halo = assemble_halo(gathered, r, world)
+        xout, f = torch.empty_like(xt[r]), torch.zeros(1, dtype=torch.float64, device="cuda")
+        _cabi.check(dev.lib.krn_laplacian_primal(dev.h, P(xt[r]), P(xout), P(bt[r]), l, o, n, P(halo), P(f), 0))
+        _cabi.check(dev.lib.krn_laplacian_partials(dev.h, P(rows[r]), counts[r]))
+        torch.cuda.synchronize()
+        plain += float(f.item())
+    nodes = combine_partials(rows, counts)
+    f = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _cabi.check(dev.lib.krn_reduce_pairwise(dev.h, P(nodes), nodes.numel(), P(f), 0))
+    torch.cuda.synchronize()
+    assert_bits(float(f.item()), fo, f"exact objective, {world} shards")
+    assert abs(plain - fo) <= 1e-13 * abs(fo)  # what a plain all_reduce(SUM) would give

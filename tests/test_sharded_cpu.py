@@ -102,3 +102,64 @@ def test_halo_exchange_over_gloo(world):
     assert_bits(np.concatenate([p[2] for p in pieces]), dbo, "_d_b")
     fo = cport.laplacian_primal(x.copy(), b.copy())
     assert abs(f - fo) <= 1e-14 * abs(fo)  # allreduce order differs from the tree: reassociation only
+
+
+def _exact_worker(rank, world, port, n, span, out):
+    """the exact-objective protocol of ShardedLaplacian.primal over gloo: pad the block partials to
+    the widest rank, all_gather, cut the padding off, fold with the reference's tree"""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import interp, shard as shard_oracle
+        from paper_2507_13204_b200.sharded import combine_partials, partial_count
+
+        x, b, dx0, db0, *_ = _whole(n)
+        parts = partition(n, world, span)
+        o, l = parts[rank]
+        xt, bt = torch.from_numpy(x[o:o + l].copy()), torch.from_numpy(b[o:o + l].copy())
+        gathered = torch.empty(world * 6, dtype=torch.float64)
+        dist.all_gather_into_tensor(gathered, pack_boundary(xt, bt))
+        halo = assemble_halo(gathered.view(world, 6), rank, world).numpy()
+        _, y2 = shard_oracle.laplacian_shard(x[o:o + l], b[o:o + l], dx0[o:o + l].copy(), db0[o:o + l].copy(), halo, o, n)
+        counts = [partial_count(length, span) for _, length in parts]
+        width = max(counts)
+        mine = torch.zeros(width, dtype=torch.float64)
+        mine[:counts[rank]] = torch.from_numpy(shard_oracle.block_partials(y2, o, n, span))
+        allp = torch.empty(world * width, dtype=torch.float64)
+        dist.all_gather_into_tensor(allp, mine)
+        nodes = combine_partials(allp.view(world, width), counts).numpy()
+        out.put((rank, float(interp.pairwise_sum(nodes))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,span", [(2, 257, 16), (3, 1000, 64), (3, 96, 16)])
+def test_exact_objective_over_gloo(world, n, span):
+    """every rank ends up with the SAME bits, equal to the whole-problem oracle"""
+    from oracle import cport
+
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = 29000 + os.getpid() % 500 + 7 * world + span
+    procs = [ctx.Process(target=_exact_worker, args=(r, world, port, n, span, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=60) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    x, b, *_ = _whole(n)
+    fo = cport.laplacian_primal(x.copy(), b.copy())
+    for r in range(world):
+        assert_bits(got[r], fo, f"rank {r} of {world}")
+
+
+def test_block_partials_fold_to_the_reference_tree():
+    from oracle import interp, shard as shard_oracle
+
+    rng = np.random.default_rng(0)
+    for n, span, world in [(1, 4, 1), (100, 8, 3), (257, 16, 2), (1000, 64, 5), (64, 16, 4)]:
+        v = rng.normal(size=n)
+        parts = partition(n, world, span)
+        nodes = np.concatenate([shard_oracle.block_partials(v[o:o + l], o, n, span) for o, l in parts if l])
+        assert_bits(interp.pairwise_sum(nodes), interp.pairwise_sum(v), f"n={n} span={span} world={world}")
