@@ -558,6 +558,52 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("        }")
         w("    }")
 
+    def emit_apply(view, sites, producer, interior: bool):
+        """`acc = target(row); acc += contributions landing on the row, reference order; target = acc`,
+        once per literal column for a rank-2 target."""
+        v = b.vid(view)
+        order = sorted(sites, key=lambda st: (-st.offset, st.index))
+        try:
+            ptrip = an.trip(producer.upper)
+        except (TypeError, ValueError):
+            ptrip = None
+        rank2 = b.rank.get(view) == 2
+        for col in (sorted({st.column for st in sites}) if rank2 else [None]):
+            if rank2 and view in regs:
+                tgt, head = f"{regs[view]}c{col}[e]", "{"
+            elif rank2:
+                tgt, head = f"E.v[{v}][i * E.e1[{v}] + {col}]", f"if ({col} < E.e1[{v}]) {{"
+            elif view in regs:
+                tgt, head = f"{regs[view]}[e]", "{"
+            elif view in wins:
+                tgt, head = f"{wins[view]}[wq]", "{"
+            else:
+                tgt, head = f"E.v[{v}][i]", "{"
+            w(f"            {head}")
+            w(f"            double acc = {tgt};")
+            if interior and ptrip is not None:
+                b.interior = dict(counter=producer.counter, trip=ptrip, sym=an.trip, lo=LO, up=UP)
+            try:
+                for st in order:
+                    if rank2 and st.column != col:
+                        continue
+                    parts = ([] if interior else ["i >= 0", "i < n"]) + \
+                            [b.compare(g, {producer.counter}) for g in st.guards]
+                    guard = " && ".join(x for x in parts if x != "(true)") or "true"
+                    nm = fusion.stage_name(st.index, producer)
+                    if nm in wp.stage_windows:
+                        src = f"TW{st.index}[wq - ({st.offset})]"
+                    elif nm in wp.stage_regs:
+                        src = f"T{st.index}[e]"
+                    else:
+                        src = f"stage[{st.index} * ld + i]"
+                    w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); (void)i; "
+                      f"if ({guard}) acc = acc + {src}; }} }}")
+            finally:
+                b.interior = None
+            w(f"            {tgt} = acc;")
+            w("            }")
+
     def emit_step(interior: bool):
         # ---- windows in (values were fetched into registers by the prologue, all loads in flight at once)
         loaded = False
@@ -597,57 +643,12 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                     if loop.what == "apply":
                         view, sites, producer = loop.apply_of
                         v = b.vid(view)
-                        order = sorted(sites, key=lambda st: (-st.offset, st.index))
                         if not interior:
                             conds.append(f"i < n + {loop.shift}")
                         if not (interior and view in in_kernel_views):
                             conds.append(f"i < E.e0[{v}]")
                         w(f"        if ({' && '.join(conds) if conds else 'true'}) {{  // deferred atomic adds landing on row i, reference order")
-                        try:
-                            ptrip = an.trip(producer.upper)
-                        except (TypeError, ValueError):
-                            ptrip = None
-                        rank2 = b.rank.get(view) == 2
-                        columns = sorted({st.column for st in sites}) if rank2 else [None]
-                        for col in columns:
-                          if rank2 and view in regs:
-                              tgt = f"{regs[view]}c{col}[e]"
-                              w("            {")
-                          elif rank2:
-                              tgt = f"E.v[{v}][i * E.e1[{v}] + {col}]"
-                              w(f"            if ({col} < E.e1[{v}]) {{")
-                          elif view in regs:
-                              tgt = f"{regs[view]}[e]"
-                              w("            {")
-                          elif view in wins:
-                              tgt = f"{wins[view]}[wq]"
-                              w("            {")
-                          else:
-                              tgt = f"E.v[{v}][i]"
-                              w("            {")
-                          w(f"            double acc = {tgt};")
-                          if interior and ptrip is not None:
-                              b.interior = dict(counter=producer.counter, trip=ptrip, sym=an.trip, lo=LO, up=UP)
-                          try:
-                            for st in order:
-                                if rank2 and st.column != col:
-                                    continue
-                                parts = ([] if interior else ["i >= 0", "i < n"]) + \
-                                        [b.compare(g, {producer.counter}) for g in st.guards]
-                                guard = " && ".join(x for x in parts if x != "(true)") or "true"
-                                nm = fusion.stage_name(st.index, producer)
-                                if nm in wp.stage_windows:
-                                    src = f"TW{st.index}[wq - ({st.offset})]"
-                                elif nm in wp.stage_regs:
-                                    src = f"T{st.index}[e]"
-                                else:
-                                    src = f"stage[{st.index} * ld + i]"
-                                w(f"            {{ const krn_i64 k_ = i; {{ const krn_i64 i = k_ - ({st.offset}); (void)i; "
-                                  f"if ({guard}) acc = acc + {src}; }} }}")
-                          finally:
-                            b.interior = None
-                          w(f"            {tgt} = acc;")
-                          w("            }")
+                        emit_apply(view, sites, producer, interior)
                         w("        }")
                         continue
                     sites = {id(st.stmt): st for st in loop.sites}
