@@ -382,7 +382,8 @@ class _CompiledRun:
         from .runtime import atomic_choice
 
         env = self.env(ptrs, needed - set(ptrs),
-                       atomic_choice(self.cfg, recipe["atomic_views"], self.views, self.b, n_launch))
+                       atomic_choice(self.cfg, recipe["atomic_views"], self.views, self.b, n_launch,
+                                     recipe.get("static_smem", 0)))
         extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
         steps = 1 if n_launch <= (1 << 20) else 8  # must be a power of two (tree node per block)
         nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)

@@ -540,7 +540,7 @@ def _plan_for(fn) -> _Plan:
 SMEM_PRIVATE_MAX = 6144  # doubles: 48 KB of dynamic shared memory
 
 
-def atomic_choice(cfg, atomic_views, views, builder, n):
+def atomic_choice(cfg, atomic_views, views, builder, n, static_smem: int = 0):
     """(rows, policy, view id) for Env: how a kernel accumulates its direct atomic_add
     contributions.  Privatisation pays when the target is small and hit often: every block
     folds its contributions in shared memory and issues at most one RED per row."""
@@ -556,6 +556,10 @@ def atomic_choice(cfg, atomic_views, views, builder, n):
         want = "smem" if (0 < rows <= SMEM_PRIVATE_MAX and n >= 4 * rows) else "lead"
     if want == "smem" and not (0 < rows <= SMEM_PRIVATE_MAX):
         want = "red"
+    if want == "smem" and 8 * rows + static_smem > 48 * 1024:
+        # the kernel's own shared memory (windows, reduction scratch) and the privatised rows
+        # together exceed what a launch gets without opting in: aggregate in the warp instead
+        want = "lead"
     return (rows, {"red": 0, "warp": 1, "smem": 2, "lead": 3}[want], builder.vid(name))
 
 

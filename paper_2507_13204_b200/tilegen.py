@@ -350,7 +350,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     w("}")
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
-                gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct)
+                gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct,
+                static_smem=512 if gather is not None else 0)
 
 
 # ---------------------------------------------------------------------------------------
@@ -755,4 +756,5 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     return dict(name=name, promoted=every, stage_cols=plan["stage_cols"], has_stage=bool(plan["stage_cols"]),
                 gather=gather, max_shift=plan["max_shift"],
                 elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct,
-                window=True, alt=alts, hlo=HLO, hhi=HHI)
+                window=True, alt=alts, hlo=HLO, hhi=HHI,
+                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (512 if gather is not None else 0))

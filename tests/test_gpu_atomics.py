@@ -76,3 +76,33 @@ def test_rank2_target_privatised():
                "m": ViewStorage.from_values("m", np.ones((rows, 3)))}
         krn.execute(p, "f", got, ExecutionConfig(atomic_policy=apol))
         assert np.allclose(got["m"].buffer, want["m"], rtol=1e-12, atol=1e-12), apol
+
+
+def test_privatised_rows_next_to_the_kernels_own_shared_memory():
+    """a scatter into exactly the largest privatisable target (6144 rows = 48 KB) fused with a
+    reduction (static shared memory for the block tree) and with a neighbour window: the host must
+    not ask for more shared memory than a launch gets"""
+    from oracle import interp
+
+    src = """fn f(a: view<f64, 1>, idx: view<f64, 1>, acc: view<f64, 1>) -> f64 {
+        let t: view<f64, 1> = view("t", extent(a, 0));
+        parallel_for i in 0..extent(a, 0) { a(i) = 2.0 * a(i); }
+        parallel_for i in 0..extent(a, 0) {
+            t(i) = a(i);
+            if (i != 0) { t(i) += a(i - 1); }
+            atomic_add(acc(idx(i)), 1.0);
+        }
+        s = parallel_sum(t);
+        return s; }"""
+    p = parse(src)
+    n, rows = 40_000, 6144
+    rng = np.random.default_rng(3)
+    a, idx = rng.normal(size=n), rng.integers(0, rows, size=n).astype(np.float64)
+    want = {"a": a.copy(), "idx": idx.copy(), "acc": np.zeros(rows)}
+    wv = interp.run(p, "f", want)
+    for apol in ("auto", "smem"):
+        got = {"a": ViewStorage.from_values("a", a), "idx": ViewStorage.from_values("idx", idx),
+               "acc": ViewStorage.zeros("acc", (rows,))}
+        v = krn.execute(p, "f", got, ExecutionConfig(policy="compiled", atomic_policy=apol)).value
+        assert v == wv
+        assert np.array_equal(got["acc"].buffer, want["acc"]) and np.array_equal(got["a"].buffer, want["a"])
