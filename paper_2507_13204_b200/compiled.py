@@ -350,7 +350,10 @@ class _CompiledRun:
             if zero:
                 zero_mask |= 1 << k_
             if p["store"]:
-                ptrs[p["view"]] = v.device_ptr(dev, discard=zero)
+                # rank-2 register columns: only the written columns are stored, so the others must
+                # really hold their zeros (the kernel still skips the loads)
+                partial = "cols" in p and {c for c in p["cols"] if p["col_store"][c]} != set(range(v.extents[1]))
+                ptrs[p["view"]] = v.device_ptr(dev, discard=zero and not partial)
             elif zero:
                 ptrs[p["view"]] = 0
             else:

@@ -297,6 +297,9 @@ class TapingViolation:
     span: SourceSpan
     name: str
     overwrite_span: SourceSpan
+    # the statement whose reversal needs the value (not part of the reference's record; used by
+    # lang/tape.py to snapshot the value instead of rejecting the function)
+    stmt: object = _dc.field(default=None, compare=False, repr=False)
 
 
 @_dc.dataclass(frozen=True)
@@ -350,12 +353,15 @@ def taping_feasibility(fn, act: ActivityResult) -> TapingVerdict:
             names |= _index_views(target)
         names |= _index_views(rhs, only_if_view_in=active)
         if names:
-            needs.append((pos, frozenset(names), span))
+            needs.append((pos, frozenset(names), span, current[0]))
+
+    current = [None]
 
     def visit(body, in_kernel):
         nonlocal pos
         for s in body:
             pos += 1
+            current[0] = s
             k = kind(s)
             if k == "AssignView":
                 need(s.rhs, s.target, s.span, s.target.view)
@@ -380,12 +386,12 @@ def taping_feasibility(fn, act: ActivityResult) -> TapingVerdict:
     visit(fn.body, False)
 
     bad: list = []
-    for npos, names, nspan in needs:
+    for npos, names, nspan, nstmt in needs:
         for name in sorted(names):
             if name in loop_locals:  # dies with its kernel; cannot be replayed
-                bad.append(TapingViolation(nspan, name, loop_locals[name]))
+                bad.append(TapingViolation(nspan, name, loop_locals[name], nstmt))
                 continue
             clobber = next((w for w in writes if w[0] >= npos and w[1] == name), None)
             if clobber is not None:
-                bad.append(TapingViolation(nspan, name, clobber[2]))
+                bad.append(TapingViolation(nspan, name, clobber[2], nstmt))
     return TapingVerdict(not bad, tuple(bad))

@@ -111,3 +111,36 @@ def test_rank2_scatter_with_integer_contributions_is_exact():
             krn.execute(p, "f", {"idx": ViewStorage.from_values("idx", idx.astype(np.float64)), "acc": acc},
                         ExecutionConfig(policy=policy, atomic_policy=apol))
             assert np.array_equal(acc.buffer, want), (policy, apol)
+
+
+@pytest.mark.parametrize("policy", sorted(POLICIES))
+@pytest.mark.parametrize("n", [1, 2, 7, 130, 1030, 300_001])
+def test_taped_gradients_on_the_gpu(policy, n):
+    """differentiate(tape=True) (lang/tape.py): the emitted gradient is an ordinary program; every
+    policy must execute it like the oracle does, bit for bit (snapshots in registers or in HBM)"""
+    from oracle import interp
+    from test_tape import CASES, _inputs
+
+    for name, (prog, fn_name, wrt) in sorted(CASES.items()):
+        fn = prog.function(fn_name)
+        gp = krn.differentiate(prog, fn_name, wrt, tape=True)
+        gfn = gp.functions[-1]
+        base = _inputs(fn, n, np.random.default_rng(n))
+        shadows = [p.name for p in gfn.params[len(fn.params):]]
+        got = _views(base)
+        for s_, w in zip(shadows, wrt):
+            got[s_] = ViewStorage.zeros(s_, base[w].shape)
+        krn.execute(gp, gfn.name, got, POLICIES[policy])
+        if n <= 2000:
+            want = {k: v.copy() for k, v in base.items()}
+            for s_, w in zip(shadows, wrt):
+                want[s_] = np.zeros_like(base[w])
+            interp.run(gp, gfn.name, want)
+        else:
+            ref = _views(base)
+            for s_, w in zip(shadows, wrt):
+                ref[s_] = ViewStorage.zeros(s_, base[w].shape)
+            krn.execute(gp, gfn.name, ref, POLICIES["statements"])
+            want = {k: v.buffer for k, v in ref.items()}
+        for k in want:
+            assert_bits(got[k].buffer, want[k], f"{name} {policy} n={n} {k}")

@@ -282,3 +282,25 @@ def test_untouched_local_read_at_neighbours_reads_as_zero():
         got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
         assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"n={n} value")
         assert_bits(got["a"].buffer, want["a"], f"n={n} a")
+
+
+def test_rank2_partial_column_store_keeps_the_other_columns():
+    """found by the taped-gradient test: a zero-provenance rank-2 View of which a kernel writes
+    only some columns must still read as zero in the others afterwards"""
+    from oracle import interp
+
+    src = """fn f(m: view<f64, 2>, out: view<f64, 2>) -> f64 {
+        parallel_for i in 0..extent(m, 0) { out(i, 1) = m(i, 0) * 2.0; }
+        return parallel_sum(out); }"""
+    prog = parse(src)
+    for n in (1, 130, 5000):
+        m = np.random.default_rng(n).normal(size=(n, 3))
+        want = {"m": m.copy(), "out": np.zeros((n, 3))}
+        wv = interp.run(prog, "f", want)
+        # poison the pool so that a skipped zero fill shows
+        junk = ViewStorage.from_values("junk", np.full((n, 3), 7.0))
+        junk.device_ptr(krn.Device.get())
+        del junk
+        got = {"m": ViewStorage.from_values("m", m), "out": ViewStorage.zeros("out", (n, 3))}
+        assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"n={n} value")
+        assert_bits(got["out"].buffer, want["out"], f"n={n} out")
