@@ -25,16 +25,23 @@ def programs(draw):
     temps = [f"t{k}" for k in range(ntemps)]
     use_idx = draw(st.booleans())
     use_c = draw(st.booleans())
-    params = ["a: view<f64, 1>", "b: view<f64, 1>"] + (["idx: view<f64, 1>"] if use_idx else []) + (["c: f64"] if use_c else [])
+    use_m = draw(st.booleans())  # rank-2 Views: rows at the running index, literal columns
+    params = (["a: view<f64, 1>", "b: view<f64, 1>"] + (["idx: view<f64, 1>"] if use_idx else [])
+              + (["m: view<f64, 2>"] if use_m else []) + (["c: f64"] if use_c else []))
     lines = [f'    let {t}: view<f64, 1> = view("{t}", extent(a, 0));' for t in temps]
+    if use_m:
+        lines.append('    let q: view<f64, 2> = view("q", extent(a, 0), extent(m, 1));')
     scalars: list = []
 
     def leaf(allow):
         # gather results are not read inside kernels: the reference's transform has no reduction
         # reversal for an active function-scope scalar used in a kernel body (it would emit an
         # assignment to a non-local scalar, which its own validator forbids)
-        kinds = ["a", "b", "lit"] + (["c"] if use_c else []) + (["tmp"] if allow else []) + ["i"]
+        kinds = ["a", "b", "lit"] + (["c"] if use_c else []) + (["tmp"] if allow else []) + ["i"] + \
+                (["m", "q"] if use_m else [])
         k = draw(st.sampled_from(kinds))
+        if k in ("m", "q"):
+            return f"{k}(i, {draw(st.integers(0, 2))})"
         if k == "a":
             return "a(i)"
         if k == "b":
@@ -62,7 +69,8 @@ def programs(draw):
     nstmts = draw(st.integers(2, 6))
     for _ in range(nstmts):
         kind_ = draw(st.sampled_from(["point", "point", "stencil", "inplace", "copy", "fill", "accv", "accs", "gather"]
-                                     + (["indirect"] if use_idx else [])))
+                                     + (["indirect"] if use_idx else [])
+                                     + (["r2w", "r2w", "r2bulk", "r2gather"] if use_m else [])))
         dst = draw(st.sampled_from(temps))
         others = [t for t in temps if t != dst]
         if kind_ == "point":
@@ -88,17 +96,30 @@ def programs(draw):
             name = f"s{len(scalars)}"
             lines.append(f"    {name} = parallel_sum({draw(st.sampled_from(temps + ['a']))});")
             scalars.append(name)
+        elif kind_ == "r2w":
+            op = draw(st.sampled_from(["=", "+=", "-="]))
+            lines.append(f"    parallel_for i in 0..extent(a, 0) {{ q(i, {draw(st.integers(0, 2))}) {op} {expr(2, temps)}; }}")
+        elif kind_ == "r2bulk":
+            lines.append(draw(st.sampled_from([
+                f"    deep_copy(q, {draw(st.sampled_from(LITS))});", "    deep_copy(q, m);",
+                "    parallel_sum(q, m);", f"    parallel_sum(q, {draw(st.sampled_from(LITS))});"])))
+        elif kind_ == "r2gather":
+            name = f"s{len(scalars)}"
+            lines.append(f"    {name} = parallel_sum(q);")
+            scalars.append(name)
         elif kind_ == "indirect":
             lines.append(f"    parallel_for i in 0..extent(idx, 0) {{ {dst}(i) = a(idx(i)) * {draw(st.sampled_from(LITS))} + b(i); }}")
     ret = draw(st.sampled_from(temps))
     tail = f"    r = parallel_sum({ret});\n    return r" + (f" + {scalars[0]} * 0.5" if scalars and draw(st.booleans()) else "") + ";"
     text = "fn f(" + ", ".join(params) + ") -> f64 {\n" + "\n".join(lines) + "\n" + tail + "\n}\n"
-    return text, use_idx, use_c
+    return text, use_idx, use_c, use_m
 
 
-def _inputs(n, use_idx, use_c, seed):
+def _inputs(n, use_idx, use_c, seed, use_m=False):
     rng = np.random.default_rng(seed)
     d = {"a": rng.normal(size=n), "b": rng.normal(size=n)}
+    if use_m:
+        d["m"] = rng.normal(size=(n, 3))
     if use_idx:
         d["idx"] = rng.integers(0, n, size=n).astype(np.float64)
     if use_c:
@@ -125,12 +146,12 @@ def _close(got, want, atomic):
 def test_random_programs_match_the_oracle(prog, n, seed):
     from oracle import interp
 
-    text, use_idx, use_c = prog
+    text, use_idx, use_c, use_m = prog
     try:
         program = krn.parse(text)
     except (krn.ParseError, krn.ValidationError):
         assume(False)
-    inputs = _inputs(n, use_idx, use_c, seed)
+    inputs = _inputs(n, use_idx, use_c, seed, use_m)
     want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
     with np.errstate(all="ignore"):
         wv = interp.run(program, "f", want)
@@ -147,21 +168,26 @@ def test_random_programs_match_the_oracle(prog, n, seed):
 
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
-            gp = krn.differentiate(program, "f", ("a", "b"))
+            wrt = ("a", "b") + (("m",) if use_m else ())
+            try:
+                gp = krn.differentiate(program, "f", wrt)
+            except krn.NotFeasible:
+                # the reference refuses; the snapshot rewrite (lang/tape.py) may still accept
+                gp = krn.differentiate(program, "f", wrt, tape=True)
     except krn.NotFeasible:
         return
     gfn = gp.functions[-1]
     shadows = [p.name for p in gfn.params[len(program.functions[0].params):]]
     want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
     for s in shadows:
-        want[s] = np.zeros(n)
+        want[s] = np.zeros((n, 3) if s == "_d_m" else n)
     with np.errstate(all="ignore"):
         interp.run(gp, gfn.name, want)
     atomic = use_idx and "idx(i)" in text
     for policy in ("compiled", "pointwise", "statements"):
         got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in inputs.items()}
         for s in shadows:
-            got[s] = ViewStorage.zeros(s, (n,))
+            got[s] = ViewStorage.zeros(s, (n, 3) if s == "_d_m" else (n,))
         krn.execute(gp, gfn.name, got, _cfg(policy))
         for k, v in got.items():
             if isinstance(v, ViewStorage):

@@ -103,3 +103,69 @@ def test_what_cannot_be_snapshotted_still_raises():
         return parallel_sum(y); }""")
     with pytest.raises(krn.NotFeasible):
         krn.differentiate(p, "f", ("x",), tape=True)
+
+
+def test_random_programs_taped_gradient_against_finite_differences():
+    """random programs the reference refuses (in-place updates of Views whose values an earlier
+    statement's reversal needs): the taped gradient must agree with central differences of the
+    ORIGINAL primal (oracle interpreter, n = 4)"""
+    import warnings
+
+    from hypothesis import HealthCheck, assume, given, settings, strategies as st
+
+    from oracle import interp
+    from test_gpu_random_programs import _inputs as fuzz_inputs, programs
+
+    checked = [0]
+
+    @settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck), database=None)
+    @given(programs(), st.integers(0, 10**6))
+    def run(prog, seed):
+        text, use_idx, use_c, use_m = prog
+        assume(not use_idx)
+        program = krn.parse(text)
+        wrt = ("a", "b") + (("m",) if use_m else ())
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            try:
+                krn.differentiate(program, "f", wrt)
+                assume(False)  # feasible without a tape: covered elsewhere
+            except krn.NotFeasible:
+                pass
+            try:
+                gp = krn.differentiate(program, "f", wrt, tape=True)
+            except krn.NotFeasible:
+                assume(False)
+        gfn = gp.functions[-1]
+        n = 4
+        base = fuzz_inputs(n, use_idx, use_c, seed, use_m)
+
+        def value(d):
+            call = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+            with np.errstate(all="ignore"):
+                return interp.run(program, "f", call)
+
+        v0 = value(base)
+        assume(np.isfinite(v0) and abs(v0) < 1e6)
+        call = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in base.items()}
+        shadows = [p.name for p in gfn.params[len(program.functions[0].params):]]
+        active = [s_[3:] for s_ in shadows]
+        for s_ in shadows:
+            call[s_] = np.zeros_like(base[s_[3:]])
+        with np.errstate(all="ignore"):
+            interp.run(gp, gfn.name, call)
+        h = 1e-5
+        for w in active:
+            got = call["_d_" + w].reshape(-1)
+            for k in range(got.size):
+                up = {a: (b.copy() if isinstance(b, np.ndarray) else b) for a, b in base.items()}
+                dn = {a: (b.copy() if isinstance(b, np.ndarray) else b) for a, b in base.items()}
+                up[w].reshape(-1)[k] += h
+                dn[w].reshape(-1)[k] -= h
+                fd = (value(up) - value(dn)) / (2 * h)
+                scale = max(1.0, abs(fd), abs(v0))
+                assert abs(got[k] - fd) <= 2e-5 * scale, (text, w, k, got[k], fd)
+        checked[0] += 1
+
+    run()
+    assert checked[0] >= 10  # the generator does produce functions that need a tape
