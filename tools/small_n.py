@@ -1,4 +1,4 @@
-"""Launches the headline objective + gradient at the paper's sizes, both policies,
+"""Launches the headline objective + gradient at the paper's sizes, all three policies,
 a few times each (meant to run under `ncu --metrics gpu__time_duration.sum`)."""
 import os
 import sys
@@ -14,7 +14,7 @@ gp = krn.differentiate(lap, FN, ("x", "b"))
 for n in (5000, 10000):
     rng = np.random.default_rng(0)
     x, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
-    for policy in ("fused", "statements"):
+    for policy in ("fused", "compiled", "statements"):
         cfg = krn.ExecutionConfig(policy=policy)
         for rep in range(3):
             krn.execute(lap, FN, {"x": x.copy(), "b": b.copy()}, cfg)
