@@ -93,6 +93,29 @@ __device__ __forceinline__ double krn_warp_tree(double v)
     return v;
 }
 
+// Four 32-leaf subtrees at once: r_e of lane L is leaf 32*e + L of a 128-leaf tree (the lane-strided
+// mapping of the generated kernels).  Instead of four butterflies (20 shuffles) the lanes split the
+// work: after the xor-1 level even lanes carry subtrees 0,1 and odd lanes 2,3, after the xor-2 level
+// every lane carries ONE subtree, three more levels finish it, two more fold the four roots:
+// 8 shuffles.  Every addition pairs the same two nodes as the reference's tree (operands possibly
+// swapped, and IEEE addition is commutative), so the result is bit-identical.  Valid in all lanes.
+__device__ __forceinline__ double krn_warp_tree4(double r0, double r1, double r2, double r3)
+{
+    const int lane = threadIdx.x & 31;
+    const bool b0 = lane & 1, b1 = lane & 2;
+    double k0 = b0 ? r2 : r0, k1 = b0 ? r3 : r1;  // kept
+    double s0 = b0 ? r0 : r2, s1 = b0 ? r1 : r3;  // sent to the partner, which keeps them
+    k0 = k0 + __shfl_xor_sync(KRN_FULL_MASK, s0, 1);
+    k1 = k1 + __shfl_xor_sync(KRN_FULL_MASK, s1, 1);
+    double k = b1 ? k1 : k0, s = b1 ? k0 : k1;
+    k = k + __shfl_xor_sync(KRN_FULL_MASK, s, 2);
+#pragma unroll
+    for (int o = 4; o < KRN_WARP; o <<= 1) k = k + __shfl_xor_sync(KRN_FULL_MASK, k, o);
+    // lane bits (b0, b1) now select the subtree: 00 -> 0, 01(b1) -> 1, 10(b0) -> 2, 11 -> 3
+    k = k + __shfl_xor_sync(KRN_FULL_MASK, k, 2);  // (0 + 1) in lanes with b0 = 0, (2 + 3) in the others
+    return k + __shfl_xor_sync(KRN_FULL_MASK, k, 1);
+}
+
 // Tree over `count` (power of two, <= 1024) consecutive nodes held in shared
 // memory, by the first warp; result valid in every lane of warp 0.
 __device__ __forceinline__ double krn_smem_tree(const double *s, int count, int lane)

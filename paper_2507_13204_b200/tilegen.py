@@ -322,8 +322,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
           f"{r}[e] : krn_tree_pad((krn_u64)KRN_IT(e), (krn_u64)n); }}")
         if strided:
             # element e of the 32 lanes = 32 consecutive leaves: four 32-leaf subtrees, then two levels
-            w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
-            w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
+            w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
         else:
             w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
         w("        int m_ = t;")
@@ -729,8 +728,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         val = f"{regs[src]}[e]" if src in regs else f"{wins[src]}[wq_[e]]"
         w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = {val}; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n); }}")
-        w("        for (int e = 0; e < 4; ++e) R[e] = krn_warp_tree(R[e]);")
-        w("        double node = (R[0] + R[1]) + (R[2] + R[3]);")
+        w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
         w("        int m_ = t;")
         w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
         w("        tstack[tdepth++] = node;")
