@@ -159,7 +159,9 @@ int krn_laplacian_partials(krn_ctx *ctx, double *d_out, size_t count);
 /* ---- generated kernels (parallel_for bodies compiled from the program tree;
  *      replaces _Compiler/_Interpreter.parallel_for, runtime.py:230-447, 567-624)
  * `cuda_source` is CUDA C++ for sm_100a; it may #include "krn_prelude.cuh"
- * (shipped inside the library).  Compiled with --fmad=false. */
+ * (shipped inside the library).  Compiled with --fmad=false.  Compiled images are
+ * cached on disk under $KRN_CACHE_DIR (default ~/.cache/krn_b200; empty = off),
+ * keyed by source, prelude, options and NVRTC version. */
 int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_module **out);
 int krn_module_destroy(krn_module *m);
 /* launch `name` over `n_iterations` (grid sized by the library: a multiple of

@@ -5,6 +5,12 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <string>
 #include <vector>
@@ -101,6 +107,77 @@ int driver_fail(const char *what, CUresult r)
     return KRN_E_CUDA;
 }
 
+// ---- on-disk cache of compiled modules ------------------------------------------------------
+// NVRTC takes 0.3-2 s per generated module; the cubin only depends on the source text, the prelude,
+// the options and the compiler version, so it is kept under $KRN_CACHE_DIR (default
+// $XDG_CACHE_HOME/krn_b200 or ~/.cache/krn_b200; KRN_CACHE_DIR= (empty) switches the cache off).
+// A damaged or stale file is simply recompiled over.
+std::string cache_dir()
+{
+    const char *d = getenv("KRN_CACHE_DIR");
+    if (d) return d;  // may be empty: disabled
+    const char *x = getenv("XDG_CACHE_HOME");
+    if (x && *x) return std::string(x) + "/krn_b200";
+    const char *h = getenv("HOME");
+    return (h && *h) ? std::string(h) + "/.cache/krn_b200" : std::string();
+}
+
+unsigned long long fnv1a(const char *p, size_t n, unsigned long long h)
+{
+    for (size_t i = 0; i < n; ++i) {
+        h ^= (unsigned char)p[i];
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+std::string cache_path(const char *source, const char *const *opts, int nopts, int major, int minor)
+{
+    std::string dir = cache_dir();
+    if (dir.empty()) return std::string();
+    unsigned long long a = 14695981039346656037ull, b = 0x9e3779b97f4a7c15ull;
+    auto mix = [&](const char *p, size_t n) {
+        a = fnv1a(p, n, a);
+        b = fnv1a(p, n, b ^ n);
+    };
+    mix(source, strlen(source));
+    mix(kPreludeSource, sizeof(kPreludeSource));
+    for (int i = 0; i < nopts; ++i) mix(opts[i], strlen(opts[i]));
+    char tail[96];
+    snprintf(tail, sizeof tail, "/%016llx%016llx_nvrtc%d.%d.cubin", a, b, major, minor);
+    return dir + tail;
+}
+
+bool read_file(const std::string &path, std::vector<char> &out)
+{
+    FILE *f = fopen(path.c_str(), "rb");
+    if (!f) return false;
+    fseek(f, 0, SEEK_END);
+    long n = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    bool ok = n > 0;
+    if (ok) {
+        out.resize(size_t(n));
+        ok = fread(out.data(), 1, size_t(n), f) == size_t(n);
+    }
+    fclose(f);
+    return ok;
+}
+
+void write_file_atomically(const std::string &path, const std::vector<char> &data)
+{
+    std::string dir = path.substr(0, path.rfind('/'));
+    for (size_t i = 1; i <= dir.size(); ++i) {  // mkdir -p
+        if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    }
+    std::string tmp = path + ".tmp" + std::to_string((long)getpid());
+    FILE *f = fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+    ok = fclose(f) == 0 && ok;
+    if (!ok || rename(tmp.c_str(), path.c_str()) != 0) unlink(tmp.c_str());
+}
+
 }  // namespace
 
 extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_module **out)
@@ -112,6 +189,24 @@ extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_mod
     KRN_CUDA(cudaSetDevice(ctx->device));
     KRN_CUDA(cudaFree(nullptr));  // make sure the primary context exists
 
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
+                          "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-DKRN_NO_LD256"};
+    const int nopts = int(sizeof(opts) / sizeof(opts[0])) - (api.ld256 ? 1 : 0);
+    int major = 0, minor = 0;
+    api.Version(&major, &minor);
+    const std::string cached = cache_path(cuda_source, opts, nopts, major, minor);
+    if (!cached.empty()) {
+        std::vector<char> image;
+        if (read_file(cached, image)) {
+            krn_module *m = new krn_module();
+            if (api.ModuleLoadData(&m->module, image.data()) == CUDA_SUCCESS) {
+                *out = m;
+                return KRN_OK;
+            }
+            delete m;  // unreadable image: compile again and overwrite it
+        }
+    }
+
     nvrtcProgram prog;
     const char *headers[] = {kPreludeSource};
     const char *names[] = {"krn_prelude.cuh"};
@@ -119,9 +214,6 @@ extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_mod
         krn_set_error("nvrtcCreateProgram failed");
         return KRN_E_NVRTC;
     }
-    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
-                          "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-DKRN_NO_LD256"};
-    const int nopts = int(sizeof(opts) / sizeof(opts[0])) - (api.ld256 ? 1 : 0);
     nvrtcResult cr = api.CompileProgram(prog, nopts, opts);
     if (cr != NVRTC_SUCCESS) {
         size_t n = 0;
@@ -144,6 +236,7 @@ extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_mod
         delete m;
         return driver_fail("cuModuleLoadData", r);
     }
+    if (!cached.empty()) write_file_atomically(cached, cubin);
     *out = m;
     return KRN_OK;
 }

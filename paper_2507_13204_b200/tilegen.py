@@ -131,6 +131,24 @@ def plan_group(builder, group, an, live_after: set) -> dict:
                 has_user_ops=any(l.what != "apply" for l in group.ops), strided=strided)
 
 
+def _specialise_interior_chunks(L: list, start: int, end: int, cond: str, subst: dict) -> None:
+    """L[start:end] is the text of the step loop.  Almost every warp's whole chunk (all its steps,
+    halo included) lies inside the range, far from both ends; for those warps the per-step
+    classification (`full`, `live`, `interior`, tail activity: 64-bit compares on every step) is
+    decided ONCE: the loop is emitted twice, the first copy with those flags as compile-time
+    constants (the compiler drops every slow-path branch), selected by `cond` per warp."""
+    general = L[start:end]
+    fast = []
+    for line in general:
+        for old, new in subst.items():
+            if line.strip() == old:
+                line = line.replace(old, new)
+        fast.append(line)
+    L[start:end] = ([f"    const bool chunk_interior_ = {cond};", "    if (chunk_interior_) {"] + fast +
+                    ["    } else {"] + general + ["    }"])
+
+
+
 def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b = builder
     elided: set = set()
@@ -178,6 +196,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w("    const bool full = j0 + 4 <= n_safe;")
         w("    const bool live = j0 < n_launch;")
 
+    loop_start = len(L)
     if gather is not None:
         # steps is 1 or 8 (compiled.py): unrolled, so that the step index - and with it the shape of
         # the binary-counter tree over the steps - is known at compile time (registers, no local memory)
@@ -331,6 +350,13 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("    }")
     w("    }  // step of the batch")
     w("    }  // steps")
+    _specialise_interior_chunks(
+        L, loop_start, len(L),
+        f"wbase >= {LO + OFF} && wbase + (krn_i64)128 * steps + {UP + OFF} <= n && wbase + (krn_i64)128 * steps <= n_safe",
+        {"const bool full = j0 + 128 <= n_safe;": "const bool full = true;",
+         "const bool full = j0 + 4 <= n_safe;": "const bool full = true;",
+         "const bool live = j0 < n_launch;": "const bool live = true;",
+         f"const bool interior = full && j0 >= {LO + OFF} && j0 + {span + UP + OFF} <= n;": "const bool interior = true;"})
     w("#undef KRN_IT")
     if direct:
         w("    krn_priv_end(E);")
@@ -495,6 +521,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     w("    int wq_[5];  // window position of each slot's iteration")
     w(f"    for (int e = 0; e < 4; ++e) wq_[e] = e * 32 + lane_ + {HLO};")
     w(f"    wq_[4] = lane_ < {HLO} ? lane_ : 128 + lane_;")
+    loop_start = len(L)
     w("    for (int t = 0; t < steps; ++t) {")
     w("    const krn_i64 j0 = wbase + (krn_i64)t * 128;  // the warp's first own iteration of this step")
     w(f"    const krn_i64 wlo = j0 - {HLO};                // iteration held by window position 0")
@@ -735,6 +762,15 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("    }")
     w("    __syncwarp();")
     w("    }  // steps")
+    _specialise_interior_chunks(
+        L, loop_start, len(L),
+        f"wbase >= {LO + HLO} && wbase + (krn_i64)128 * steps + {HHI + UP} <= n && wbase + (krn_i64)128 * steps <= n_safe",
+        {"const bool full = j0 + 128 <= n_safe;": "const bool full = true;",
+         "const bool live = j0 < n_launch;": "const bool live = true;",
+         f"const bool interior = full && wlo >= {LO} && j0 + {128 + HHI + UP} <= n;": "const bool interior = true;",
+         "for (int e = 0; e < 4; ++e) { it_[e] = j0 + e * 32 + lane_; act_[e] = live && it_[e] < n_launch; }":
+             "for (int e = 0; e < 4; ++e) { it_[e] = j0 + e * 32 + lane_; act_[e] = true; }",
+         f"act_[4] = live && lane_ < {HLO + HHI} && it_[4] >= 0 && it_[4] < n_launch;": f"act_[4] = lane_ < {HLO + HHI};"})
     if direct:
         w("    krn_priv_end(E);")
     if gather is not None:

@@ -272,3 +272,35 @@ def test_bench_ratio_runs():
         assert r.gradient_entries == 20_000 and math.isfinite(r.ratio)
     with pytest.raises(ValueError):
         krn.bench_ratio(lap, "normRes1DLaplacianSQ", 100, reps=2)
+
+
+def test_compiled_modules_are_cached_on_disk(tmp_path, monkeypatch):
+    """krn_module_compile keeps the cubin under $KRN_CACHE_DIR keyed by source/options/compiler; a
+    damaged file is recompiled over, an empty KRN_CACHE_DIR switches the cache off"""
+    import ctypes as C
+
+    from paper_2507_13204_b200 import _cabi
+
+    dev = krn.Device.get()
+    src = ('#include "krn_prelude.cuh"\nextern "C" __global__ void cache_probe_%d(double *p) { p[0] = %d.0; }\n'
+           % (id(tmp_path) % 100000, id(tmp_path) % 977))
+
+    def compile_once():
+        h = C.c_void_p()
+        _cabi.check(dev.lib.krn_module_compile(dev.h, src.encode(), C.byref(h)))
+        _cabi.check(dev.lib.krn_module_destroy(h))
+
+    monkeypatch.setenv("KRN_CACHE_DIR", str(tmp_path / "cache"))
+    compile_once()
+    files = list((tmp_path / "cache").iterdir())
+    assert len(files) == 1 and files[0].suffix == ".cubin" and files[0].stat().st_size > 0
+    stamp = files[0].stat().st_mtime_ns
+    compile_once()                                  # served from the cache: file untouched
+    assert files[0].stat().st_mtime_ns == stamp and len(list((tmp_path / "cache").iterdir())) == 1
+    files[0].write_bytes(b"not a cubin")            # damaged image: recompiled and replaced
+    compile_once()
+    assert files[0].stat().st_size > 100
+    monkeypatch.setenv("KRN_CACHE_DIR", "")
+    other = tmp_path / "cache2"
+    compile_once()
+    assert not other.exists()
