@@ -178,6 +178,17 @@ int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_
 /* ---- status word: 8 x int64 {code, line, view id, index0, index1, 0, 0, 0} of the
  *      first failing access (first error wins) ---- */
 int krn_status_reset(krn_ctx *ctx);
+
+/* Start of one execute(): clears the status word AND the context's function-scope scalar slots
+ * (reference: `self.scalars = {}` per run, runtime.py:468-479) with a single memset, and returns
+ * the slot array (doubles, device memory, owned by the context; `capacity` slots). */
+int krn_run_begin(krn_ctx *ctx, double **d_slots, size_t *capacity);
+
+/* The context's reduction workspace for generated kernels that fold a parallel_sum into their
+ * epilogue (partials + scratch of at least `blocks` doubles each, arrival ticket kept at zero
+ * between launches): no per-launch allocation.  Valid until the next call that needs more. */
+int krn_reduce_workspace(krn_ctx *ctx, size_t blocks, double **d_partials, double **d_scratch,
+                         unsigned int **d_ticket);
 int krn_status_device_ptr(krn_ctx *ctx, long long **d_status);
 int krn_status_read(krn_ctx *ctx, long long h_status[8]);      /* synchronous */
 

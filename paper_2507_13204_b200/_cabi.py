@@ -73,6 +73,8 @@ SIGNATURES = {
     "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),
     "krn_module_launch_exact": (_i, [_vp, _vp, C.c_char_p, _sz, C.c_uint, _sz, _pp]),
     "krn_status_reset": (_i, [_vp]),
+    "krn_run_begin": (_i, [_vp, _pp, C.POINTER(C.c_size_t)]),
+    "krn_reduce_workspace": (_i, [_vp, _sz, _pp, _pp, _pp]),
     "krn_status_device_ptr": (_i, [_vp, _pp]),
     "krn_status_read": (_i, [_vp, C.POINTER(C.c_longlong)]),
 }

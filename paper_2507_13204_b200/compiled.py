@@ -181,6 +181,15 @@ def run(dev, fn, views: dict, scalars: dict, cfg):
     return r.go()
 
 
+class _Borrowed:
+    """A device pointer owned by someone else (the context's scalar slots)."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, ptr: int):
+        self.ptr = ptr
+
+
 class _CompiledRun:
     def __init__(self, dev, plan: CompiledPlan, views, scalars, cfg):
         self.dev, self.plan, self.views, self.cfg = dev, plan, views, cfg
@@ -192,6 +201,21 @@ class _CompiledRun:
 
     # ---- host-only rehearsal ----------------------------------------------------------
     def dry_check(self) -> bool:
+        """Memoised per plan on the extents of the bound Views (the check depends on nothing else,
+        apart from aliasing, which is looked at every time)."""
+        objs = [id(v) for v in self.views.values()]
+        if len(set(objs)) != len(objs):
+            return False  # one storage object bound to two names: registers/windows would hide the aliasing
+        key = tuple((k, v.extents) for k, v in self.views.items())
+        memo = self.plan.__dict__.setdefault("_dry_memo", {})
+        hit = memo.get(key)
+        if hit is None:
+            if len(memo) > 256:
+                memo.clear()
+            hit = memo[key] = self._dry_check()
+        return hit
+
+    def _dry_check(self) -> bool:
         from .runtime import _index_value
 
         ext = {k: v.extents for k, v in self.views.items()}
@@ -203,10 +227,6 @@ class _CompiledRun:
         def trip(e):
             return int(_index_value(e, {k: _V(v) for k, v in ext.items()}))
 
-        # one storage object bound to two names: registers/windows would hide the aliasing
-        objs = [id(v) for v in self.views.values()]
-        if len(set(objs)) != len(objs):
-            return False
         try:
             for step in self.plan.steps:
                 tag = step[0]
@@ -293,9 +313,14 @@ class _CompiledRun:
 
         dev = self.dev
         self.mod = dev.module(self.plan.source)
-        self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
-        dev.fill(self.S.ptr, self.plan.nslots, 0.0)
-        _cabi.check(dev.lib.krn_status_reset(dev.h))
+        # status word and scalar slots live side by side in the context: one memset starts the run
+        slots, cap = C.c_void_p(), C.c_size_t()
+        _cabi.check(dev.lib.krn_run_begin(dev.h, C.byref(slots), C.byref(cap)))
+        if self.plan.nslots <= cap.value:
+            self.S = _Borrowed(slots.value)
+        else:
+            self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
+            dev.fill(self.S.ptr, self.plan.nslots, 0.0)
         for step in self.plan.steps:
             getattr(self, "do_" + step[0])(*step[1:])
         return self.finish()
@@ -375,13 +400,16 @@ class _CompiledRun:
         if g.gather is not None:
             stmt, accumulate = g.gather
             red_out, acc = self.S.ptr + 8 * self.b.slot(stmt.dst), int(accumulate)
-        needed = set()
-        for loop in g.ops:
-            if loop.what == "apply":
-                needed.add(loop.apply_of[0])
-                continue
-            staged = {st.view for st in loop.sites if st.mode == "gather"}
-            needed |= {a.view for a in loop.accesses() if not (a.atomic and a.view in staged)}
+        needed = recipe.get("_needed")
+        if needed is None:  # Views the kernel touches (walks the tree: once per plan, not per call)
+            needed = set()
+            for loop in g.ops:
+                if loop.what == "apply":
+                    needed.add(loop.apply_of[0])
+                    continue
+                staged = {st.view for st in loop.sites if st.mode == "gather"}
+                needed |= {a.view for a in loop.accesses() if not (a.atomic and a.view in staged)}
+            recipe["_needed"] = needed
         from .runtime import atomic_choice
 
         env = self.env(ptrs, needed - set(ptrs),
@@ -391,11 +419,10 @@ class _CompiledRun:
         steps = 1 if n_launch <= (1 << 20) else 8  # must be a power of two (tree node per block)
         nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)
         if g.gather is not None:
-            ws = _DeviceBuffer(dev, 8 * 2 * nblocks + 64)
-            tk = dev.ticket_ptr()
-            extra += [C.c_void_p(ws.ptr), C.c_void_p(ws.ptr + 8 * nblocks), C.c_void_p(tk), C.c_void_p(red_out),
-                      C.c_int(acc)]
-            self._keep = ws
+            # the context's reduction workspace: no allocation inside the launch sequence
+            pa, sc, tk = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            _cabi.check(dev.lib.krn_reduce_workspace(dev.h, nblocks, C.byref(pa), C.byref(sc), C.byref(tk)))
+            extra += [pa, sc, tk, C.c_void_p(red_out), C.c_int(acc)]
         else:
             extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]
         extra.append(C.c_int(steps))

@@ -52,5 +52,6 @@ void krn_set_error(const char *fmt, ...);
 
 // make sure each ping-pong half of the reduction workspace holds `count` doubles
 int krn_reserve_partials(krn_ctx *ctx, size_t count);
+#define KRN_SCALAR_SLOTS 120  // function-scope scalar slots that live next to the status word
 
 static inline bool krn_aligned32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }

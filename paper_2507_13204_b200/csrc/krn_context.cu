@@ -56,8 +56,9 @@ extern "C" int krn_ctx_create(int device, void *cuda_stream, krn_ctx **out)
     KRN_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
     KRN_CUDA(cudaMalloc(&ctx->d_ticket, sizeof(unsigned int)));
     KRN_CUDA(cudaMemset(ctx->d_ticket, 0, sizeof(unsigned int)));
-    KRN_CUDA(cudaMalloc(&ctx->d_status, 8 * sizeof(long long)));
-    KRN_CUDA(cudaMemset(ctx->d_status, 0, 8 * sizeof(long long)));
+    // one block: [status: 8 x int64][scalar slots: KRN_SCALAR_SLOTS doubles], reset by ONE memset
+    KRN_CUDA(cudaMalloc(&ctx->d_status, (8 + KRN_SCALAR_SLOTS) * 8));
+    KRN_CUDA(cudaMemset(ctx->d_status, 0, (8 + KRN_SCALAR_SLOTS) * 8));
     int rc = krn_reserve_partials(ctx, 4096);
     if (rc) return rc;
     *out = ctx;
@@ -277,6 +278,27 @@ extern "C" int krn_status_reset(krn_ctx *ctx)
 {
     KRN_REQUIRE(ctx != nullptr, "null context");
     KRN_CUDA(cudaMemsetAsync(ctx->d_status, 0, 8 * sizeof(long long), ctx->stream));
+    return KRN_OK;
+}
+
+extern "C" int krn_run_begin(krn_ctx *ctx, double **d_slots, size_t *capacity)
+{
+    KRN_REQUIRE(ctx && d_slots && capacity, "null argument");
+    KRN_CUDA(cudaMemsetAsync(ctx->d_status, 0, (8 + KRN_SCALAR_SLOTS) * 8, ctx->stream));
+    *d_slots = reinterpret_cast<double *>(ctx->d_status + 8);
+    *capacity = KRN_SCALAR_SLOTS;
+    return KRN_OK;
+}
+
+extern "C" int krn_reduce_workspace(krn_ctx *ctx, size_t blocks, double **d_partials, double **d_scratch,
+                                    unsigned int **d_ticket)
+{
+    KRN_REQUIRE(ctx && d_partials && d_scratch && d_ticket, "null argument");
+    int rc = krn_reserve_partials(ctx, blocks);
+    if (rc) return rc;
+    *d_partials = ctx->d_partials;
+    *d_scratch = ctx->d_partials + ctx->partial_capacity;
+    *d_ticket = ctx->d_ticket;
     return KRN_OK;
 }
 
