@@ -263,6 +263,8 @@ class _CompiledRun:
                             return False  # a literal column outside the View: the statement path reports it
                     if g.gather is not None and ext[g.gather[0].src][0] != n:
                         return False
+                    if recipe.get("gather_cols") and ext[g.gather[0].src][1] != recipe["gather_cols"]:
+                        return False  # the fused flat reduction was laid out for exactly these columns
                     for v in recipe["elided_views"]:
                         if n > ext[v][0]:
                             return False  # the elided checks assumed extent >= range
@@ -421,7 +423,8 @@ class _CompiledRun:
         if g.gather is not None:
             # the context's reduction workspace: no allocation inside the launch sequence
             pa, sc, tk = C.c_void_p(), C.c_void_p(), C.c_void_p()
-            _cabi.check(dev.lib.krn_reduce_workspace(dev.h, nblocks, C.byref(pa), C.byref(sc), C.byref(tk)))
+            _cabi.check(dev.lib.krn_reduce_workspace(dev.h, nblocks * max(1, recipe.get("gather_cols", 0)),
+                                                     C.byref(pa), C.byref(sc), C.byref(tk)))
             extra += [pa, sc, tk, C.c_void_p(red_out), C.c_int(acc)]
         else:
             extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]

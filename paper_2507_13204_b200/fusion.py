@@ -145,6 +145,20 @@ def guarded_accesses(loop: "LoopOp") -> list:
     return out
 
 
+def group_columns(ops: list, view: str) -> set:
+    """Literal columns with which the loops of a group touch rank-2 `view` (apply targets included)."""
+    cols: set = set()
+    for loop in ops:
+        if loop.what == "apply":
+            if loop.apply_of[0] == view:
+                cols |= {st.column for st in loop.apply_of[1]}
+            continue
+        for a in loop.accesses():
+            if a.view == view and len(a.indices) == 2 and kind(a.indices[1]) == "IntLiteral":
+                cols.add(a.indices[1].value)
+    return cols
+
+
 def stage_name(index: int, producer) -> str:
     return f"__stage{index}@{id(producer)}"
 
@@ -152,6 +166,7 @@ def stage_name(index: int, producer) -> str:
 MAX_HALO = 32      # halo iterations of a warp step are handled by the 32 lanes in one extra slot
 MAX_WINDOWS = 5    # 8 warps x (128 + halo) doubles each: 5 windows stay under 48 KB of static shared memory
 MAX_ALT = 4        # out-of-place output pointers a window kernel accepts
+MAX_GATHER_COLS = 4  # a fused flat reduction of a rank-2 View stages 128 x C leaves per warp in shared memory
 # Also serve neighbour reads of READ-ONLY Views from a window.  Measured on B200 (stencil_smooth,
 # 67 M rows): no gain for the primal, -10% for the gradient - the three L1-cached loads per row are
 # all in flight at once, the window adds a shared-memory round trip - so it stays off.
@@ -701,8 +716,16 @@ def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
                 except (TypeError, ValueError):
                     src_trip = None
                 info = acc.get(src)
-                if (an.rank.get(src) == 1 and src_trip == trip and all(o.shift == 0 for o in g.ops)
-                        and (info is None or (info[0] and not info[2]))):
+                fusable = (src_trip == trip and all(o.shift == 0 for o in g.ops)
+                           and (info is None or (info[0] and not info[2])))
+                if fusable and an.rank.get(src) == 2:
+                    # flat reduction of a rank-2 View: every column must be in registers, i.e. the group
+                    # touches exactly the columns 0..C-1 (the host checks extent(src, 1) == C)
+                    fusable = windows and info is not None and 1 <= len(group_columns(g.ops, src)) <= MAX_GATHER_COLS \
+                        and group_columns(g.ops, src) == set(range(len(group_columns(g.ops, src))))
+                elif an.rank.get(src) != 1:
+                    fusable = False
+                if fusable:
                     g.gather = (stmt, op[2])
                     close()
                     continue

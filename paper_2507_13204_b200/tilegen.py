@@ -436,8 +436,14 @@ def plan_window_group(builder, group, an, live_after: set) -> dict:
                 name = fusion.stage_name(st.index, loop)
                 if st.mode == "gather" and name not in wp.stage_windows and name not in wp.stage_regs:
                     stage_cols.append((id(loop), st.index))
+    gather_cols = 0
+    if group.gather is not None and builder.rank.get(group.gather[0].src) == 2:
+        rec = next(p for p in promoted if p["view"] == group.gather[0].src)
+        gather_cols = len(rec["cols"])
+        if rec["cols"] != list(range(gather_cols)):
+            raise ValueError("flat reduction of a rank-2 View needs every column in registers")
     return dict(promoted=promoted, windows=windows, stage_cols=stage_cols, wp=wp,
-                max_shift=max(l.shift for l in group.ops), strided=True, window=True)
+                max_shift=max(l.shift for l in group.ops), strided=True, window=True, gather_cols=gather_cols)
 
 
 def _guard_margins(group, an) -> tuple:
@@ -508,6 +514,10 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     for wn in list(wins.values()) + list(stage_win_sites.values()):
         w(f"    __shared__ double {wn}_[8][{WN}];")
         w(f"    double *{wn} = {wn}_[warp_];")
+    if plan.get("gather_cols"):
+        w(f"    __shared__ double G_all_[8][{128 * plan['gather_cols']}];")
+        w("    double *G_ = G_all_[warp_];")
+        w(f"    double gn_[{8 * plan['gather_cols']}];  // the warp's tree nodes, step-major")
     # which lanes of the halo slot run statement k (it covers [j0 - hlo_k, j0 + 128 + hhi_k))
     for k, (hlo, hhi) in enumerate(wp.halo):
         if hlo or hhi:
@@ -748,7 +758,25 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("    }")
     for (_, idx) in plan["stage_cols"]:
         w(f"    if (live) {{ for (int e = 0; e < 4; ++e) if (act_[e]) stage[{idx} * ld + it_[e]] = T{idx}[e]; }}")
-    if gather is not None:
+    gcols = plan.get("gather_cols", 0)
+    if gather is not None and gcols:
+        # flat reduction of a rank-2 View (leaf index = row * C + column): the warp's 128 x C leaves
+        # are laid out in flat order in shared memory; they are C aligned 128-leaf subtrees of the
+        # reference's tree over the flattened buffer (runtime.py:643-651: pairwise_sum(view.flat))
+        src, r = gather[0].src, regs[gather[0].src]
+        w("    {")
+        w("        for (int e = 0; e < 4; ++e) {")
+        w("            const bool in_ = full || it_[e] < n;")
+        for c in range(gcols):
+            w(f"            G_[(e * 32 + lane_) * {gcols} + {c}] = in_ ? {r}c{c}[e] : "
+              f"krn_tree_pad((krn_u64)(it_[e] * {gcols} + {c}), (krn_u64)(n * {gcols}));")
+        w("        }")
+        w("        __syncwarp();")
+        for k in range(gcols):
+            w(f"        gn_[t * {gcols} + {k}] = krn_warp_tree4(G_[{128 * k} + lane_], G_[{128 * k + 32} + lane_], "
+              f"G_[{128 * k + 64} + lane_], G_[{128 * k + 96} + lane_]);")
+        w("    }")
+    elif gather is not None:
         src = gather[0].src
         w("    {")
         w("        double R[4];")
@@ -773,7 +801,29 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
          f"act_[4] = live && lane_ < {HLO + HHI} && it_[4] >= 0 && it_[4] < n_launch;": f"act_[4] = lane_ < {HLO + HHI};"})
     if direct:
         w("    krn_priv_end(E);")
-    if gather is not None:
+    if gather is not None and gcols:
+        C_ = gcols
+        w("    {")
+        w(f"        // the warp's {C_} x steps nodes start at a node index that is a multiple of `steps`: fold log2(steps) levels")
+        w(f"        for (int cnt = {C_} * steps; cnt > {C_}; cnt >>= 1)")
+        w("            for (int i = 0; i < cnt / 2; ++i) gn_[i] = gn_[2 * i] + gn_[2 * i + 1];")
+        w(f"        __shared__ double s_g[{8 * C_}];")
+        w(f"        if (lane_ == 0) for (int k = 0; k < {C_}; ++k) s_g[warp_ * {C_} + k] = gn_[k];")
+        w("        __syncthreads();")
+        w("        if (threadIdx.x == 0) {  // 8 warps x C nodes -> C nodes of the block (three exact levels)")
+        w(f"            for (int cnt = {8 * C_}; cnt > {C_}; cnt >>= 1)")
+        w("                for (int i = 0; i < cnt / 2; ++i) s_g[i] = s_g[2 * i] + s_g[2 * i + 1];")
+        w(f"            for (int k = 0; k < {C_}; ++k) partials[(krn_i64)blockIdx.x * {C_} + k] = s_g[k];")
+        w("        }")
+        w("        if (krn_last_block(ticket, gridDim.x)) {")
+        w("            // nodes past the end of the flattened View were computed from padding leaves and equal")
+        w("            // the padding of the tree over the partials: only the real ones are folded")
+        w(f"            const krn_u64 span_ = (krn_u64)1024 * steps, m_ = ((krn_u64)n * {C_} + span_ - 1) / span_;")
+        w("            double root = krn_final_tree(partials, scratch, m_);")
+        w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
+        w("        }")
+        w("    }")
+    elif gather is not None:
         w("    {")
         w("        __shared__ double s_warp[8];")
         w("        if (lane_ == 0) s_warp[warp_] = tstack[0];")
@@ -790,5 +840,6 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     return dict(name=name, promoted=every, stage_cols=plan["stage_cols"], has_stage=bool(plan["stage_cols"]),
                 gather=gather, max_shift=plan["max_shift"],
                 elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct,
-                window=True, alt=alts, hlo=HLO, hhi=HHI,
-                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (512 if gather is not None else 0))
+                window=True, alt=alts, hlo=HLO, hhi=HHI, gather_cols=gcols,
+                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (512 if gather is not None else 0)
+                + 8 * (8 * 128 + 8) * gcols)

@@ -126,9 +126,13 @@ def test_rank2_rows_become_register_columns():
     assert not any(views["_d_q"]["col_load"].values())                                   # fresh local: +0.0
     assert all(views["_d_m"]["col_store"].values()) and views["_d_r"]["store"]
     assert not recipe["stage_cols"] and plan.launch_count == 1
-    # primal: q must exist for the flat reduction (its tree interleaves the columns)
+    # primal: the flat reduction (its tree interleaves the columns) is folded into the kernel too:
+    # the warp's 128 x 3 leaves are three aligned subtrees; q is never stored
     _, shape = _shape(fn, True)
-    assert shape == ["declview", "G[kernel]", "gather", "return"]
+    assert shape == ["declview", "G[kernel+gather]", "return"]
+    plan = compiled.plan_for(fn, True)
+    recipe = [s[2] for s in plan.steps if s[0] == "group"][0]
+    assert recipe["gather_cols"] == 3 and not {p["view"]: p for p in recipe["promoted"]}["q"]["store"]
 
 
 def test_read_only_neighbour_reads_can_use_a_window(monkeypatch):

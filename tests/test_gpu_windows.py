@@ -304,3 +304,53 @@ def test_rank2_partial_column_store_keeps_the_other_columns():
         got = {"m": ViewStorage.from_values("m", m), "out": ViewStorage.zeros("out", (n, 3))}
         assert_bits(krn.execute(prog, "f", got, WIN).value, wv, f"n={n} value")
         assert_bits(got["out"].buffer, want["out"], f"n={n} out")
+
+
+@pytest.mark.parametrize("cols", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 42, 43, 127, 128, 129, 341, 342, 1023, 1024, 1025, 2731, 8192, 8193,
+                               (1 << 20) - 1, 1 << 20, (1 << 20) + 1, (1 << 20) + 8192 * 3 + 17])
+def test_fused_flat_reduction_of_rank2_views(cols, n):
+    """`parallel_sum(q)` over a rank-2 View is the reference's tree over the FLATTENED buffer
+    (leaf = row * C + column).  Fused into the producing kernel the 128 x C leaves of a warp step are
+    C aligned subtrees; the objective must keep the reference's bits for every C, around the warp /
+    block / multi-step boundaries, without q ever being stored."""
+    from oracle import interp
+
+    body = "\n".join(f"        q(i, {c}) = r(i) * m(i, {c}) + {c}.5;" for c in range(cols))
+    src = f"""fn f(m: view<f64, 2>, r: view<f64, 1>) -> f64 {{
+        let q: view<f64, 2> = view("q", extent(m, 0), extent(m, 1));
+        parallel_for i in 0..extent(m, 0) {{
+{body}
+        }}
+        s = parallel_sum(q);
+        return s; }}"""
+    prog = parse(src)
+    plan = compiled.plan_for(prog.functions[0], True)
+    assert plan.launch_count == 1 and not any(s[0] == "gather" for s in plan.steps)
+    rng = np.random.default_rng(cols * 1000 + n % 997)
+    m, r = rng.normal(size=(n, cols)), rng.normal(size=n)
+    if n <= 3000:
+        want = interp.run(prog, "f", {"m": m.copy(), "r": r.copy()})
+    else:
+        want = krn.execute(prog, "f", {"m": ViewStorage.from_values("m", m), "r": ViewStorage.from_values("r", r)},
+                           STMT).value
+    got = krn.execute(prog, "f", {"m": ViewStorage.from_values("m", m), "r": ViewStorage.from_values("r", r)}, WIN).value
+    assert_bits(got, want, f"cols={cols} n={n}")
+
+
+def test_fused_flat_reduction_needs_exactly_the_named_columns():
+    """a View with more columns than the kernel names: the fused layout does not apply, the general
+    route must still give the reference's value"""
+    from oracle import interp
+
+    src = """fn f(m: view<f64, 2>, r: view<f64, 1>) -> f64 {
+        let q: view<f64, 2> = view("q", extent(m, 0), extent(m, 1));
+        parallel_for i in 0..extent(m, 0) { q(i, 0) = r(i) * m(i, 0); q(i, 1) = m(i, 1); }
+        s = parallel_sum(q);
+        return s; }"""
+    prog = parse(src)
+    rng = np.random.default_rng(0)
+    m, r = rng.normal(size=(300, 3)), rng.normal(size=300)
+    want = interp.run(prog, "f", {"m": m.copy(), "r": r.copy()})
+    got = krn.execute(prog, "f", {"m": ViewStorage.from_values("m", m), "r": ViewStorage.from_values("r", r)}, WIN).value
+    assert_bits(got, want, "3 columns, 2 named")
