@@ -12,7 +12,8 @@ verify.py:272-280; wrt = (x, b), so 2 gradient entries per row).  The workload
 steps.  The paper's headline configuration (10,000 gradient entries,
 configs[1]) is latency bound; its gradient/primal ratio is measured too and
 reported in the "headline" object, with an L2 flush before every timed
-evaluation.
+evaluation.  configs[2] (1e6..1e9 rows) is the "sweep" object, configs[3] (2-D
+Views, injective and non-injective index maps) the "two_d_views" object.
 
 Rank 0 prints ONE JSON line.  value = rows*2*steps*ranks / max-over-ranks device
 time.  roofline.achieved uses the algorithmic bytes: 56 B/row for the gradient
@@ -349,6 +350,7 @@ def main():
             "compulsory_bytes_zero_shadows": GRAD_ZERO_BYTES_PER_ROW / PRIMAL_BYTES_PER_ROW,
         }
         line["sweep"] = sweep(dev, torch)
+        line["two_d_views"] = two_d_views(krn, dev, torch)
         line["statements_policy_large_n"] = stm
         line["compiled_policy_large_n"] = cmp_
         tp, tg = cpu_port_timing(min(rows, 20_000_000))
@@ -409,6 +411,66 @@ def sweep(dev, torch):
                     "l2": "flushed between repetitions" if flush is not None else "Views exceed L2"})
         del bufs, x, b, dx, db, xo, flush
         torch.cuda.empty_cache()
+    return out
+
+
+def two_d_views(krn, dev, torch, rows=1 << 24):
+    """BASELINE configs[3]: 2-D Views.  The reference has no MDRange, so the
+    two forms it CAN run are measured: `rowscale_rank2` (the corpus' 2-D program: rows at the running
+    index; the reference flags its adjoint atomic although the map is injective - generated as
+    conflict-free register columns) and `gather_rows_rank2` (extra_programs/: rows reached through a
+    NON-injective index map; the adjoint accumulates with hardware atomics, warp-aggregated).
+    Device time of the whole launch sequence, generated kernels (policy "compiled")."""
+    from paper_2507_13204_b200.runtime import ViewStorage
+
+    out = {}
+    rng = np.random.default_rng(5)
+    flush = torch.empty(1 << 29, dtype=torch.uint8, device="cuda")
+    for stem, bytes_primal, bytes_grad in (("rowscale_rank2", 32, 64), ("gather_rows_rank2", 40, 96)):
+        prog = krn.load_program(stem)
+        fn = prog.functions[0]
+        base = {}
+        for p in fn.params:
+            if p.name == "idx":
+                base[p.name] = ViewStorage.from_values("idx", rng.integers(0, rows, size=rows).astype(np.float64))
+            elif p.type.rank == 2:
+                base[p.name] = ViewStorage.from_values(p.name, rng.normal(size=(rows, 3)))
+            else:
+                base[p.name] = ViewStorage.from_values(p.name, rng.normal(size=rows))
+        for v in base.values():
+            v.device_ptr(dev, write=False)
+        wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+        gp = krn.differentiate(prog, fn.name, wrt)
+        gfn = gp.functions[-1]
+        cfg = krn.ExecutionConfig(policy="compiled", synchronous=False, device=dev)
+        best = {"primal": [], "grad": []}
+        launches = {}
+        for rep in range(4):
+            for which in ("primal", "grad"):
+                call = {k: v.copy() for k, v in base.items()}
+                if which == "grad":
+                    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+                        call[sp.name] = ViewStorage.zeros(sp.name, base[w].extents)
+                dev.sync()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                for _ in range(6):
+                    flush.zero_()
+                l0 = dev.launches()
+                e0.record()
+                krn.execute(prog if which == "primal" else gp, fn.name if which == "primal" else gfn.name, call, cfg)
+                e1.record()
+                torch.cuda.synchronize()
+                best[which].append(e0.elapsed_time(e1))
+                launches[which] = dev.launches() - l0
+                del call
+        tp, tg = min(best["primal"][1:]), min(best["grad"][1:])
+        out[stem] = {"rows": rows, "columns": 3, "primal_ms": tp, "grad_ms": tg, "ratio": tg / tp,
+                     "primal_launches": launches["primal"], "grad_launches": launches["grad"],
+                     "primal_compulsory_gbs": bytes_primal * rows / tp / 1e6,
+                     "grad_compulsory_gbs": bytes_grad * rows / tg / 1e6,
+                     "gradient_entries_per_s": (3 * rows + rows) / tg * 1e3}
+    out["note"] = ("compulsory bytes per row: rowscale 32 / 64, gather_rows 40 / 96 (3 gathered + 3 scattered "
+                   "columns of a randomly indexed row: sector- and atomic-bound, not HBM-bound)")
     return out
 
 
