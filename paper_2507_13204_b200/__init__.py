@@ -58,6 +58,8 @@ from .verify import (
     laplacian_oracle,
 )
 
+from .shard_program import NotShardable, ShardedProgram  # noqa: E402  (multi-GPU, beyond the reference)
+
 __version__ = "0.1.0"
 
 import os as _os

@@ -1,0 +1,112 @@
+"""GPU tier: sharded execution of row-wise functions (shard_program.py) with the real `execute`:
+the ranks of a multi-GPU run are played by threads on ONE device (segments serialised by a lock,
+the all-reduce a barrier), and once by two processes over gloo sharing the device - NCCL refuses
+two ranks on one GPU.  Compared with the single-device run of the whole problem."""
+
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import ExecutionConfig, ViewStorage, shard_program
+from conftest import assert_bits
+from test_shard_program_cpu import INDEXED, ROWWISE, _data, run_sharded
+
+pytestmark = pytest.mark.gpu
+_lock = threading.Lock()
+
+
+def locked_execute(program, fn_name, inputs, cfg=None):
+    with _lock:  # one context, one stream: a rank's launch sequence must not interleave with another's
+        return krn.execute(program, fn_name, inputs, cfg)
+
+
+def _whole(program, fn_name, data, policy):
+    call = {k: (ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+    value = krn.execute(program, fn_name, call, ExecutionConfig(policy=policy)).value
+    return value, {k: v.buffer for k, v in call.items() if isinstance(v, ViewStorage)}
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("n", [97, 5000, 300_001])
+@pytest.mark.parametrize("stem", ROWWISE)
+def test_rowwise_corpus_sharded_on_one_device(stem, n, world):
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    rng = np.random.default_rng(n + world)
+    data = _data(fn, n, rng)
+    wrt = tuple(p.name for p in fn.params if p.is_view)
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    gdata = dict(data)
+    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+        gdata[sp.name] = rng.normal(size=np.shape(data[w]))
+    exact = stem != "mean_shift"  # there a gathered scalar is written back into the Views
+    for program, name, d in ((prog, fn.name, data), (gp, gfn.name, gdata)):
+        wv, want = _whole(program, name, d, "compiled")
+        values, whole = run_sharded(program, name, d, world, locked_execute)
+        for v in values:
+            if wv is None:
+                assert v is None
+            else:
+                assert v == values[0] and abs(v - wv) <= 1e-12 * abs(wv), (stem, v, wv)
+        for k, arr in whole.items():
+            if exact:
+                assert_bits(arr, want[k], f"{name} n={n} world={world} {k}")
+            else:
+                assert np.all(np.abs(arr - want[k]) <= 1e-12 * np.abs(want[k])), (name, k)
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_localised_guards_on_the_device(world):
+    prog = krn.parse(INDEXED)
+    rng = np.random.default_rng(world)
+    n = 10_007
+    data = {"a": rng.normal(size=n), "b": rng.normal(size=n), "c": 0.75}
+    wv, want = _whole(prog, "f", data, "compiled")
+    values, whole = run_sharded(prog, "f", data, world, locked_execute)
+    assert all(v == values[0] for v in values) and abs(values[0] - wv) <= 1e-12 * abs(wv)
+    assert_bits(whole["a"], want["a"], "a (independent of the gathered scalars)")
+    assert np.all(np.abs(whole["b"] - want["b"]) <= 1e-12 * np.abs(want["b"]))
+
+
+def _gloo_worker(rank, world, port, n, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_13204_b200.sharded import partition
+
+        prog = krn.load_program("mean_shift")
+        v = np.random.default_rng(11).uniform(0.5, 1.5, size=n)
+        lo, ln = partition(n, world)[rank]
+        sp = shard_program.ShardedProgram(prog, "shiftedEnergy", n, lo)  # default comm: torch.distributed
+        local = {"v": v[lo:lo + ln].copy()}
+        value = sp.run(local)
+        out.put((rank, value, local["v"].buffer.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_over_gloo():
+    import torch.multiprocessing as mp
+
+    n, world = 20_001, 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = 29300 + os.getpid() % 400
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(out.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    prog = krn.load_program("mean_shift")
+    v = np.random.default_rng(11).uniform(0.5, 1.5, size=n)
+    wv, want = _whole(prog, "shiftedEnergy", {"v": v}, "compiled")
+    assert got[0][1] == got[1][1] and abs(got[0][1] - wv) <= 1e-12 * abs(wv)
+    assert_bits(np.concatenate([got[0][2], got[1][2]]), want["v"], "v")

@@ -1,0 +1,182 @@
+"""CPU tier: sharded execution of row-wise functions (shard_program.py).  The transform under
+test - segmentation at the gathers, localisation of guards / float(i) / extents, host scalars,
+the all-reduce protocol - runs here with the oracle interpreter standing in for the GPU
+`execute` and one thread per rank (a barrier-based all-reduce), against the whole-problem oracle."""
+
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2507_13204_b200 as krn
+from paper_2507_13204_b200 import shard_program
+from paper_2507_13204_b200.sharded import partition
+from conftest import assert_bits
+
+ROWWISE = ["affine_weighted", "copy_chain", "fill_scale", "inplace_axpy", "mean_shift", "rowscale_rank2",
+           "safe_divide", "sum_squares"]
+INDEXED = """fn f(a: view<f64, 1>, b: view<f64, 1>, c: f64) -> f64 {
+    let t: view<f64, 1> = view("t", extent(a, 0));
+    let w: f64 = c * 2.0 + extent(a, 0);
+    parallel_for i in 0..extent(a, 0) {
+        t(i) = a(i) * i + w;
+        if (i != 0) { t(i) += b(i); }
+        if (i >= 5) { a(i) = a(i) - c; }
+        if (i != extent(a, 0) - 1) { b(i) = b(i) * 0.5 + extent(a, 0); }
+    }
+    s = parallel_sum(t);
+    deep_copy(t, s);
+    parallel_for i in 0..extent(a, 0) { b(i) += t(i) * 1.0e-3; }
+    s2 = parallel_sum(b);
+    return s * 0.5 + s2 - extent(a, 0);
+}"""
+
+
+class ThreadComm:
+    """all-reduce among `world` threads: every rank deposits its value, all sum in rank order."""
+
+    def __init__(self, world):
+        self.world, self.slots, self.barrier = world, [0.0] * world, threading.Barrier(world)
+
+    def view(self, rank):
+        comm = self
+
+        class _C:
+            def allreduce_sum(self, value):
+                comm.slots[rank] = value
+                comm.barrier.wait()
+                total = 0.0
+                for v in comm.slots:
+                    total = total + v
+                comm.barrier.wait()
+                return total
+
+        return _C()
+
+
+def oracle_execute(program, fn_name, inputs, cfg=None):
+    """stand-in for runtime.execute on the CPU: the oracle interpreter on the Views' host arrays"""
+    from oracle import interp
+
+    arrays = {k: (v.buffer if isinstance(v, krn.ViewStorage) else v) for k, v in inputs.items()}
+    return krn.ExecResult(interp.run(program, fn_name, arrays))
+
+
+def run_sharded(program, fn_name, data, world, execute):
+    """data: whole-problem arrays/scalars.  Returns (values per rank, whole arrays reassembled)."""
+    fn = program.function(fn_name)
+    n = next(np.shape(data[p.name])[0] for p in fn.params if p.is_view)
+    parts = partition(n, world)
+    comm = ThreadComm(world)
+    results, pieces, errors = [None] * world, [None] * world, []
+
+    def work(r):
+        try:
+            lo, ln = parts[r]
+            local = {k: (np.array(v[lo:lo + ln]) if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+            sp = shard_program.ShardedProgram(program, fn_name, n, lo, comm.view(r))
+            results[r] = sp.run(local)
+            pieces[r] = {k: (v.buffer if isinstance(v, krn.ViewStorage) else v) for k, v in local.items()}
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+            comm.barrier.abort()
+
+    old = shard_program.__dict__.get("_execute_override")
+    shard_program._execute_override = execute
+    try:
+        threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+    finally:
+        shard_program._execute_override = old
+    if errors:
+        raise errors[0]
+    whole = {k: np.concatenate([p[k] for p in pieces]) for k, v in data.items() if isinstance(v, np.ndarray)}
+    return results, whole
+
+
+def _data(fn, n, rng):
+    out = {}
+    for p in fn.params:
+        if not p.is_view:
+            out[p.name] = 0.75
+        elif p.type.rank == 2:
+            out[p.name] = rng.uniform(0.5, 1.5, size=(n, 3))
+        else:
+            out[p.name] = rng.uniform(0.5, 1.5, size=n)
+    return out
+
+
+def _check(program, fn_name, data, world, exact_views):
+    from oracle import interp
+
+    want = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+    wv = interp.run(program, fn_name, want)
+    values, whole = run_sharded(program, fn_name, data, world, oracle_execute)
+    for v in values:
+        if wv is None:
+            assert v is None
+        else:
+            assert v == values[0] and abs(v - wv) <= 1e-12 * abs(wv), (v, wv)
+    for k, arr in whole.items():
+        if exact_views:
+            assert_bits(arr, want[k], f"{fn_name} world={world} {k}")
+        else:
+            assert np.all(np.abs(arr - want[k]) <= 1e-12 * np.abs(want[k])), (fn_name, k)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("stem", ROWWISE)
+def test_rowwise_corpus_programs_and_gradients(stem, world):
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    rng = np.random.default_rng(len(stem) + world)
+    n = 41
+    data = _data(fn, n, rng)
+    feeds_views = stem == "mean_shift"  # a gathered scalar is written back into Views there
+    _check(prog, fn.name, data, world, exact_views=not feeds_views)
+    wrt = tuple(p.name for p in fn.params if p.is_view)
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    gdata = dict(data)
+    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+        gdata[sp.name] = rng.normal(size=np.shape(data[w]))
+    _check(gp, gfn.name, gdata, world, exact_views=not feeds_views)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_guards_float_i_and_extents_are_localised(world):
+    prog = krn.parse(INDEXED)
+    rng = np.random.default_rng(world)
+    data = {"a": rng.normal(size=23), "b": rng.normal(size=23), "c": 0.75}
+    _check(prog, "f", data, world, exact_views=False)
+    # the first kernel's Views do not depend on a gathered scalar: compare those exactly
+    from oracle import interp
+
+    want = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+    interp.run(prog, "f", want)
+    _, whole = run_sharded(prog, "f", data, world, oracle_execute)
+    assert_bits(whole["a"], want["a"], "a")
+
+
+def test_segments_are_plain_functions_of_the_language():
+    prog = krn.load_program("mean_shift")
+    sp = shard_program.ShardedProgram(prog, "shiftedEnergy", 100, 25, comm=ThreadComm(1).view(0))
+    kinds = [s.what for s in sp.steps]
+    assert kinds == ["host", "decl", "segment", "segment", "return"]
+    seg = [s for s in sp.steps if s.what == "segment"]
+    assert seg[0].gather == ("total", True) and seg[1].scalars == ("total",)
+    from paper_2507_13204_b200.lang.nodes import Program
+
+    for s in seg:
+        assert krn.validate(Program((s.fn,))) == []
+        krn.parse(krn.emit(Program((s.fn,))).replace("__part", "part_"))  # prints and parses back
+
+
+@pytest.mark.parametrize("stem", ["laplacian", "stencil_smooth", "gather_indirect"])
+def test_neighbour_and_indirect_programs_are_refused(stem):
+    prog = krn.load_program(stem)
+    with pytest.raises(shard_program.NotShardable):
+        shard_program.ShardedProgram(prog, prog.functions[0].name, 100, 0, comm=ThreadComm(1).view(0))
