@@ -20,8 +20,15 @@ View (rank-2: whole rows); nothing but scalars ever crosses a rank:
 
 Views come out bit-identical to a single-device run wherever they do not depend on a gathered
 scalar; a gathered scalar is the sum of the ranks' partial trees, i.e. exact up to
-reassociation (the 1e-12 relative tolerance of BASELINE.json).  Functions with neighbour reads
-or indirect indices are refused (``NotShardable``) - their halos / all-to-all are future work.
+reassociation (the 1e-12 relative tolerance of BASELINE.json).
+
+Views reached through another row (``x(idx(i))``, ``q(idx(i), 2)``) are *replicated*: every rank
+holds all of them.  They may be read freely; written only by ``atomic_add`` (the generated adjoint
+of an indirect read): every rank then accumulates its own contributions (rank 0 on top of the
+caller's values, the others on zeros) and the copies are all-reduced once at the end - the one
+bandwidth-carrying collective of this module (N doubles), as SURVEY.md section 8e prescribes.
+Functions with neighbour reads are refused (``NotShardable``): their halos are future work (the
+headline stencil has its own sharded kernels).
 """
 
 from __future__ import annotations
@@ -46,24 +53,55 @@ _execute_override = None  # tests only: a stand-in for runtime.execute (see test
 # analysis
 
 
-def check_shardable(fn) -> None:
-    """Raises NotShardable unless every kernel touches Views at the running row only."""
+def classify(fn) -> tuple:
+    """(replicated Views, replicated Views that are scatter targets); raises NotShardable.
+
+    A View accessed at the running row is *sharded* (a rank holds its own rows).  A View reached
+    through another row - `x(idx(i))`, `q(idx(i), 2)`, `v(0)` - is *replicated*: every rank holds
+    all of it.  Replicated Views may be read freely; they may be written only by `atomic_add`
+    (the generated adjoint of an indirect read), and then every rank accumulates its own
+    contributions and the copies are summed across ranks at the end (SURVEY.md section 8e:
+    "replicate _d_x per GPU and allreduce it")."""
+    row_use, other_use, scattered, plainly_written = set(), set(), set(), set()
+    trip_views = set()
     for s in fn.body:
         k = kind(s)
         if k == "ParallelFor":
             if not (kind(s.upper) == "Extent" and s.upper.dim == 0):
                 raise NotShardable(f"kernel range is not extent(view, 0): {kind(s.upper)}")
+            trip_views.add(s.upper.view)
+
+            def note(acc, write, atomic, counter=s.counter):
+                row = acc.indices[0]
+                if kind(row) == "Counter" and row.name == counter:
+                    row_use.add(acc.view)
+                elif any(kind(m) == "Counter" for m in walk_expr(row)) and not any(
+                        kind(m) == "ViewAccess" for m in walk_expr(row)):
+                    raise NotShardable(f"view '{acc.view}' is read at a neighbouring row (needs halos)")
+                else:
+                    other_use.add(acc.view)
+                    if write:
+                        (scattered if atomic else plainly_written).add(acc.view)
+                for other in acc.indices[1:]:
+                    if any(kind(m) in ("Counter", "ViewAccess") for m in walk_expr(other)):
+                        raise NotShardable(f"view '{acc.view}': column index depends on the row")
+                for i in acc.indices:  # accesses inside index positions: idx(i)
+                    for m in walk_expr(i):
+                        if kind(m) == "ViewAccess":
+                            note(m, False, False)
+
             for inner in walk_statements(s.body):
-                # (an atomic_add whose target is the running row stays inside the rank like any write)
+                kk = kind(inner)
+                if kk in ("AssignView", "AtomicAdd"):
+                    note(inner.target, True, kk == "AtomicAdd")
+                    if kk == "AssignView" and inner.op != "=":
+                        pass  # the read of the target is the same access
                 for e in N.statement_exprs(inner):
+                    if kk in ("AssignView", "AtomicAdd") and e is inner.target:
+                        continue
                     for n in walk_expr(e):
-                        if kind(n) == "ViewAccess":
-                            row = n.indices[0]
-                            if not (kind(row) == "Counter" and row.name == s.counter):
-                                raise NotShardable(f"view '{n.view}' is not accessed at the running row")
-                            for other in n.indices[1:]:
-                                if any(kind(m) in ("Counter", "ViewAccess") for m in walk_expr(other)):
-                                    raise NotShardable(f"view '{n.view}': column index depends on the row")
+                        if kind(n) == "ViewAccess" and not _inside_index(e, n):
+                            note(n, False, False)
         elif k == "DeclView":
             if not s.dyn_args or not (kind(s.dyn_args[0]) == "Extent" and s.dyn_args[0].dim == 0):
                 raise NotShardable(f"local view '{s.name}' is not declared with extent(view, 0) rows")
@@ -73,16 +111,52 @@ def check_shardable(fn) -> None:
                 raise NotShardable("function-scope scalar reads a view element")
         elif k in ("If", "AtomicAdd", "AssignView"):
             raise NotShardable(f"function-scope {k} is not supported")
+    both = row_use & other_use
+    if both:
+        raise NotShardable(f"views accessed both at the running row and elsewhere: {sorted(both)}")
+    if plainly_written:
+        raise NotShardable(f"replicated views written without atomic_add: {sorted(plainly_written)}")
+    replicated = set(other_use)
+    if trip_views & replicated:
+        raise NotShardable("a kernel ranges over a replicated view")
+    for s in fn.body:  # bulk statements and declarations must not involve replicated Views
+        k = kind(s)
+        names = set()
+        if k in ("DeepCopy", "ParallelSumInto"):
+            names = {s.dst} | ({s.src} if isinstance(s.src, str) else set())
+        elif k == "ParallelSum":
+            names = {s.src}
+        elif k == "DeclView":
+            names = {s.name} | {n.view for a in s.dyn_args for n in walk_expr(a) if kind(n) == "Extent"}
+        if names & replicated:
+            raise NotShardable(f"bulk statement / declaration on a replicated view: {sorted(names & replicated)}")
+    return frozenset(replicated), frozenset(scattered)
 
 
-def localize(stmt, lo: int, n_global: int):
-    """The statement as rank `lo`'s rows see it: guards and float(i) use the global row."""
+def _inside_index(root, node) -> bool:
+    """True when `node` occurs inside the index positions of an access of `root` (those are
+    visited through their owner)."""
+    for n in walk_expr(root):
+        if kind(n) == "ViewAccess" and n is not node:
+            for i in n.indices:
+                if any(m is node for m in walk_expr(i)):
+                    return True
+    return False
+
+
+def check_shardable(fn) -> None:
+    classify(fn)
+
+
+def localize(stmt, lo: int, n_global: int, replicated=frozenset()):
+    """The statement as rank `lo`'s rows see it: guards and float(i) use the global row; the
+    extent of a sharded View is the global row count (a replicated View is whole already)."""
 
     def in_condition(e):
         def f(n):
             if kind(n) == "Counter":
                 return N.IdxBinary("+", n, N.IntLiteral(lo)) if lo else None
-            if kind(n) == "Extent" and n.dim == 0:
+            if kind(n) == "Extent" and n.dim == 0 and n.view not in replicated:
                 return N.IntLiteral(n_global)
             return None
 
@@ -92,7 +166,7 @@ def localize(stmt, lo: int, n_global: int):
         def f(n):
             if kind(n) == "IndexVar":
                 return N.Binary("+", n, N.Literal(float(lo))) if lo else None
-            if kind(n) == "Extent" and n.dim == 0:
+            if kind(n) == "Extent" and n.dim == 0 and n.view not in replicated:
                 return N.Literal(float(n_global))
             return None
 
@@ -245,6 +319,20 @@ class TorchComm:
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def allreduce_array(self, arr: np.ndarray) -> None:
+        """In-place sum of a replicated View's copies (host array; NCCL: staged through the device)."""
+        if self.world == 1:
+            return
+        import torch
+
+        if self.dist.get_backend(self.group) == "nccl":
+            t = torch.from_numpy(arr).cuda()
+            self.dist.all_reduce(t, group=self.group)
+            arr[...] = t.cpu().numpy()
+        else:
+            t = torch.from_numpy(arr)
+            self.dist.all_reduce(t, group=self.group)
+
 
 class ShardedProgram:
     """One rank's executor of `fn_name` over rows [lo, lo + local rows) of a problem of
@@ -261,12 +349,13 @@ class ShardedProgram:
         for s in walk_statements(fn.body):
             if kind(s) == "DeclView":
                 self.ranks[s.name] = s.descriptor.rank
+        self.replicated, self.scattered = classify(fn)
         self.steps = plan_steps(fn, self.ranks)
         # localised segment programs (one Program per segment: `execute` caches its plan per function)
         self.programs = {}
         for st in self.steps:
             if st.what == "segment":
-                body = tuple(localize(s, self.lo, self.n_global) for s in st.fn.body)
+                body = tuple(localize(s, self.lo, self.n_global, self.replicated) for s in st.fn.body)
                 st.fn = N.FunctionDef(st.fn.name, st.fn.params, body, st.fn.returns)
                 self.programs[st.fn.name] = N.Program((st.fn,))
 
@@ -288,9 +377,16 @@ class ShardedProgram:
             else:
                 H[p.name] = np.float64(v)
 
+        # scatter targets are replicated: rank 0 keeps the caller's values, the others start from zero,
+        # every rank adds its own contributions, the copies are summed at the end
+        for name in self.scattered:
+            if self.lo > 0:
+                views[name].buffer[...] = 0.0
+
         class _Global:  # host_eval asks Views for extents: rows are the GLOBAL count
             def __init__(self, v, n):
                 self.extents = (n,) + tuple(v.extents[1:])
+
 
         value = None
         for st in self.steps:
@@ -302,7 +398,7 @@ class ShardedProgram:
                 views[s.name] = ViewStorage.zeros(s.name, dims)
             elif st.what == "host":
                 s = st.stmt
-                g = {k: _Global(v, self.n_global) for k, v in views.items()}
+                g = {k: (v if k in self.replicated else _Global(v, self.n_global)) for k, v in views.items()}
                 rhs = host_eval(s.init if kind(s) == "DeclScalar" else s.rhs, H, g)
                 if kind(s) == "DeclScalar" or s.op == "=":
                     H[s.name] = rhs
@@ -318,6 +414,8 @@ class ShardedProgram:
                     # reference: scalars[dst] = scalars.get(dst, 0.0) + total (runtime.py:649-651)
                     H[dst] = (H[dst] if accumulate else np.float64(0.0)) + total
             elif st.what == "return":
-                g = {k: _Global(v, self.n_global) for k, v in views.items()}
+                g = {k: (v if k in self.replicated else _Global(v, self.n_global)) for k, v in views.items()}
                 value = float(host_eval(st.stmt.value, H, g))
+        for name in sorted(self.scattered):
+            self.comm.allreduce_array(views[name].buffer)
         return value

@@ -110,3 +110,35 @@ def test_two_processes_over_gloo():
     wv, want = _whole(prog, "shiftedEnergy", {"v": v}, "compiled")
     assert got[0][1] == got[1][1] and abs(got[0][1] - wv) <= 1e-12 * abs(wv)
     assert_bits(np.concatenate([got[0][2], got[1][2]]), want["v"], "v")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("stem", ["gather_indirect", "gather_rows_rank2"])
+def test_replicated_views_and_their_scattered_shadows(stem, world):
+    """indirectly indexed Views are replicated; the generated adjoint scatters into a replicated
+    shadow on every rank (hardware atomics) and the copies are all-reduced at the end"""
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    n, rows = 40_003, 6_001
+    rng = np.random.default_rng(world)
+    data = {}
+    for p in fn.params:
+        if p.name == "idx":
+            data[p.name] = rng.integers(0, rows, size=n).astype(np.float64)
+        elif p.name in ("x", "q"):
+            data[p.name] = rng.normal(size=(rows, 3) if p.type.rank == 2 else rows)
+        else:
+            data[p.name] = rng.normal(size=n)
+    wv, want = _whole(prog, fn.name, data, "compiled")
+    values, whole = run_sharded(prog, fn.name, data, world, locked_execute)
+    assert all(v == values[0] for v in values) and abs(values[0] - wv) <= 1e-12 * abs(wv)
+    wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    gdata = dict(data)
+    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+        gdata[sp.name] = rng.normal(size=np.shape(data[w]))
+    _, want = _whole(gp, gfn.name, gdata, "statements")
+    _, whole = run_sharded(gp, gfn.name, gdata, world, locked_execute)
+    for k, arr in whole.items():
+        assert np.all(np.abs(arr - want[k]) <= 1e-12 * np.maximum(np.abs(want[k]), 1.0)), (stem, k)

@@ -51,6 +51,15 @@ class ThreadComm:
                 comm.barrier.wait()
                 return total
 
+            def allreduce_array(self, arr):
+                comm.slots[rank] = arr.copy()
+                comm.barrier.wait()
+                total = comm.slots[0].copy()
+                for v in comm.slots[1:]:
+                    total = total + v
+                comm.barrier.wait()
+                arr[...] = total
+
         return _C()
 
 
@@ -65,7 +74,8 @@ def oracle_execute(program, fn_name, inputs, cfg=None):
 def run_sharded(program, fn_name, data, world, execute):
     """data: whole-problem arrays/scalars.  Returns (values per rank, whole arrays reassembled)."""
     fn = program.function(fn_name)
-    n = next(np.shape(data[p.name])[0] for p in fn.params if p.is_view)
+    rep, _ = shard_program.classify(fn)
+    n = next(np.shape(data[p.name])[0] for p in fn.params if p.is_view and p.name not in rep)
     parts = partition(n, world)
     comm = ThreadComm(world)
     results, pieces, errors = [None] * world, [None] * world, []
@@ -73,7 +83,9 @@ def run_sharded(program, fn_name, data, world, execute):
     def work(r):
         try:
             lo, ln = parts[r]
-            local = {k: (np.array(v[lo:lo + ln]) if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+            replicated, _ = shard_program.classify(fn)
+            local = {k: ((np.array(v) if k in replicated else np.array(v[lo:lo + ln])) if isinstance(v, np.ndarray)
+                         else v) for k, v in data.items()}
             sp = shard_program.ShardedProgram(program, fn_name, n, lo, comm.view(r))
             results[r] = sp.run(local)
             pieces[r] = {k: (v.buffer if isinstance(v, krn.ViewStorage) else v) for k, v in local.items()}
@@ -93,7 +105,16 @@ def run_sharded(program, fn_name, data, world, execute):
         shard_program._execute_override = old
     if errors:
         raise errors[0]
-    whole = {k: np.concatenate([p[k] for p in pieces]) for k, v in data.items() if isinstance(v, np.ndarray)}
+    replicated, _ = shard_program.classify(fn)
+    whole = {}
+    for k, v in data.items():
+        if isinstance(v, np.ndarray):
+            if k in replicated:
+                for p in pieces[1:]:
+                    assert np.array_equal(p[k], pieces[0][k]), f"replicated view {k} differs between ranks"
+                whole[k] = pieces[0][k]
+            else:
+                whole[k] = np.concatenate([p[k] for p in pieces])
     return results, whole
 
 
@@ -175,8 +196,44 @@ def test_segments_are_plain_functions_of_the_language():
         krn.parse(krn.emit(Program((s.fn,))).replace("__part", "part_"))  # prints and parses back
 
 
-@pytest.mark.parametrize("stem", ["laplacian", "stencil_smooth", "gather_indirect"])
-def test_neighbour_and_indirect_programs_are_refused(stem):
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("stem", ["gather_indirect", "gather_rows_rank2"])
+def test_indirectly_indexed_views_are_replicated(stem, world):
+    """x(idx(i)) / q(idx(i), c): the indexed View is replicated, its shadow accumulates per rank and
+    is all-reduced at the end"""
+    from oracle import interp
+
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    n, rows = 53, 17
+    rng = np.random.default_rng(world)
+    data = {}
+    for p in fn.params:
+        if p.name == "idx":
+            data[p.name] = rng.integers(0, rows, size=n).astype(np.float64)
+        elif p.name in ("x", "q"):
+            data[p.name] = rng.normal(size=(rows, 3) if p.type.rank == 2 else rows)
+        else:
+            data[p.name] = rng.normal(size=n)
+    assert shard_program.classify(fn)[0] == {"x"} or shard_program.classify(fn)[0] == {"q"}
+    _check(prog, fn.name, data, world, exact_views=True)
+    wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    gdata = dict(data)
+    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+        gdata[sp.name] = rng.normal(size=np.shape(data[w]))
+    rep, scat = shard_program.classify(gfn)
+    assert scat == {"_d_" + next(iter(shard_program.classify(fn)[0]))}
+    want = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in gdata.items()}
+    interp.run(gp, gfn.name, want)
+    _, whole = run_sharded(gp, gfn.name, gdata, world, oracle_execute)
+    for k, arr in whole.items():
+        assert np.all(np.abs(arr - want[k]) <= 1e-12 * np.maximum(np.abs(want[k]), 1.0)), (stem, k)
+
+
+@pytest.mark.parametrize("stem", ["laplacian", "stencil_smooth"])
+def test_neighbour_programs_are_refused(stem):
     prog = krn.load_program(stem)
     with pytest.raises(shard_program.NotShardable):
         shard_program.ShardedProgram(prog, prog.functions[0].name, 100, 0, comm=ThreadComm(1).view(0))
