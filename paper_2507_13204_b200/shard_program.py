@@ -1,11 +1,9 @@
-"""Sharded execution of ANY row-wise function over several GPUs (SURVEY.md section 8e:
-"everything else in the corpus is elementwise -> partition only").
+"""Sharded execution of ANY function of the language over several GPUs.
 
-The headline objective has its own sharded kernels (sharded.py: halo rows, bit-identical
-reduction).  This module covers the rest: functions whose kernels touch every View only at
-the running row - all of the reference's corpus except the two stencils and the indirect
-gather, and their generated gradients.  One process per GPU owns the rows [lo, hi) of every
-View (rank-2: whole rows); nothing but scalars ever crosses a rank:
+The headline objective has its own sharded kernels (sharded.py: six halo values, bit-identical
+reduction, everything resident on the device).  This module is the general mechanism: one process
+per GPU owns the rows [lo, hi) of every View (rank-2: whole rows) and runs the SAME generated
+kernels as a single device would, on programs derived from the tree:
 
 * the function is cut into *segments* at its ``s = parallel_sum(v)`` statements.  A segment
   is an ordinary function of the same language (built here, executed by ``execute`` under any
@@ -16,19 +14,28 @@ View (rank-2: whole rows); nothing but scalars ever crosses a rank:
   are evaluated on the host, identically on every rank;
 * index-dependent code is *localised*: in guards and ``float(i)`` the counter becomes
   ``i + lo`` and ``extent(v, 0)`` the global row count, while memory accesses and trip counts
-  stay local.
+  stay local;
+* **neighbour accesses** (stencil reads ``v(i + c)``, writes / atomic adds to ``v(i + c)``) are
+  served by *ghost rows*, the rank-level twin of the window kernels' halo recompute: every rank
+  extends its Views by ``ghost`` rows of each neighbour (one all-gather of 2 x ghost rows per
+  View at the start), runs the whole function on the extended rows - re-running its neighbours'
+  edge iterations - and keeps its own rows.  ``ghost`` is the sum over the kernels of (farthest
+  neighbour read + farthest neighbour write); statements that would reach outside the rows held
+  are fenced off (their results lie in the discarded band); gathers sum a copy masked to the own
+  rows.  No adjoint crosses a rank and the order of every accumulation is the single-device one;
+* Views reached through **another row** (``x(idx(i))``, ``q(idx(i), 2)``) are *replicated*: every
+  rank holds all of them.  They may be read freely; written only by ``atomic_add`` (the generated
+  adjoint of an indirect read): every rank accumulates its own contributions (rank 0 on top of the
+  caller's values, the others on zeros) and the copies are all-reduced once at the end - the one
+  bandwidth-carrying collective (N doubles), as SURVEY.md section 8e prescribes.
 
 Views come out bit-identical to a single-device run wherever they do not depend on a gathered
-scalar; a gathered scalar is the sum of the ranks' partial trees, i.e. exact up to
-reassociation (the 1e-12 relative tolerance of BASELINE.json).
-
-Views reached through another row (``x(idx(i))``, ``q(idx(i), 2)``) are *replicated*: every rank
-holds all of them.  They may be read freely; written only by ``atomic_add`` (the generated adjoint
-of an indirect read): every rank then accumulates its own contributions (rank 0 on top of the
-caller's values, the others on zeros) and the copies are all-reduced once at the end - the one
-bandwidth-carrying collective of this module (N doubles), as SURVEY.md section 8e prescribes.
-Functions with neighbour reads are refused (``NotShardable``): their halos are future work (the
-headline stencil has its own sharded kernels).
+scalar or on the order of hardware atomics; a gathered scalar is the sum of the ranks' partial
+trees, i.e. exact up to reassociation (the 1e-12 relative tolerance of BASELINE.json).  All 11
+corpus programs and their gradients run this way.  Ghost rows and replicated shadows are staged
+through the host in this version (the generic path's point is coverage; the headline path keeps
+everything on the device).  Refused (``NotShardable``): non-unit strides, rank-2 Views at a
+neighbouring row, kernel-local scalars initialised from a neighbouring row.
 """
 
 from __future__ import annotations
@@ -53,8 +60,8 @@ _execute_override = None  # tests only: a stand-in for runtime.execute (see test
 # analysis
 
 
-def classify(fn) -> tuple:
-    """(replicated Views, replicated Views that are scatter targets); raises NotShardable.
+def classify(fn):
+    """Classification(replicated Views, scatter targets among them, ghost width); raises NotShardable.
 
     A View accessed at the running row is *sharded* (a rank holds its own rows).  A View reached
     through another row - `x(idx(i))`, `q(idx(i), 2)`, `v(0)` - is *replicated*: every rank holds
@@ -64,20 +71,34 @@ def classify(fn) -> tuple:
     "replicate _d_x per GPU and allreduce it")."""
     row_use, other_use, scattered, plainly_written = set(), set(), set(), set()
     trip_views = set()
+    ghost = 0
+    reach: dict = {}  # id(kernel) -> (lowest, highest) neighbour offset it touches
     for s in fn.body:
         k = kind(s)
         if k == "ParallelFor":
             if not (kind(s.upper) == "Extent" and s.upper.dim == 0):
                 raise NotShardable(f"kernel range is not extent(view, 0): {kind(s.upper)}")
             trip_views.add(s.upper.view)
+            rd, wr = [0, 0], [0, 0]
 
-            def note(acc, write, atomic, counter=s.counter):
+            def note(acc, write, atomic, counter=s.counter, rd=rd, wr=wr):
+                from .codegen import _unit_affine
+
                 row = acc.indices[0]
+                c = _unit_affine(row, counter)
                 if kind(row) == "Counter" and row.name == counter:
                     row_use.add(acc.view)
+                elif c is not None:
+                    # a neighbouring row: served by ghost rows - the rank re-runs its neighbours' edge
+                    # iterations, so a row it owns also receives what iteration k - c writes or adds to it
+                    if len(acc.indices) != 1:
+                        raise NotShardable(f"rank-2 view '{acc.view}' is accessed at a neighbouring row")
+                    row_use.add(acc.view)
+                    box = wr if write else rd
+                    box[0], box[1] = min(box[0], c), max(box[1], c)
                 elif any(kind(m) == "Counter" for m in walk_expr(row)) and not any(
                         kind(m) == "ViewAccess" for m in walk_expr(row)):
-                    raise NotShardable(f"view '{acc.view}' is read at a neighbouring row (needs halos)")
+                    raise NotShardable(f"view '{acc.view}' is accessed at a non-unit stride")
                 else:
                     other_use.add(acc.view)
                     if write:
@@ -92,6 +113,12 @@ def classify(fn) -> tuple:
 
             for inner in walk_statements(s.body):
                 kk = kind(inner)
+                if kk == "DeclScalar":
+                    from .codegen import _unit_affine as _ua
+
+                    for n in walk_expr(inner.init):
+                        if kind(n) == "ViewAccess" and _ua(n.indices[0], s.counter) not in (None, 0):
+                            raise NotShardable("a kernel-local scalar is initialised from a neighbouring row")
                 if kk in ("AssignView", "AtomicAdd"):
                     note(inner.target, True, kk == "AtomicAdd")
                     if kk == "AssignView" and inner.op != "=":
@@ -102,6 +129,10 @@ def classify(fn) -> tuple:
                     for n in walk_expr(e):
                         if kind(n) == "ViewAccess" and not _inside_index(e, n):
                             note(n, False, False)
+            # every kernel shrinks the band of ghost rows that still hold correct values by what it
+            # reads from its neighbours plus how far it scatters
+            ghost += max(-rd[0], rd[1]) + max(-wr[0], wr[1])
+            reach[id(s)] = (min(rd[0], wr[0]), max(rd[1], wr[1]))
         elif k == "DeclView":
             if not s.dyn_args or not (kind(s.dyn_args[0]) == "Extent" and s.dyn_args[0].dim == 0):
                 raise NotShardable(f"local view '{s.name}' is not declared with extent(view, 0) rows")
@@ -130,7 +161,35 @@ def classify(fn) -> tuple:
             names = {s.name} | {n.view for a in s.dyn_args for n in walk_expr(a) if kind(n) == "Extent"}
         if names & replicated:
             raise NotShardable(f"bulk statement / declaration on a replicated view: {sorted(names & replicated)}")
-    return frozenset(replicated), frozenset(scattered)
+    if ghost:
+        for s in fn.body:
+            if kind(s) == "ParallelSum" and _rank_of(fn, s.src) != 1:
+                raise NotShardable("gather over a rank-2 view in a function with neighbour reads")
+    return Classification(frozenset(replicated), frozenset(scattered), ghost, reach)
+
+
+def _rank_of(fn, view) -> int:
+    p = fn.param(view)
+    if p is not None:
+        return p.type.rank
+    for s in walk_statements(fn.body):
+        if kind(s) == "DeclView" and s.name == view:
+            return s.descriptor.rank
+    return 1
+
+
+@_dc.dataclass(frozen=True)
+class Classification:
+    replicated: frozenset   # Views every rank holds whole (reached through another row)
+    scattered: frozenset    # replicated Views written by atomic_add: summed across ranks at the end
+    ghost: int              # rows of its neighbours a rank keeps (and recomputes) on either side
+    reach: dict = _dc.field(default_factory=dict, compare=False)
+
+    def __iter__(self):     # (replicated, scattered) for callers that only need the sets
+        return iter((self.replicated, self.scattered))
+
+    def __getitem__(self, i):
+        return (self.replicated, self.scattered)[i]
 
 
 def _inside_index(root, node) -> bool:
@@ -222,6 +281,7 @@ class Step:
     views: tuple = ()         # segment: view parameter names
     scalars: tuple = ()       # segment: f64 parameter names
     gather: object = None     # segment: (dst scalar, accumulate?) when it ends with a gather
+    mask: object = None       # segment with ghost rows: (masked copy, gathered view) - see ShardedProgram._build
 
 
 def _names_in(stmts):
@@ -245,8 +305,10 @@ def _names_in(stmts):
     return views, scalars
 
 
-def plan_steps(fn, ranks: dict) -> list:
-    """Cut `fn` into host steps, local-view declarations and segments."""
+def plan_steps(fn, ranks: dict, ghost: int = 0) -> list:
+    """Cut `fn` into host steps, local-view declarations and segments.  With ghost rows a gather
+    must only count the rank's own rows: it sums a masked copy (`__own<k>`, zero on ghost rows; the
+    bounds GLO_ / GHI_ are filled in per rank by ShardedProgram)."""
     check_shardable(fn)
     steps: list = []
     pending: list = []
@@ -260,20 +322,31 @@ def plan_steps(fn, ranks: dict) -> list:
         pending.clear()
         gather = None
         returns = None
+        mask = None
         if gather_stmt is not None:
-            body.append(N.ParallelSum("__part", gather_stmt.src))
+            src = gather_stmt.src
+            mask = None
+            if ghost:
+                own = f"__own{counter[0]}"
+                ranks[own] = 1
+                steps.append(Step("decl", stmt=N.DeclView(N.ViewDescriptor(own, rank=1), (N.Extent(src, 0),), label=own)))
+                mask, src = (own, src), own
+            body.append(N.ParallelSum("__part", src))
             body.append(N.Return(N.ScalarVar("__part")))
             returns = "f64"
             gather = (gather_stmt.dst, gather_stmt.dst in bound)
             bound.add(gather_stmt.dst)
         views, scalars = _names_in(body)
+        if gather_stmt is not None and mask is not None:
+            views |= {mask[0], mask[1]}
         scalars.discard("__part")
         params = tuple(N.Param(v, N.ViewDescriptor(v, rank=ranks[v])) for v in sorted(views)) + \
             tuple(N.Param(s_, "f64") for s_ in sorted(scalars))
         name = f"{fn.name}__seg{counter[0]}"
         counter[0] += 1
         steps.append(Step("segment", fn=N.FunctionDef(name, params, tuple(body), returns),
-                          views=tuple(sorted(views)), scalars=tuple(sorted(scalars)), gather=gather))
+                          views=tuple(sorted(views)), scalars=tuple(sorted(scalars)), gather=gather,
+                          mask=mask if gather_stmt is not None else None))
 
     for s in fn.body:
         k = kind(s)
@@ -319,6 +392,21 @@ class TorchComm:
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def exchange_rows(self, first: np.ndarray, last: np.ndarray):
+        """(last rows of the rank below, first rows of the rank above); None at the ends."""
+        if self.world == 1:
+            return None, None
+        import torch
+
+        device = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        mine = torch.from_numpy(np.concatenate([first.reshape(-1), last.reshape(-1)])).to(device)
+        everyone = torch.empty(self.world * mine.numel(), dtype=mine.dtype, device=device)
+        self.dist.all_gather_into_tensor(everyone, mine, group=self.group)
+        everyone = everyone.cpu().numpy().reshape(self.world, 2, *first.shape)
+        below = everyone[self.rank - 1, 1] if self.rank > 0 else None
+        above = everyone[self.rank + 1, 0] if self.rank < self.world - 1 else None
+        return below, above
+
     def allreduce_array(self, arr: np.ndarray) -> None:
         """In-place sum of a replicated View's copies (host array; NCCL: staged through the device)."""
         if self.world == 1:
@@ -349,15 +437,69 @@ class ShardedProgram:
         for s in walk_statements(fn.body):
             if kind(s) == "DeclView":
                 self.ranks[s.name] = s.descriptor.rank
-        self.replicated, self.scattered = classify(fn)
-        self.steps = plan_steps(fn, self.ranks)
-        # localised segment programs (one Program per segment: `execute` caches its plan per function)
-        self.programs = {}
+        self.cls = classify(fn)
+        self.replicated, self.scattered, self.ghost = self.cls.replicated, self.cls.scattered, self.cls.ghost
+        self.steps = plan_steps(fn, self.ranks, self.ghost)
+        self._built: dict = {}  # (ghost rows below, own rows, ghost rows above) -> {segment name: Program}
+
+    def _build(self, glo: int, own: int, ghi: int) -> dict:
+        """The segment programs as this rank runs them: guards / float(i) / extents localised to the
+        first row it holds (lo - glo); with ghost rows, kernels skip the edge iterations whose
+        neighbours lie outside the rows held (their results are in the discarded band anyway) and
+        gathers sum a copy masked to the rank's own rows."""
+        key = (glo, own, ghi)
+        hit = self._built.get(key)
+        if hit is not None:
+            return hit
+        from .codegen import _unit_affine
+
+        def reach(stmt, counter):
+            lo_c = hi_c = 0
+            for e in N.statement_exprs(stmt):
+                for n in walk_expr(e):
+                    if kind(n) == "ViewAccess" and n.view not in self.replicated:
+                        c = _unit_affine(n.indices[0], counter)
+                        if c is not None:
+                            lo_c, hi_c = min(lo_c, c), max(hi_c, c)
+            return lo_c, hi_c
+
+        def fence(stmts, kernel):
+            """every statement that touches a neighbouring row runs only where that row is held"""
+            out_ = []
+            i = N.Counter(kernel.counter)
+            for x in stmts:
+                if kind(x) == "If":
+                    out_.append(N.If(x.cond, tuple(fence(x.body, kernel)), span=x.span))
+                    continue
+                cmin, cmax = reach(x, kernel.counter)
+                if ghi and cmax > 0:
+                    x = N.If(N.Compare("<", i, N.IdxBinary("-", kernel.upper, N.IntLiteral(cmax))), (x,))
+                if glo and cmin < 0:
+                    x = N.If(N.Compare(">=", i, N.IntLiteral(-cmin)), (x,))
+                out_.append(x)
+            return out_
+
+        out = {}
         for st in self.steps:
-            if st.what == "segment":
-                body = tuple(localize(s, self.lo, self.n_global, self.replicated) for s in st.fn.body)
-                st.fn = N.FunctionDef(st.fn.name, st.fn.params, body, st.fn.returns)
-                self.programs[st.fn.name] = N.Program((st.fn,))
+            if st.what != "segment":
+                continue
+            body = []
+            for s in st.fn.body:
+                s = localize(s, self.lo - glo, self.n_global, self.replicated)
+                if kind(s) == "ParallelFor" and self.ghost:
+                    s = N.ParallelFor(s.counter, s.upper, tuple(fence(s.body, s)), span=s.span)
+                if kind(s) == "ParallelSum" and st.mask is not None:
+                    own_view, src = st.mask
+                    i = N.Counter("__i")
+                    copy = N.AssignView(N.ViewAccess(own_view, (i,)), "=", N.ViewAccess(src, (i,)))
+                    body.append(N.ParallelFor("__i", N.Extent(src, 0), (
+                        N.If(N.Compare(">=", i, N.IntLiteral(glo)), (
+                            N.If(N.Compare("<", i, N.IntLiteral(glo + own)), (copy,)),)),)))
+                body.append(s)
+            fn = N.FunctionDef(st.fn.name, st.fn.params, tuple(body), st.fn.returns)
+            out[fn.name] = N.Program((fn,))
+        self._built[key] = out
+        return out
 
     def run(self, inputs: dict, cfg=None):
         from .compiled import host_eval
@@ -376,6 +518,26 @@ class ShardedProgram:
                 views[p.name] = v
             else:
                 H[p.name] = np.float64(v)
+
+        # ghost rows: every sharded parameter is extended by the neighbours' edge rows (one all-gather of
+        # 2 x ghost rows per View); the function then runs on the extended rows and the own rows are
+        # written back at the end
+        sharded = [p.name for p in self.fn.params if p.is_view and p.name not in self.replicated]
+        own = views[sharded[0]].extents[0] if sharded else 0
+        glo = ghi = 0
+        originals: dict = {}
+        if self.ghost and sharded:
+            G = self.ghost
+            if own < G:
+                raise NotShardable(f"a rank needs at least {G} rows of its own, got {own}")
+            for name in sharded:
+                host = views[name].buffer
+                below, above = self.comm.exchange_rows(host[:G].copy(), host[own - G:].copy())
+                parts = ([below] if below is not None else []) + [host] + ([above] if above is not None else [])
+                glo, ghi = (G if below is not None else 0), (G if above is not None else 0)
+                originals[name] = views[name]
+                views[name] = ViewStorage.from_values(name, np.concatenate(parts))
+        programs = self._build(glo, own, ghi)
 
         # scatter targets are replicated: rank 0 keeps the caller's values, the others start from zero,
         # every rank adds its own contributions, the copies are summed at the end
@@ -407,7 +569,7 @@ class ShardedProgram:
             elif st.what == "segment":
                 call = {v: views[v] for v in st.views}
                 call.update({s_: float(H[s_]) for s_ in st.scalars})
-                part = execute(self.programs[st.fn.name], st.fn.name, call, cfg).value
+                part = execute(programs[st.fn.name], st.fn.name, call, cfg).value
                 if st.gather is not None:
                     dst, accumulate = st.gather
                     total = np.float64(self.comm.allreduce_sum(float(part)))
@@ -416,6 +578,8 @@ class ShardedProgram:
             elif st.what == "return":
                 g = {k: (v if k in self.replicated else _Global(v, self.n_global)) for k, v in views.items()}
                 value = float(host_eval(st.stmt.value, H, g))
+        for name, original in originals.items():
+            original.buffer[...] = views[name].buffer[glo:glo + own]
         for name in sorted(self.scattered):
             self.comm.allreduce_array(views[name].buffer)
         return value

@@ -51,6 +51,14 @@ class ThreadComm:
                 comm.barrier.wait()
                 return total
 
+            def exchange_rows(self, first, last):
+                comm.slots[rank] = (first, last)
+                comm.barrier.wait()
+                below = comm.slots[rank - 1][1].copy() if rank > 0 else None
+                above = comm.slots[rank + 1][0].copy() if rank < comm.world - 1 else None
+                comm.barrier.wait()
+                return below, above
+
             def allreduce_array(self, arr):
                 comm.slots[rank] = arr.copy()
                 comm.barrier.wait()
@@ -232,8 +240,44 @@ def test_indirectly_indexed_views_are_replicated(stem, world):
         assert np.all(np.abs(arr - want[k]) <= 1e-12 * np.maximum(np.abs(want[k]), 1.0)), (stem, k)
 
 
-@pytest.mark.parametrize("stem", ["laplacian", "stencil_smooth"])
-def test_neighbour_programs_are_refused(stem):
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+@pytest.mark.parametrize("stem", ["laplacian", "stencil_smooth", "window_wide", "window_partial", "window_war",
+                                  "window_scatter"])
+def test_neighbour_reads_are_served_by_ghost_rows(stem, world):
+    """stencils, scatters to neighbouring rows, in-place updates read by neighbours: every rank keeps
+    `ghost` rows of its neighbours and recomputes their edge iterations; own rows must equal the
+    single-device result bit for bit (gathered scalars within 1e-12)"""
+    from oracle import interp
+
     prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    rng = np.random.default_rng(world + len(stem))
+    n = 61
+    data = _data(fn, n, rng)
+    assert shard_program.classify(fn).ghost >= 1
+    _check(prog, fn.name, data, world, exact_views=True)
+    wrt = tuple(p.name for p in fn.params if p.is_view)
+    try:
+        gp = krn.differentiate(prog, fn.name, wrt)
+    except (krn.NotFeasible, ValueError):
+        return
+    gfn = gp.functions[-1]
+    gdata = dict(data)
+    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+        gdata[sp.name] = rng.normal(size=np.shape(data[w]))
+    _check(gp, gfn.name, gdata, world, exact_views=True)
+
+
+def test_shards_smaller_than_the_ghost_band_are_refused():
+    prog = krn.load_program("laplacian")
+    gp = krn.differentiate(prog, "normRes1DLaplacianSQ", ("x", "b"))
+    data = {k: np.ones(3) for k in ("x", "b", "_d_x", "_d_b")}
+    with pytest.raises(shard_program.NotShardable, match="at least 2 rows"):
+        run_sharded(gp, "normRes1DLaplacianSQ_grad", data, 3, oracle_execute)
+
+
+def test_strided_accesses_are_refused():
+    prog = krn.parse("""fn f(a: view<f64, 1>, b: view<f64, 1>) { parallel_for i in 0..extent(b, 0) {
+                        b(i) = a(2 * i); } }""")
     with pytest.raises(shard_program.NotShardable):
-        shard_program.ShardedProgram(prog, prog.functions[0].name, 100, 0, comm=ThreadComm(1).view(0))
+        shard_program.ShardedProgram(prog, "f", 100, 0, comm=ThreadComm(1).view(0))
