@@ -175,3 +175,68 @@ def test_neighbour_reads_through_ghost_rows_on_the_device(stem, n, world):
                 assert v == values[0] and abs(v - wv) <= 1e-12 * abs(wv), (stem, v, wv)
         for k, arr in whole.items():
             assert_bits(arr, want[k], f"{name} n={n} world={world} {k}")
+
+
+def _gloo_worker_all(rank, world, port, n, out):
+    """the torch.distributed communicator on every collective it offers: scalar all-reduce
+    (laplacian primal), ghost-row exchange (laplacian gradient), array all-reduce (indirect gather)"""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_13204_b200.sharded import partition
+
+        rng = np.random.default_rng(21)
+        x, b, dx, db = (rng.normal(size=n) for _ in range(4))
+        idx = rng.integers(0, 500, size=n).astype(np.float64)
+        xs, dxs = rng.normal(size=500), rng.normal(size=500)
+        lo, ln = partition(n, world)[rank]
+        sl = slice(lo, lo + ln)
+        lap = krn.load_program("laplacian")
+        gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+        local = {"x": x[sl].copy(), "b": b[sl].copy()}
+        f = shard_program.ShardedProgram(lap, "normRes1DLaplacianSQ", n, lo).run(local)
+        g = {"x": x[sl].copy(), "b": b[sl].copy(), "_d_x": dx[sl].copy(), "_d_b": db[sl].copy()}
+        shard_program.ShardedProgram(gp, "normRes1DLaplacianSQ_grad", n, lo).run(g)
+        gi = krn.load_program("gather_indirect")
+        ggi = krn.differentiate(gi, "gatherSquares", ("x",))
+        h = {"x": xs.copy(), "idx": idx[sl].copy(), "_d_x": dxs.copy()}
+        shard_program.ShardedProgram(ggi, "gatherSquares_grad", n, lo).run(h)
+        out.put((rank, f, g["_d_x"].buffer.copy(), g["_d_b"].buffer.copy(), g["x"].buffer.copy(), h["_d_x"].buffer.copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_every_collective_over_gloo():
+    import torch.multiprocessing as mp
+
+    n, world = 30_011, 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = 29700 + os.getpid() % 250
+    procs = [ctx.Process(target=_gloo_worker_all, args=(r, world, port, n, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(out.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(21)
+    x, b, dx, db = (rng.normal(size=n) for _ in range(4))
+    idx = rng.integers(0, 500, size=n).astype(np.float64)
+    xs, dxs = rng.normal(size=500), rng.normal(size=500)
+    lap = krn.load_program("laplacian")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    wf, _ = _whole(lap, "normRes1DLaplacianSQ", {"x": x, "b": b}, "fused")
+    _, want = _whole(gp, "normRes1DLaplacianSQ_grad", {"x": x, "b": b, "_d_x": dx, "_d_b": db}, "fused")
+    assert got[0][1] == got[1][1] and abs(got[0][1] - wf) <= 1e-12 * abs(wf)
+    assert_bits(np.concatenate([got[0][2], got[1][2]]), want["_d_x"], "_d_x")
+    assert_bits(np.concatenate([got[0][3], got[1][3]]), want["_d_b"], "_d_b")
+    assert_bits(np.concatenate([got[0][4], got[1][4]]), want["x"], "x")
+    gi = krn.load_program("gather_indirect")
+    ggi = krn.differentiate(gi, "gatherSquares", ("x",))
+    _, wi = _whole(ggi, "gatherSquares_grad", {"x": xs, "idx": idx, "_d_x": dxs}, "statements")
+    for r in range(world):  # the replicated shadow is the same, complete, on every rank
+        assert np.all(np.abs(got[r][5] - wi["_d_x"]) <= 1e-12 * np.maximum(np.abs(wi["_d_x"]), 1.0))
+    assert np.array_equal(got[0][5], got[1][5])
