@@ -32,9 +32,9 @@ kernels as a single device would, on programs derived from the tree:
 Views come out bit-identical to a single-device run wherever they do not depend on a gathered
 scalar or on the order of hardware atomics; a gathered scalar is the sum of the ranks' partial
 trees, i.e. exact up to reassociation (the 1e-12 relative tolerance of BASELINE.json).  All 11
-corpus programs and their gradients run this way.  Ghost rows and replicated shadows are staged
-through the host in this version (the generic path's point is coverage; the headline path keeps
-everything on the device).  Refused (``NotShardable``): non-unit strides, rank-2 Views at a
+corpus programs and their gradients run this way.  Extended Views are assembled in HBM (own rows
+device to device; only the 2 x ghost edge rows and the gathered scalars touch the host); replicated
+shadows are all-reduced through the host in this version.  Refused (``NotShardable``): non-unit strides, rank-2 Views at a
 neighbouring row, kernel-local scalars initialised from a neighbouring row.
 """
 
@@ -372,6 +372,48 @@ def plan_steps(fn, ranks: dict, ghost: int = 0) -> list:
 # execution
 
 
+def _edge_rows(v, start: int, count: int) -> np.ndarray:
+    """`count` rows of a View from row `start`, fetched from wherever the View lives."""
+    from .runtime import Device
+
+    if v._dev_ok and not v._host_ok:
+        dev = v._dev.dev
+        cols = v.size // max(v.extents[0], 1)
+        out = np.empty((count,) + tuple(v.extents[1:]), dtype=np.float64)
+        dev.download(out, v._dev.ptr + 8 * start * cols)
+        return out
+    del Device
+    return np.array(v.peek()[start:start + count])
+
+
+def _extended_on_device(v, below, above):
+    """A new View = [ghost rows from below | v | ghost rows from above], assembled in HBM: the own
+    rows are copied device to device, only the few ghost rows travel from the host."""
+    from .runtime import Device, ViewStorage, _DeviceBuffer
+
+    dev = v._dev.dev if (v._dev is not None and v._dev_ok) else Device.get()
+    cols = v.size // max(v.extents[0], 1)
+    glo = 0 if below is None else below.shape[0]
+    ghi = 0 if above is None else above.shape[0]
+    rows = glo + v.extents[0] + ghi
+    ext = ViewStorage._blank(v.name, (rows,) + tuple(v.extents[1:]))
+    ext._dev = _DeviceBuffer(dev, 8 * rows * cols)
+    if glo:
+        dev.upload(ext._dev.ptr, np.ascontiguousarray(below))
+    dev.copy(ext._dev.ptr + 8 * glo * cols, v.device_ptr(dev, write=False), v.size)
+    if ghi:
+        dev.upload(ext._dev.ptr + 8 * (glo + v.extents[0]) * cols, np.ascontiguousarray(above))
+    ext._dev_ok, ext._host_ok, ext._zero = True, False, False
+    return ext
+
+
+def _copy_rows_on_device(dst, src, start: int, count: int) -> None:
+    """dst[:] = src[start : start + count] without leaving the device."""
+    dev = src._dev.dev
+    cols = dst.size // max(dst.extents[0], 1)
+    dev.copy(dst.device_ptr(dev, discard=True), src.device_ptr(dev, write=False) + 8 * start * cols, count * cols)
+
+
 class TorchComm:
     """all-reduce(SUM) of a few doubles over torch.distributed (NCCL: through a device tensor)."""
 
@@ -530,13 +572,17 @@ class ShardedProgram:
             G = self.ghost
             if own < G:
                 raise NotShardable(f"a rank needs at least {G} rows of its own, got {own}")
+            on_device = _execute_override is None
             for name in sharded:
-                host = views[name].buffer
-                below, above = self.comm.exchange_rows(host[:G].copy(), host[own - G:].copy())
-                parts = ([below] if below is not None else []) + [host] + ([above] if above is not None else [])
+                v = views[name]
+                first, last = (_edge_rows(v, 0, G), _edge_rows(v, own - G, G)) if on_device else \
+                    (v.buffer[:G].copy(), v.buffer[own - G:].copy())
+                below, above = self.comm.exchange_rows(first, last)
                 glo, ghi = (G if below is not None else 0), (G if above is not None else 0)
-                originals[name] = views[name]
-                views[name] = ViewStorage.from_values(name, np.concatenate(parts))
+                originals[name] = v
+                views[name] = _extended_on_device(v, below, above) if on_device else ViewStorage.from_values(
+                    name, np.concatenate(([below] if below is not None else []) + [v.buffer] +
+                                         ([above] if above is not None else [])))
         programs = self._build(glo, own, ghi)
 
         # scatter targets are replicated: rank 0 keeps the caller's values, the others start from zero,
@@ -579,7 +625,10 @@ class ShardedProgram:
                 g = {k: (v if k in self.replicated else _Global(v, self.n_global)) for k, v in views.items()}
                 value = float(host_eval(st.stmt.value, H, g))
         for name, original in originals.items():
-            original.buffer[...] = views[name].buffer[glo:glo + own]
+            if _execute_override is None:
+                _copy_rows_on_device(original, views[name], glo, own)
+            else:
+                original.buffer[...] = views[name].buffer[glo:glo + own]
         for name in sorted(self.scattered):
             self.comm.allreduce_array(views[name].buffer)
         return value
