@@ -374,15 +374,12 @@ def plan_steps(fn, ranks: dict, ghost: int = 0) -> list:
 
 def _edge_rows(v, start: int, count: int) -> np.ndarray:
     """`count` rows of a View from row `start`, fetched from wherever the View lives."""
-    from .runtime import Device
-
     if v._dev_ok and not v._host_ok:
         dev = v._dev.dev
         cols = v.size // max(v.extents[0], 1)
         out = np.empty((count,) + tuple(v.extents[1:]), dtype=np.float64)
         dev.download(out, v._dev.ptr + 8 * start * cols)
         return out
-    del Device
     return np.array(v.peek()[start:start + count])
 
 
@@ -594,7 +591,6 @@ class ShardedProgram:
         class _Global:  # host_eval asks Views for extents: rows are the GLOBAL count
             def __init__(self, v, n):
                 self.extents = (n,) + tuple(v.extents[1:])
-
 
         value = None
         for st in self.steps:
