@@ -33,8 +33,8 @@ Views come out bit-identical to a single-device run wherever they do not depend 
 scalar or on the order of hardware atomics; a gathered scalar is the sum of the ranks' partial
 trees, i.e. exact up to reassociation (the 1e-12 relative tolerance of BASELINE.json).  All 11
 corpus programs and their gradients run this way.  Extended Views are assembled in HBM (own rows
-device to device; only the 2 x ghost edge rows and the gathered scalars touch the host); replicated
-shadows are all-reduced through the host in this version.  Refused (``NotShardable``): non-unit strides, rank-2 Views at a
+device to device; only the 2 x ghost edge rows and the gathered scalars touch the host); under NCCL
+replicated shadows are all-reduced in place in HBM.  Refused (``NotShardable``): non-unit strides, rank-2 Views at a
 neighbouring row, kernel-local scalars initialised from a neighbouring row.
 """
 
@@ -447,7 +447,7 @@ class TorchComm:
         return below, above
 
     def allreduce_array(self, arr: np.ndarray) -> None:
-        """In-place sum of a replicated View's copies (host array; NCCL: staged through the device)."""
+        """In-place sum of a replicated View's copies, given as a host array (gloo)."""
         if self.world == 1:
             return
         import torch
@@ -459,6 +459,44 @@ class TorchComm:
         else:
             t = torch.from_numpy(arr)
             self.dist.all_reduce(t, group=self.group)
+
+    def allreduce_view(self, view) -> None:
+        """In-place sum of a replicated View's copies.  NCCL: directly on the View's HBM buffer (a
+        torch tensor aliasing it through __cuda_array_interface__) - N doubles over NVLink, nothing
+        through the host; gloo: through the host array."""
+        if self.world == 1:
+            return
+        if self.dist.get_backend(self.group) == "nccl":
+            import torch
+
+            dev = view._dev.dev if (view._dev is not None and view._dev_ok) else None
+            if dev is None:
+                from .runtime import Device
+
+                dev = Device.get()
+            t = device_tensor(view, dev)
+            dev.sync()  # the library's stream and torch's are different timelines
+            self.dist.all_reduce(t, group=self.group)
+            torch.cuda.synchronize()
+        else:
+            self.allreduce_array(view.buffer)
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ carrier for a device pointer."""
+
+    def __init__(self, ptr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def device_tensor(view, dev):
+    """A torch CUDA tensor that ALIASES the View's device buffer (no copy); the View's host copy is
+    marked stale because the tensor may be written through."""
+    import torch
+
+    ptr = view.device_ptr(dev, write=True)
+    return torch.as_tensor(_CudaArray(ptr, view.extents), device=torch.device("cuda", dev.ordinal))
 
 
 class ShardedProgram:
@@ -626,5 +664,8 @@ class ShardedProgram:
             else:
                 original.buffer[...] = views[name].buffer[glo:glo + own]
         for name in sorted(self.scattered):
-            self.comm.allreduce_array(views[name].buffer)
+            if hasattr(self.comm, "allreduce_view") and _execute_override is None:
+                self.comm.allreduce_view(views[name])
+            else:
+                self.comm.allreduce_array(views[name].buffer)
         return value

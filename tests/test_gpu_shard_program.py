@@ -240,3 +240,19 @@ def test_every_collective_over_gloo():
     for r in range(world):  # the replicated shadow is the same, complete, on every rank
         assert np.all(np.abs(got[r][5] - wi["_d_x"]) <= 1e-12 * np.maximum(np.abs(wi["_d_x"]), 1.0))
     assert np.array_equal(got[0][5], got[1][5])
+
+
+def test_device_tensor_aliases_the_view():
+    """the NCCL path all-reduces a replicated shadow in place: the torch tensor handed to NCCL must
+    alias the View's HBM buffer, not copy it"""
+    import torch
+
+    dev = krn.Device.get()
+    v = ViewStorage.from_values("v", np.arange(12.0).reshape(4, 3))
+    t = shard_program.device_tensor(v, dev)
+    assert t.shape == (4, 3) and t.dtype == torch.float64 and t.is_cuda
+    assert t.data_ptr() == v.device_ptr(dev, write=False)
+    dev.sync()
+    t.mul_(2.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(v.buffer, 2.0 * np.arange(12.0).reshape(4, 3))
