@@ -281,3 +281,62 @@ def test_strided_accesses_are_refused():
                         b(i) = a(2 * i); } }""")
     with pytest.raises(shard_program.NotShardable):
         shard_program.ShardedProgram(prog, "f", 100, 0, comm=ThreadComm(1).view(0))
+
+
+def test_random_programs_sharded_against_the_whole_problem():
+    """random programs (pointwise statements, stencils on inputs and on temporaries, in-place
+    updates, fills, copies, gathers feeding later statements, rank-2 rows, indirect reads) and their
+    gradients: sharded over 2 and 3 ranks with the oracle as executor, against the oracle on the
+    whole problem"""
+    import warnings
+
+    from hypothesis import HealthCheck, assume, given, settings, strategies as st
+
+    from oracle import interp
+    from test_gpu_random_programs import _inputs as fuzz_inputs, programs
+
+    ran = [0]
+
+    @settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck), database=None)
+    @given(programs(), st.sampled_from([2, 3]), st.integers(0, 10**6))
+    def run(prog, world, seed):
+        text, use_idx, use_c, use_m = prog
+        program = krn.parse(text)
+        n = 37
+        base = fuzz_inputs(n, use_idx, use_c, seed, use_m)
+        cases = [(program, "f", base)]
+        wrt = ("a", "b") + (("m",) if use_m else ())
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            try:
+                gp = krn.differentiate(program, "f", wrt, tape=True)
+                gfn = gp.functions[-1]
+                gdata = dict(base)
+                rng = np.random.default_rng(seed)
+                for sp in gfn.params[len(program.functions[0].params):]:
+                    gdata[sp.name] = rng.normal(size=np.shape(base[sp.name[3:]]))
+                cases.append((gp, gfn.name, gdata))
+            except krn.NotFeasible:
+                pass
+        for pr, name, data in cases:
+            try:
+                cls = shard_program.classify(pr.function(name))
+            except shard_program.NotShardable:
+                continue
+            if cls.ghost and n // world < cls.ghost:
+                continue
+            want = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in data.items()}
+            with np.errstate(all="ignore"):
+                wv = interp.run(pr, name, want)
+                values, whole = run_sharded(pr, name, data, world, oracle_execute)
+            if wv is not None:
+                assume(np.isfinite(wv))
+                assert all(v == values[0] for v in values)
+                assert abs(values[0] - wv) <= 1e-9 * max(1.0, abs(wv)), (text, values[0], wv)
+            for k, arr in whole.items():
+                scale = max(1.0, float(np.max(np.abs(want[k])))) if want[k].size else 1.0
+                assert np.all(np.abs(arr - want[k]) <= 1e-9 * scale) or not np.all(np.isfinite(want[k])), (text, name, k)
+            ran[0] += 1
+
+    run()
+    assert ran[0] >= 60
