@@ -51,3 +51,15 @@ def test_runtime_errors_exit_1(tmp_path, capsys):
     rc = main(["run", LAP, "--fn", "normRes1DLaplacianSQ", "--input", f"x={tmp_path / 'x.tensor'}",
                "--input", f"b={tmp_path / 'b.tensor'}"])
     assert rc == 1 and "outside extent" in capsys.readouterr().err
+
+
+def test_quickstart_example_runs():
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "examples", "quickstart.py"), "20000"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "passed = True" in out.stdout and "1 kernel launch(es)" in out.stdout and out.stdout.strip().endswith("done")
