@@ -418,7 +418,12 @@ class _CompiledRun:
                        atomic_choice(self.cfg, recipe["atomic_views"], self.views, self.b, n_launch,
                                      recipe.get("static_smem", 0)))
         extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
-        steps = 1 if n_launch <= (1 << 20) else 8  # must be a power of two (tree node per block)
+        # steps per warp (a power of two: a block is a node of the reduction tree).  Measured on B200 at
+        # 134 M rows (tools/corpus_bench.py): kernels that end in a fused reduction pay a block-level
+        # tree, a ticket and a partial per block and run best with 8 (4: -4%, 1: -50%); kernels without
+        # one run best with 2 (8: -2..4%, 1: -2..5%).  Small problems are latency bound: as many
+        # blocks as possible.
+        steps = 1 if n_launch <= (1 << 20) else (8 if g.gather is not None else 2)
         nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)
         if g.gather is not None:
             # the context's reduction workspace: no allocation inside the launch sequence

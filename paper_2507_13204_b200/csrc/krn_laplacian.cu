@@ -28,7 +28,7 @@
 //
 // Work decomposition: a block owns an aligned chunk of 1024*R rows, warp w the
 // aligned sub-chunk of 128*R rows, processed as R steps of 128 rows (4 per lane,
-// one LDG.E.256 per operand).  Neighbour values travel by warp shuffle; the two
+// one LDG.E.256 per operand); R = 1 for the gradient, 1 or 4 for the primal (steps_for).  Neighbour values travel by warp shuffle; the two
 // edge lanes fetch the ghost rows of the neighbouring warp themselves (L2 hits).
 // Interior steps need no guard at all; the (at most three) steps per shard that
 // touch row 0, row n-1, a shard boundary or the ragged tail take a scalar,
@@ -362,11 +362,18 @@ laplacian_kernel(Shard s, double *__restrict__ x_out, double *dx, double *db, do
     }
 }
 
-int steps_for(size_t n_global)
+int steps_for(size_t n_global, bool grad)
 {
-    // small problems are latency bound: spread them over as many blocks as possible;
-    // large ones amortise the per-block epilogue and keep the partial count low
-    return n_global <= (size_t(1) << 20) ? 1 : 8;
+    // Measured on B200 (tools/microbench.py, 125 M rows, device time):
+    //   steps per warp      1        2        4        8       16
+    //   gradient (56 B)  1.010    1.034    1.061    1.107    1.101 ms
+    //   primal           0.609    0.482    0.460    0.484    0.512 ms
+    // The gradient has no block epilogue, so the finest decomposition wins (most blocks in flight,
+    // the whole device sweeps memory front to back): 6.93 TB/s.  The primal pays a block-level tree,
+    // a ticket and a partial per block: 4 steps balance that against the sweep (6.52 TB/s); small
+    // problems are latency bound and spread over as many blocks as possible.
+    if (grad) return 1;
+    return n_global <= (size_t(1) << 20) ? 1 : 4;
 }
 
 template <bool GRAD, int STEPS>
@@ -417,7 +424,7 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
         if (!GRAD && !accumulate) KRN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), ctx->stream));
         return KRN_OK;
     }
-    const int steps = steps_for(n_global);
+    const int steps = steps_for(n_global, GRAD);
     const size_t chunk = size_t(kThreads) * 4 * steps;
     const size_t blocks = (n_local + chunk - 1) / chunk;
     KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
@@ -432,7 +439,7 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
     if (steps == 1)
         dispatch<GRAD, 1>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
     else
-        dispatch<GRAD, 8>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
+        dispatch<GRAD, 4>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
     KRN_LAUNCH_CHECK(ctx);
     return KRN_OK;
 }
@@ -441,7 +448,7 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
 
 extern "C" size_t krn_laplacian_partial_span(size_t n_global)
 {
-    return size_t(kThreads) * 4 * steps_for(n_global);
+    return size_t(kThreads) * 4 * steps_for(n_global, false);
 }
 
 extern "C" int krn_laplacian_primal(krn_ctx *ctx, const double *d_x_in, double *d_x_out,

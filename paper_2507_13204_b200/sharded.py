@@ -11,8 +11,8 @@ reference's.  Collectives, both latency bound:
 
 * one all_gather of 6 doubles per rank (the halo rows)
 * for the objective value (primal only; the gradient does not depend on it) one
-  all_gather of the per-block tree partials (one double per 1024 or 8192 rows;
-  122 KB per rank at 125 M rows), folded by every rank with the reference's tree:
+  all_gather of the per-block tree partials (one double per 1024 or 4096 rows;
+  244 KB per rank at 125 M rows), folded by every rank with the reference's tree:
   shard cuts are multiples of the partial span, so the partials of all ranks in
   rank order ARE the nodes of the single-device tree and the result is
   bit-identical to the single-device and to the reference's value for any number
