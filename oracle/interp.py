@@ -37,9 +37,17 @@ Semantics restated (reference file:line in brackets):
   [runtime.py:628-641]
 * ``check_finite`` traps non-finite views after each kernel / bulk statement
   and non-finite scalars at gather / return [runtime.py:669-676]
+* conflict detection (``detect``): each kernel is replayed sequentially in the order
+  ``random.Random(rng_seed + kernel_index).shuffle`` gives; every view read, plain write and
+  atomic_add is logged as (view, offset) -> iteration -> kinds; a location touched by two or
+  more distinct iterations with a plain write among its accesses is one record, records
+  sorted by (view, offset) within a kernel [runtime.py:198-227, 284-285, 418-419, 439-440,
+  574-585]; pinned by ``tests/golden/conflicts.json`` (oracle/make_golden_conflicts.py)
 """
 
 from __future__ import annotations
+
+import random
 
 import numpy as np
 
@@ -89,6 +97,14 @@ class Machine:
         self.iteration = -1
         self.seq = 0
         self.value = None
+        self.trace = None  # conflict detection: {(view, offset): {iteration: {kinds}}} of the running kernel
+        self.rng_seed = None  # not None: conflict detection on
+        self.kernel_index = 0
+        self.records: list = []
+
+    def touch(self, view, off, what):
+        if self.trace is not None:
+            self.trace.setdefault((view, off), {}).setdefault(self.iteration, set()).add(what)
 
     # ---- index sub-language (Python ints) -----------------------------------
 
@@ -125,6 +141,7 @@ class Machine:
 
     def load(self, acc):
         flat, off = self.offset(acc)
+        self.touch(acc.view, off, "read")
         return flat[off]
 
     # ---- value sub-language (numpy float64 scalars: IEEE, no exceptions) ----
@@ -181,6 +198,7 @@ class Machine:
         elif k == "AssignView":
             flat, off = self.offset(s.target)
             v = self.val(s.rhs)
+            self.touch(s.target.view, off, "write")
             if s.op == "=":
                 flat[off] = v
             elif s.op == "+=":
@@ -190,6 +208,7 @@ class Machine:
         elif k == "AtomicAdd":
             flat, off = self.offset(s.target)
             v = self.val(s.value)
+            self.touch(s.target.view, off, "atomic")
             if self.queue is None:
                 flat[off] += v
             else:
@@ -289,14 +308,25 @@ class Machine:
     def kernel(self, loop):
         n = int(self.index(loop.upper))
         self.queue = []
+        order = list(range(n))
+        if self.rng_seed is not None:
+            random.Random(self.rng_seed + self.kernel_index).shuffle(order)
+            self.trace = {}
         try:
-            for i in range(n):
+            for i in order:
                 self.local = {loop.counter: i}
                 self.iteration, self.seq = i, 0
                 for s in loop.body:
                     self.element(s, in_kernel=True)
         finally:
             queue, self.queue, self.local = self.queue, None, {}
+            log, self.trace = self.trace, None
+        if log is not None:
+            for (view, off), by_iter in sorted(log.items()):
+                if len(by_iter) >= 2 and any("write" in ks for ks in by_iter.values()):
+                    self.records.append((self.kernel_index, view, int(off), tuple(sorted(by_iter)),
+                                         tuple(sorted({k for ks in by_iter.values() for k in ks}))))
+        self.kernel_index += 1
         # kernel boundary: queued contributions land in (iteration, sequence) order
         queue.sort(key=lambda q: (q[0], q[1]))
         for _, _, flat, off, v in queue:
@@ -323,3 +353,15 @@ def run(program, fn_name: str, inputs: dict, *, check_finite=False, deterministi
     if fn is None:
         raise KeyError(f"no function named '{fn_name}'")
     return Machine(fn, check_finite, deterministic).run(inputs)
+
+
+def detect(program, fn_name: str, inputs: dict, *, rng_seed: int = 0):
+    """The reference's ``detect_conflicts``: returns the records as tuples
+    (kernel, view, offset, iterations, kinds).  Arrays are mutated in place."""
+    fn = program.function(fn_name)
+    if fn is None:
+        raise KeyError(f"no function named '{fn_name}'")
+    m = Machine(fn)
+    m.rng_seed = rng_seed
+    m.run(inputs)
+    return m.records

@@ -254,6 +254,62 @@ __device__ __forceinline__ krn_i64 to_index(const Env &E, double x, int line, in
 }
 """
 
+# Conflict detector (reference: _Tracer, runtime.py:198-227; parallel_for under
+# cfg.conflict_detect, runtime.py:574-585).  A traced kernel is a DRY replay of the body: every
+# address is computed and checked as in the real kernel, loads are performed, stores and
+# atomic_adds are not; each access tags its location instead.  One 64-bit word per element:
+#   bits 0-2  kinds seen (1 read, 2 plain write, 4 atomic)
+#   bit  3    touched by at least two distinct iterations
+#   bits 4-   first iteration seen, plus one (0 = untouched)
+# The word is order independent in everything the report uses (kinds, the two-iterations bit).
+# phase 0 tags and counts the locations that become conflicts (two iterations, one plain write);
+# phase 1 replays and emits (view | kinds << 32, offset, iteration) for every access to such a
+# location, which the host sorts into the reference's records.
+_TRACE = r"""
+struct Trace {
+    unsigned long long *tag[NV > 0 ? NV : 1];
+    unsigned long long *count;   // [0] conflicting locations (phase 0), [1] triples produced (phase 1)
+    krn_i64 *triples;
+    krn_i64 cap;                 // triples the buffer holds; production beyond it is only counted
+    int phase;
+};
+__device__ __forceinline__ void krn_touch(const Trace &T, int v, krn_i64 off, krn_i64 i, unsigned kind)
+{
+    unsigned long long *w = T.tag[v] + off;
+    unsigned long long cur = *(volatile unsigned long long *)w;
+    if (T.phase == 0) {
+        const unsigned long long me = (unsigned long long)(i + 1);
+        for (;;) {
+            unsigned long long want;
+            if (cur == 0) want = (me << 4) | kind;
+            else if ((cur >> 4) == me) want = cur | kind;
+            else want = cur | 8ull | kind;
+            if (want == cur) return;
+            const unsigned long long old = atomicCAS(w, cur, want);
+            if (old == cur) {
+                const bool was = (cur & 8ull) && (cur & 2ull), is = (want & 8ull) && (want & 2ull);
+                if (is && !was) atomicAdd(&T.count[0], 1ull);
+                return;
+            }
+            cur = old;
+        }
+    } else if ((cur & 8ull) && (cur & 2ull)) {
+        const unsigned long long k = atomicAdd(&T.count[1], 1ull);
+        if ((krn_i64)k < T.cap) {
+            T.triples[3 * k] = (krn_i64)v | ((krn_i64)(cur & 7ull) << 32);
+            T.triples[3 * k + 1] = off;
+            T.triples[3 * k + 2] = i;
+        }
+    }
+}
+__device__ __forceinline__ double krn_trace_rd(const Env &E, const Trace &T, krn_i64 i, int v, krn_i64 off, bool bad)
+{
+    if (bad) return 0.0;
+    krn_touch(T, v, off, i, 1u);
+    return E.v[v][off];
+}
+"""
+
 
 class ModuleBuilder:
     """Generates the CUDA source of one function and the launch recipes the
@@ -271,6 +327,8 @@ class ModuleBuilder:
         self.counter = None  # AST counter of the statement being generated (window kernels)
         self.elide = None  # bounds-check elision context (tile kernels only)
         self.guards: list = []  # enclosing If conditions of the statement being generated
+        self.tracing = False  # a dry, access-tagging replay of a kernel is being generated (kernel_trace)
+        self.has_trace = False
         self.views: list = []  # view table: name -> index
         self.rank: dict = {}
         self.slots: dict = {}  # function-scope scalar -> slot in S
@@ -380,6 +438,8 @@ class ModuleBuilder:
         reg = self._reg(acc)
         if reg is not None:
             return reg
+        if self.tracing:
+            return f"krn_trace_rd(E, T, i, {self.vid(acc.view)}, {self.offset(acc, local)}, bad)"
         # the offset expression may set `bad`; rd() then yields 0.0 without touching memory
         return f"krn_seq_rd(E, {self.vid(acc.view)}, {self.offset(acc, local)}, bad)"
 
@@ -442,6 +502,16 @@ class ModuleBuilder:
             reg = self._reg(s.target)
             expr = {"=": "t_", "+=": f"{reg} + t_", "-=": f"{reg} - t_"}[s.op]
             out.append(f"{pad}{{ double t_ = {self.value(s.rhs, local)}; if (bad) {stop} {reg} = {expr}; }}")
+        elif k in ("AssignView", "AtomicAdd") and self.tracing:
+            # dry replay: same evaluation order as the interpreter (offset, then value, then the
+            # record: runtime.py:414-419, 435-440); nothing is stored
+            v = self.vid(s.target.view)
+            rhs = s.rhs if k == "AssignView" else s.value
+            out.append(
+                f"{pad}{{ krn_i64 o_ = {self.offset(s.target, local)}; if (bad) {stop} "
+                f"double t_ = {self.value(rhs, local)}; (void)t_; if (bad) {stop} "
+                f"krn_touch(T, {v}, o_, i, {2 if k == 'AssignView' else 4}u); }}"
+            )
         elif k == "AssignView":
             v = self.vid(s.target.view)
             expr = {"=": "t_", "+=": f"E.v[{v}][o_] + t_", "-=": f"E.v[{v}][o_] - t_"}[s.op]
@@ -518,6 +588,43 @@ class ModuleBuilder:
         if needs_offsets:
             recipe["apply"].append(self._staged_apply(sites, f"{name}_a"))
         return recipe
+
+    def kernel_trace(self, loop, name: str) -> dict:
+        """Dry, access-tagging replay of `loop` for the conflict detector (see _TRACE)."""
+        body: list = []
+        local = {loop.counter}
+        self.tracing, self.has_trace = True, True
+        try:
+            for s in loop.body:
+                self.element(s, local, body, "        ", None, True)
+        finally:
+            self.tracing = False
+        src = [
+            f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, Trace T)',
+            "{",
+            "    for (krn_i64 i = blockIdx.x * (krn_i64)blockDim.x + threadIdx.x; i < n; "
+            "i += (krn_i64)gridDim.x * blockDim.x) {",
+            "        bool bad = false;",
+        ] + body + ["    }", "}"]
+        self.parts.append("\n".join(src))
+        touched = set()
+        for s in walk_statements(loop.body):
+            k = kind(s)
+            exprs = []
+            if k in ("AssignView", "AtomicAdd"):
+                touched.add(s.target.view)
+                exprs = list(s.target.indices) + [s.rhs if k == "AssignView" else s.value]
+            elif k == "DeclScalar":
+                exprs = [s.init]
+            elif k == "AssignScalar":
+                exprs = [s.rhs]
+            elif k == "If":
+                exprs = [s.cond.lhs, s.cond.rhs]
+            for e in exprs:
+                for node in walk_expr(e):
+                    if kind(node) == "ViewAccess":
+                        touched.add(node.view)
+        return dict(name=name, views=sorted(touched))
 
     def _gather_apply(self, loop, view, group, name) -> dict:
         """Kernel over the rows k of `view`: adds, in (iteration, program order),
@@ -600,6 +707,8 @@ class ModuleBuilder:
 
     def source(self) -> str:
         head = _PREAMBLE % dict(nv=len(self.views), nh=len(self.hslots))
+        if self.has_trace:
+            head += _TRACE
         head += (
             "__device__ __forceinline__ double krn_seq_rd(const Env &E, int v, krn_i64 off, bool &bad)\n"
             "{ return rd(E, v, off, bad); }\n"

@@ -482,7 +482,7 @@ class ExecResult:
 class _Plan:
     """Compiled form of one function: generated module + step list."""
 
-    def __init__(self, fn):
+    def __init__(self, fn, trace: bool = False):
         self.fn = fn
         b = self.builder = codegen.ModuleBuilder(fn)
         self.steps: list = []
@@ -505,7 +505,10 @@ class _Plan:
             if k == "DeclView":
                 self.steps.append(("declview", s))
             elif k == "ParallelFor":
-                self.steps.append(("kernel", s, b.kernel(s, f"k{len(self.steps)}")))
+                recipe = b.kernel(s, f"k{len(self.steps)}")
+                if trace:  # conflict detector: a dry, access-tagging replay precedes the kernel
+                    recipe["trace"] = b.kernel_trace(s, f"k{len(self.steps)}_t")
+                self.steps.append(("kernel", s, recipe))
             elif k == "DeepCopy":
                 self.steps.append(("deepcopy", s))
             elif k == "ParallelSum":
@@ -527,12 +530,12 @@ _plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 _plans_by_id: dict = {}
 
 
-def _plan_for(fn) -> _Plan:
-    key = id(fn)
+def _plan_for(fn, trace: bool = False) -> _Plan:
+    key = (id(fn), trace)
     hit = _plans_by_id.get(key)
     if hit is not None and hit[0] is fn:
         return hit[1]
-    plan = _Plan(fn)
+    plan = _Plan(fn, trace)
     _plans_by_id[key] = (fn, plan)  # holds fn alive so the id stays unique
     return plan
 
@@ -600,6 +603,7 @@ class _Run:
         dev.upload(self.S.ptr, host)
         _cabi.check(dev.lib.krn_status_reset(dev.h))
         self.kernel_index = 0
+        self.conflicts: list = []
 
     def env(self, atomic=(0, 0, 0)) -> bytes:
         nv = max(len(self.b.views), 1)
@@ -656,6 +660,8 @@ class _Run:
             if recipe["needs_offsets"]:
                 ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
                 extra[2] = C.c_void_p(ostage.ptr)
+        if n > 0 and "trace" in recipe and self.cfg.conflict_detect:
+            self.trace_kernel(recipe["trace"], n)
         if n > 0:
             self.launch(recipe["name"], n, extra, atomic_choice(self.cfg, recipe["atomic_views"], self.views,
                                                                  self.b, n))
@@ -665,6 +671,68 @@ class _Run:
                     self.launch(ap["name"], count, extra)
         self.kernel_index += 1
         self.guard()
+
+    # -- conflict detector -----------------------------------------------------------------
+    TRIPLES_FIRST = 1 << 18  # triples the first collect pass has room for (6 MB)
+
+    def trace_kernel(self, recipe, n: int):
+        """Reference: _Tracer + the instrumented replay of parallel_for (runtime.py:198-227,
+        574-585): one record per location touched by two or more distinct iterations of this
+        kernel with a plain write among the accesses.  Here: a dry replay of the kernel tags
+        every location it touches (codegen._TRACE); if any location turned into a conflict a
+        second replay lists the iterations that touch those locations.  Both replays read the
+        Views as they are BEFORE the kernel and store nothing; the real kernel runs afterwards."""
+        dev, b = self.dev, self.b
+        nv = max(len(b.views), 1)
+        tags, tag_ptrs = [], [0] * nv
+        for name in recipe["views"]:
+            v = self.views.get(name)
+            if v is None or v.size == 0:
+                continue
+            v.device_ptr(dev, write=False)  # materialise lazily zero Views: the replay loads from them
+            buf = _DeviceBuffer(dev, 8 * v.size)
+            dev.fill(buf.ptr, v.size, 0.0)
+            tags.append(buf)
+            tag_ptrs[b.vid(name)] = buf.ptr
+        counts = _DeviceBuffer(dev, 16)
+        dev.fill(counts.ptr, 2, 0.0)
+        host = np.zeros(2, dtype=np.uint64)
+
+        def replay(phase, triples_ptr, cap):
+            tr = C.create_string_buffer(struct.pack(f"{nv}QQQqi4x", *tag_ptrs, counts.ptr, triples_ptr, cap, phase))
+            self.launch(recipe["name"], n, [n, tr])
+            self.read_status()  # an access out of bounds fails here exactly as it would in the kernel
+            dev.download(host, counts.ptr)
+
+        replay(0, 0, 0)
+        if host[0] == 0:
+            return
+        cap = self.TRIPLES_FIRST
+        while True:
+            triples = _DeviceBuffer(dev, 24 * cap)
+            dev.fill(counts.ptr + 8, 1, 0.0)
+            replay(1, triples.ptr, cap)
+            produced = int(host[1])
+            if produced <= cap:
+                break
+            cap = produced
+        rows = np.zeros((produced, 3), dtype=np.int64)
+        dev.download(rows, triples.ptr)
+        if produced == 0:
+            return
+        rows = np.unique(rows, axis=0)  # sorted by (view | kinds, offset, iteration)
+        kinds_of = [tuple(sorted(k for bit, k in enumerate(("read", "write", "atomic")) if mask >> bit & 1))
+                    for mask in range(8)]
+        cuts = np.flatnonzero(np.any(rows[1:, :2] != rows[:-1, :2], axis=1)) + 1
+        starts = [0, *cuts.tolist(), len(rows)]
+        head, offs, its = rows[:, 0].tolist(), rows[:, 1].tolist(), rows[:, 2].tolist()
+        found = [
+            ConflictRecord(self.kernel_index, b.views[head[lo] & 0xFFFFFFFF], offs[lo], tuple(its[lo:hi]),
+                           kinds_of[head[lo] >> 32])
+            for lo, hi in zip(starts[:-1], starts[1:])
+        ]
+        found.sort(key=lambda r: (r.view, r.offset))  # the reference sorts its log by (view, offset)
+        self.conflicts.extend(found)
 
     def do_deepcopy(self, s):
         d = self.views[s.dst]
@@ -811,13 +879,14 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
     fn = program.function(fn_name)
     if fn is None:
         raise KeyError(f"no function named '{fn_name}'")
-    if cfg.conflict_detect:
-        raise NotImplementedError(
-            "conflict detection is the reference's sequential CPU debugging aid "
-            "(runtime.py:574-585) and is outside the GPU path"
-        )
     views, scalars = _bind(fn, inputs)
     dev = Device.get(cfg.device)
+    if cfg.conflict_detect:
+        # statement granularity (a kernel of the report = a parallel_for of the source), every
+        # kernel preceded by its access-tagging replay
+        run = _Run(dev, _plan_for(fn, trace=True), views, scalars, _dc.replace(cfg, synchronous=True))
+        value = run.go()
+        return ExecResult(value, ConflictReport(tuple(run.conflicts)))
     if cfg.policy == "fused" and not cfg.check_finite:
         hit = fused.match(fn)
         if hit is not None and hit.applicable(views):
@@ -831,10 +900,16 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
 
 
 def detect_conflicts(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = None):
-    raise NotImplementedError(
-        "detect_conflicts replays kernels sequentially on the CPU by design "
-        "(reference runtime.py:709-726); it is not part of the GPU path"
-    )
+    """Every location touched by two distinct iterations of one kernel where at least one access
+    is a plain (non-atomic) write (reference: runtime.py:709-726).  The reference replays each
+    kernel sequentially in a shuffled order and logs every access in a dictionary; here a dry
+    replay of the kernel on the device tags the locations (`_Run.trace_kernel`).  The function is
+    executed as well (inputs are mutated, like the reference's instrumented run); for a racy
+    program the values are those of an unordered parallel run rather than of the reference's
+    seeded shuffle, the report is the same."""
+    base = cfg or ExecutionConfig()
+    cfg = _dc.replace(base, conflict_detect=True, policy="statements", synchronous=True)
+    return execute(program, fn_name, inputs, cfg).conflicts
 
 
 def pairwise_sum(values) -> float:

@@ -82,6 +82,5 @@ def test_binding_checks_need_no_device():
         krn.execute(lap, "normRes1DLaplacianSQ", {"x": vec("x", [1.0]), "b": vec("b", [1.0]), "q": 1.0})
     with pytest.raises(KeyError):
         krn.execute(lap, "nope", {})
-    with pytest.raises(NotImplementedError):
-        krn.execute(lap, "normRes1DLaplacianSQ", {"x": vec("x", [1.0]), "b": vec("b", [1.0])},
-                    ExecutionConfig(conflict_detect=True))
+    with pytest.raises(ShapeMismatch, match="missing"):
+        krn.detect_conflicts(lap, "normRes1DLaplacianSQ", {"x": vec("x", [1.0])})
