@@ -64,6 +64,8 @@ class Site:
     offset: object = None  # int c when the row index is `counter + c`
     column: object = None  # int or None (rank-1)
     mode: str = "atomic"  # "gather" | "atomic" | "staged_atomic"
+    merged: tuple = ()  # sites folded into this one (merge_adjacent_atomics)
+    absorbed: bool = False  # this site's contribution travels with an earlier site
 
 
 def _unit_affine(idx, counter):
@@ -134,7 +136,31 @@ def plan_atomics(loop) -> list:
                 st.mode = "gather"
             else:
                 st.mode = "staged_atomic" if view in touched_plainly else "atomic"
+    merge_adjacent_atomics(loop.body, {id(st.stmt): st for st in sites})
     return sites
+
+
+def merge_adjacent_atomics(body, by_id) -> None:
+    """Hardware-atomic sites that follow each other directly and name the same location - the
+    product rule's `atomic_add(_d_x(idx(i)), r * x(idx(i))); atomic_add(_d_x(idx(i)), x(idx(i)) * r);`
+    - issue ONE reduction with the sum of their values.  Nothing can observe the location in
+    between (an "atomic"-mode target is neither read nor plainly written by the kernel), and the
+    policy is exact only up to reassociation anyway (d + (a + b) for (d + a) + b); gather-mode
+    sites, which are bit-identical to the interpreter, are never merged."""
+    head = None
+    for s in body:
+        k = kind(s)
+        st = by_id.get(id(s)) if k == "AtomicAdd" else None
+        if st is not None and st.mode == "atomic":
+            if head is not None and head.stmt.target == s.target:
+                head.merged += (st,)
+                st.absorbed = True
+            else:
+                head = st
+            continue
+        head = None
+        if k == "If":
+            merge_adjacent_atomics(s.body, by_id)
 
 
 def guard_interval(guards, counter, trip, sym):
@@ -524,6 +550,11 @@ class ModuleBuilder:
             head = (f"{pad}{{ krn_i64 o_ = {self.offset(s.target, local)}; if (bad) {stop} "
                     f"double t_ = {self.value(s.value, local)}; if (bad) {stop} ")
             site = sites.get(id(s)) if sites else None
+            if site is not None and site.absorbed:
+                return  # its value was added to the preceding site's (merge_adjacent_atomics)
+            if site is not None and site.merged:
+                for m in site.merged:
+                    head += f"{{ double u_ = {self.value(m.stmt.value, local)}; if (bad) {stop} t_ = t_ + u_; }} "
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
             elif site.mode == "gather" and site.index in self.stage_windows:

@@ -720,10 +720,17 @@ class _Run:
         dev.download(rows, triples.ptr)
         if produced == 0:
             return
-        rows = np.unique(rows, axis=0)  # sorted by (view | kinds, offset, iteration)
+        # sort by (view, offset, iteration) and drop repeats (an iteration may touch a location
+        # several times); offsets stay below 2^40 elements, so (view, offset) is one 64-bit key
+        key = ((rows[:, 0] & 0xFFFFFFFF) << 40) | rows[:, 1]
+        order = np.lexsort((rows[:, 2], key))
+        rows, key = rows[order], key[order]
+        keep = np.ones(len(rows), dtype=bool)
+        keep[1:] = (key[1:] != key[:-1]) | (rows[1:, 2] != rows[:-1, 2])
+        rows, key = rows[keep], key[keep]
         kinds_of = [tuple(sorted(k for bit, k in enumerate(("read", "write", "atomic")) if mask >> bit & 1))
                     for mask in range(8)]
-        cuts = np.flatnonzero(np.any(rows[1:, :2] != rows[:-1, :2], axis=1)) + 1
+        cuts = np.flatnonzero(key[1:] != key[:-1]) + 1
         starts = [0, *cuts.tolist(), len(rows)]
         head, offs, its = rows[:, 0].tolist(), rows[:, 1].tolist(), rows[:, 2].tolist()
         found = [

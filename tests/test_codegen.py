@@ -39,6 +39,29 @@ def test_atomic_policies():
     assert [s.mode for s in codegen.plan_atomics(p.functions[0].body[0])] == ["staged_atomic"]
 
 
+def test_adjacent_atomics_on_one_location_merge():
+    """The product rule emits two atomic_adds to _d_x(idx(i)) back to back: one reduction with the
+    sum of both values (hardware-atomic sites only; gather-mode sites stay separate, they are
+    bit-identical to the interpreter)."""
+    gi = _loops(_grad("gather_indirect"))[1]
+    sites = codegen.plan_atomics(gi)
+    assert [(s.mode, len(s.merged), s.absorbed) for s in sites] == [("atomic", 1, False), ("atomic", 0, True)]
+    src = _plan_for(_grad("gather_indirect")).source
+    assert sum("krn_scatter(E," in ln and "__device__" not in ln for ln in src.splitlines()) == 1
+    lap = _loops(_grad("laplacian"))[2]
+    assert all(not s.merged and not s.absorbed for s in codegen.plan_atomics(lap))
+    # different locations, a statement in between, or different guards: not merged
+    p = krn.parse("""fn f(x: view<f64,1>, idx: view<f64,1>, v: view<f64,1>) { parallel_for i in 0..extent(idx,0) {
+        atomic_add(x(idx(i)), v(i)); atomic_add(x(idx(i) + 1), v(i));
+        let t: f64 = v(i);
+        atomic_add(x(idx(i) + 1), t);
+        if (i != 0) { atomic_add(x(idx(i) + 1), t); atomic_add(x(idx(i) + 1), 2.0 * t); atomic_add(x(idx(i) + 1), t); }
+    } }""")
+    sites = codegen.plan_atomics(p.functions[0].body[0])
+    assert [(len(s.merged), s.absorbed) for s in sites] == [(0, False), (0, False), (0, False), (2, False),
+                                                            (0, True), (0, True)]
+
+
 def test_every_corpus_function_plans():
     for stem in CORPUS:
         prog = krn.load_program(stem)
