@@ -28,6 +28,23 @@ from .lang.nodes import kind, walk_statements
 STRIDE_PAD = 8  # staging columns are padded so that column starts stay 32-byte aligned
 
 
+
+# Tree over a warp's steps (`steps` is a power of two <= 16).  After krn_warp_tree* every lane
+# holds the node of the step, so lane 0 parks it in shared memory at [warp][step]; the block's
+# epilogue folds the 8 * steps parked nodes - consecutive tree nodes, in order - with
+# krn_smem_tree.  One predicated STS per step: no registers held across steps and no
+# run-time-indexed stack, which the compiler can only keep in local memory (STL/LDL in the step
+# loop).  Measured on B200 at 134 M rows against that stack: affine_weighted primal 0.340 -> 0.324 ms,
+# sum_squares 0.186 -> 0.180, copy_chain 0.188 -> 0.180, mean_shift 0.367 -> 0.354 (stencil_smooth
+# 0.229 -> 0.233, safe_divide 0.256 -> 0.260, headline window kernel unchanged); a binary counter
+# in named registers costs the window kernels a block of occupancy (headline primal 0.526 -> 0.597).
+_TREE_DECL = "    __shared__ double s_nodes[128];  // [warp][step]: nodes of the block's reduction tree"
+_TREE_PUSH = "        if (lane_ == 0) s_nodes[(threadIdx.x >> 5) * steps + t] = node;"
+_TREE_SMEM = 128 * 8 + 32 * 8  # s_nodes + krn_final_tree's scratch
+
+
+
+
 def _first_access_is_full_store(group, view, ops_with_full_range, col=None) -> bool:
     """True when, in program order, the first statement of the group touching `view`
     (column `col` of it, for a rank-2 View) is an unguarded top-level `view(i) = rhs` whose
@@ -171,9 +188,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("    krn_priv_begin(E);")
     w("    const int lane_ = threadIdx.x & 31;")
     w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + (threadIdx.x >> 5)) * 128 * steps;")
-    w("    double tstack[6];  // binary-counter tree over the warp's steps")
-    w("    int tdepth = 0;")
-    w("    (void)tstack; (void)tdepth;")
+    w(_TREE_DECL)
     # Memory-level parallelism: the loads of B consecutive steps are issued before the first of them
     # is consumed (a kernel with one or two operand streams otherwise keeps a single 1 KB request per
     # warp in flight; measured on B200: 4.5 -> 6 TB/s for a one-stream reduction).  B shrinks with
@@ -344,9 +359,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
         else:
             w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
-        w("        int m_ = t;")
-        w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
-        w("        tstack[tdepth++] = node;")
+        w(_TREE_PUSH)
         w("    }")
     w("    }  // step of the batch")
     w("    }  // steps")
@@ -362,11 +375,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("    krn_priv_end(E);")
     if gather is not None:
         w("    {")
-        w("        __shared__ double s_warp[8];")
         w("        const int warp = threadIdx.x >> 5;")
-        w("        if (lane_ == 0) s_warp[warp] = tstack[0];")
         w("        __syncthreads();")
-        w("        if (warp == 0) { double v = krn_smem_tree(s_warp, 8, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
+        w("        if (warp == 0) { double v = krn_smem_tree(s_nodes, 8 * steps, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
         w("        if (krn_last_block(ticket, gridDim.x)) {")
         w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
         w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
@@ -376,7 +387,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
                 gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct,
-                static_smem=512 if gather is not None else 0)
+                static_smem=_TREE_SMEM if gather is not None else 0)
 
 
 # ---------------------------------------------------------------------------------------
@@ -525,9 +536,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     if direct:
         w("    krn_priv_begin(E);")
     w("    const krn_i64 wbase = ((krn_i64)blockIdx.x * 8 + warp_) * 128 * steps;")
-    w("    double tstack[6];  // binary-counter tree over the warp's steps")
-    w("    int tdepth = 0;")
-    w("    (void)tstack; (void)tdepth;")
+    w(_TREE_DECL)
     w("    int wq_[5];  // window position of each slot's iteration")
     w(f"    for (int e = 0; e < 4; ++e) wq_[e] = e * 32 + lane_ + {HLO};")
     w(f"    wq_[4] = lane_ < {HLO} ? lane_ : 128 + lane_;")
@@ -784,9 +793,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = {val}; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? {val} : krn_tree_pad((krn_u64)it_[e], (krn_u64)n); }}")
         w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
-        w("        int m_ = t;")
-        w("        while (m_ & 1) { node = tstack[--tdepth] + node; m_ >>= 1; }")
-        w("        tstack[tdepth++] = node;")
+        w(_TREE_PUSH)
         w("    }")
     w("    __syncwarp();")
     w("    }  // steps")
@@ -825,10 +832,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("    }")
     elif gather is not None:
         w("    {")
-        w("        __shared__ double s_warp[8];")
-        w("        if (lane_ == 0) s_warp[warp_] = tstack[0];")
         w("        __syncthreads();")
-        w("        if (warp_ == 0) { double v = krn_smem_tree(s_warp, 8, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
+        w("        if (warp_ == 0) { double v = krn_smem_tree(s_nodes, 8 * steps, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
         w("        if (krn_last_block(ticket, gridDim.x)) {")
         w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
         w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
@@ -841,5 +846,5 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 gather=gather, max_shift=plan["max_shift"],
                 elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct,
                 window=True, alt=alts, hlo=HLO, hhi=HHI, gather_cols=gcols,
-                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (512 if gather is not None else 0)
+                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (_TREE_SMEM if gather is not None else 0)
                 + 8 * (8 * 128 + 8) * gcols)
