@@ -35,6 +35,13 @@ class SourceSpan:
 NO_SPAN = SourceSpan()
 
 
+class Node:
+    """Common base of every tree node (the reference's ``krn.ast.Node``, ast.py:35): lets callers
+    write ``isinstance(x, Node)``.  Carries nothing; ``_node`` adds the ``span`` field."""
+
+    __slots__ = ()
+
+
 def _node(cls):
     """Class decorator: frozen dataclass + keyword-only ``span`` excluded
     from equality, list-valued fields coerced to tuples."""
@@ -90,63 +97,63 @@ class ViewDescriptor:
 
 
 @_node
-class Literal:
+class Literal(Node):
     value: float
 
 
 @_node
-class ScalarVar:
+class ScalarVar(Node):
     name: str
 
 
 @_node
-class IndexVar:
+class IndexVar(Node):
     name: str
 
 
 @_node
-class ViewAccess:
+class ViewAccess(Node):
     view: str
     indices: tuple
 
 
 @_node
-class Extent:
+class Extent(Node):
     view: str
     dim: int
 
 
 @_node
-class Binary:
+class Binary(Node):
     op: str
     lhs: object
     rhs: object
 
 
 @_node
-class Neg:
+class Neg(Node):
     operand: object
 
 
 @_node
-class Counter:
+class Counter(Node):
     name: str
 
 
 @_node
-class IntLiteral:
+class IntLiteral(Node):
     value: int
 
 
 @_node
-class IdxBinary:
+class IdxBinary(Node):
     op: str
     lhs: object
     rhs: object
 
 
 @_node
-class Compare:
+class Compare(Node):
     op: str
     lhs: object
     rhs: object
@@ -156,7 +163,7 @@ class Compare:
 
 
 @_node
-class DeclView:
+class DeclView(Node):
     descriptor: ViewDescriptor
     dyn_args: tuple = ()
     label: str = ""
@@ -171,69 +178,69 @@ class DeclView:
 
 
 @_node
-class DeclScalar:
+class DeclScalar(Node):
     name: str
     init: object
 
 
 @_node
-class AssignView:
+class AssignView(Node):
     target: ViewAccess
     op: str
     rhs: object
 
 
 @_node
-class AssignScalar:
+class AssignScalar(Node):
     name: str
     op: str
     rhs: object
 
 
 @_node
-class If:
+class If(Node):
     cond: Compare
     body: tuple
 
 
 @_node
-class ParallelFor:
+class ParallelFor(Node):
     counter: str
     upper: object
     body: tuple
 
 
 @_node
-class DeepCopy:
+class DeepCopy(Node):
     dst: str
     src: object  # view name (str) or scalar expression
 
 
 @_node
-class ParallelSum:
+class ParallelSum(Node):
     dst: str
     src: str
 
 
 @_node
-class ParallelSumInto:
+class ParallelSumInto(Node):
     dst: str
     src: object  # view name (str) or scalar expression
 
 
 @_node
-class AtomicAdd:
+class AtomicAdd(Node):
     target: ViewAccess
     value: object
 
 
 @_node
-class Return:
+class Return(Node):
     value: object
 
 
 @_node
-class Param:
+class Param(Node):
     name: str
     type: object  # ViewDescriptor or "f64"
 
@@ -243,7 +250,7 @@ class Param:
 
 
 @_node
-class FunctionDef:
+class FunctionDef(Node):
     name: str
     params: tuple
     body: tuple
@@ -254,7 +261,7 @@ class FunctionDef:
 
 
 @_node
-class Program:
+class Program(Node):
     functions: tuple = ()
 
     def function(self, name: str):

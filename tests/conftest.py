@@ -87,3 +87,12 @@ def corpus_case(golden, stem, n):
             inputs[k[len(prefix):]] = float(v) if v.ndim == 0 else np.array(v)
     wrt = tuple(str(golden[key + "/wrt"]).split(","))
     return inputs, wrt, key
+
+
+def free_port() -> int:
+    """A TCP port the OS reports free on 127.0.0.1 (rendezvous of the multi-process tests)."""
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]

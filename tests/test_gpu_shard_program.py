@@ -11,7 +11,7 @@ import pytest
 
 import paper_2507_13204_b200 as krn
 from paper_2507_13204_b200 import ExecutionConfig, ViewStorage, shard_program
-from conftest import assert_bits
+from conftest import assert_bits, free_port
 from test_shard_program_cpu import INDEXED, ROWWISE, _data, run_sharded
 
 pytestmark = pytest.mark.gpu
@@ -97,7 +97,7 @@ def test_two_processes_over_gloo():
     n, world = 20_001, 2
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
-    port = 29300 + os.getpid() % 400
+    port = free_port()
     procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, n, out)) for r in range(world)]
     for p in procs:
         p.start()
@@ -214,7 +214,7 @@ def test_every_collective_over_gloo():
     n, world = 30_011, 2
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
-    port = 29700 + os.getpid() % 250
+    port = free_port()
     procs = [ctx.Process(target=_gloo_worker_all, args=(r, world, port, n, out)) for r in range(world)]
     for p in procs:
         p.start()

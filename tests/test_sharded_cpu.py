@@ -13,7 +13,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2507_13204_b200.sharded import assemble_halo, pack_boundary, partition
-from conftest import assert_bits
+from conftest import assert_bits, free_port
 
 
 def test_partition_covers_and_aligns():
@@ -88,7 +88,7 @@ def test_halo_exchange_over_gloo(world):
     n = 257
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
-    port = 29500 + os.getpid() % 500 + world
+    port = free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, out)) for r in range(world)]
     for p in procs:
         p.start()
@@ -140,7 +140,7 @@ def test_exact_objective_over_gloo(world, n, span):
 
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
-    port = 29000 + os.getpid() % 500 + 7 * world + span
+    port = free_port()
     procs = [ctx.Process(target=_exact_worker, args=(r, world, port, n, span, out)) for r in range(world)]
     for p in procs:
         p.start()
