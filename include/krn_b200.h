@@ -169,7 +169,8 @@ int krn_module_destroy(krn_module *m);
 int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, size_t n_iterations,
                       size_t shared_bytes, void **args);
 /* launch `name` with exactly `blocks` x `threads_per_block` (tile kernels of fused statement
- * groups: one thread per 4 iterations, and block-level reductions that need every thread) */
+ * groups: one thread per 4 iterations, and block-level reductions that need every thread; 1 x 1 runs
+ * a parallel_for kernel's iterations in order on one thread, for kernels whose result depends on it) */
 int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_t blocks,
                             unsigned threads_per_block, size_t shared_bytes, void **args);
 /* shared_bytes: dynamic shared memory (<= 48 KB), used by the shared-memory-privatised

@@ -163,6 +163,70 @@ def merge_adjacent_atomics(body, by_id) -> None:
             merge_adjacent_atomics(s.body, by_id)
 
 
+def _never_same_location(t1, t2) -> bool:
+    """Index tuples t1 (evaluated by iteration i1) and t2 (by a DIFFERENT iteration i2), both in
+    normalize_index form: True when they provably never name one location."""
+    for (c1, terms1), (c2, terms2) in zip(t1, t2):
+        if terms1 != terms2 or any(atom[0] == "view" for atom, _ in terms1):
+            continue  # nothing to conclude from this component
+        coef = [c for atom, c in terms1 if atom[0] == "counter"]
+        if not coef:
+            if c1 != c2:
+                return True  # two different constants (same extent terms)
+        elif c1 == c2 or (c1 - c2) % coef[0] != 0:
+            return True  # a*i1 + c1 == a*i2 + c2 would need i1 == i2 / a non-integer shift
+    return False
+
+
+def carries_across_iterations(loop) -> bool:
+    """True when, as far as the index expressions tell, two different iterations of `loop` may
+    touch one location with a plain write among the two accesses - the situation in which the
+    result depends on the order of the iterations (the reference at threads=1 runs them 0..n-1,
+    runtime.py:586-593; its own tests rely on it: tests/test_runtime.py:101-115).  Index
+    expressions are affine in the counter or go through a View (then nothing is known)."""
+    writes: dict = {}
+    every: dict = {}
+
+    def note(acc, plain_write=False):
+        try:
+            norm = tuple(normalize_index(i) for i in acc.indices)
+        except (TypeError, ValueError):
+            norm = None
+        every.setdefault(acc.view, []).append(norm)
+        if plain_write:
+            writes.setdefault(acc.view, []).append(norm)
+        for i in acc.indices:
+            for node in walk_expr(i):
+                if kind(node) == "ViewAccess":
+                    note(node)
+
+    for s in walk_statements(loop.body):
+        k = kind(s)
+        exprs = []
+        if k == "AssignView":
+            note(s.target, True)
+            exprs = [s.rhs]
+        elif k == "AtomicAdd":
+            note(s.target)
+            exprs = [s.value]
+        elif k == "DeclScalar":
+            exprs = [s.init]
+        elif k == "AssignScalar":
+            exprs = [s.rhs]
+        elif k == "If":
+            exprs = [s.cond.lhs, s.cond.rhs]
+        for e in exprs:
+            for node in walk_expr(e):
+                if kind(node) == "ViewAccess":
+                    note(node)
+    for view, ws in writes.items():
+        for w in ws:
+            for other in every[view]:
+                if w is None or other is None or not _never_same_location(w, other):
+                    return True
+    return False
+
+
 def guard_interval(guards, counter, trip, sym):
     """(lo, up): the running index satisfies lo <= i <= n-1-up under `guards`, where n is the
     trip count (`trip` = its canonical form, `sym` = the canonicaliser)."""

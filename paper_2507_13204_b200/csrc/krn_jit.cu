@@ -267,7 +267,7 @@ extern "C" int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *
 {
     KRN_REQUIRE(shared_bytes <= 48 * 1024, "more than 48 KB of dynamic shared memory");
     KRN_REQUIRE(ctx && m && name, "null argument");
-    KRN_REQUIRE(threads_per_block >= 32 && threads_per_block <= 1024, "bad block size");
+    KRN_REQUIRE(threads_per_block >= 1 && threads_per_block <= 1024, "bad block size");
     KRN_REQUIRE(blocks <= 0x7fffffffu, "too many blocks");
     CUfunction f;
     int rc = find_function(m, name, &f);

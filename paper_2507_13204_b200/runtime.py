@@ -506,7 +506,11 @@ class _Plan:
                 self.steps.append(("declview", s))
             elif k == "ParallelFor":
                 recipe = b.kernel(s, f"k{len(self.steps)}")
-                if trace:  # conflict detector: a dry, access-tagging replay precedes the kernel
+                # iterations that may touch one location with a plain write among the accesses: the
+                # result depends on their order (see _Run.do_kernel)
+                recipe["carried"] = codegen.carries_across_iterations(s)
+                if trace or recipe["carried"]:
+                    # conflict detector: a dry, access-tagging replay precedes the kernel
                     recipe["trace"] = b.kernel_trace(s, f"k{len(self.steps)}_t")
                 self.steps.append(("kernel", s, recipe))
             elif k == "DeepCopy":
@@ -524,6 +528,7 @@ class _Plan:
         flush()
         self.source = b.source()
         self.nslots = max(len(b.slots), 1) + 1
+        self.carried = any(st[0] == "kernel" and st[2]["carried"] for st in self.steps)
 
 
 _plans: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -618,7 +623,7 @@ class _Run:
         return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqii", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
                            *([0.0] * nh), *atomic)
 
-    def launch(self, name: str, n: int, extra=(), atomic=(0, 0, 0)):
+    def launch(self, name: str, n: int, extra=(), atomic=(0, 0, 0), sequential=False):
         env = C.create_string_buffer(self.env(atomic))
         holders = [env]
         args = [C.addressof(env)]
@@ -628,6 +633,9 @@ class _Run:
             args.append(C.addressof(h))
         arr = (C.c_void_p * len(args))(*args)
         shared = 8 * atomic[0] if atomic[1] == 2 else 0
+        if sequential:  # one thread: the grid-stride loop of the kernel runs iterations 0..n-1 in order
+            _cabi.check(self.dev.lib.krn_module_launch_exact(self.dev.h, self.mod, name.encode(), 1, 1, shared, arr))
+            return
         _cabi.check(self.dev.lib.krn_module_launch(self.dev.h, self.mod, name.encode(), n, shared, arr))
 
     def go(self):
@@ -660,11 +668,21 @@ class _Run:
             if recipe["needs_offsets"]:
                 ostage = _DeviceBuffer(self.dev, 8 * recipe["n_staged"] * n)
                 extra[2] = C.c_void_p(ostage.ptr)
-        if n > 0 and "trace" in recipe and self.cfg.conflict_detect:
+        sequential = False
+        if n > 0 and self.cfg.conflict_detect:
             self.trace_kernel(recipe["trace"], n)
+        elif n > 1 and recipe["carried"]:
+            # Order-dependent as far as the index expressions tell.  The reference (threads=1, its
+            # default) runs iterations 0..n-1 one after the other (runtime.py:586-593) and its
+            # tests rely on that (a scan through v(i) = v(i-1) + i, tests/test_runtime.py:101-115).
+            # The tag replay decides on the actual indices: no location shared between two
+            # iterations with a plain write -> any order gives the same result, run in parallel;
+            # otherwise run the kernel on ONE thread, in order - slow, and exactly the reference.
+            sequential = self.trace_kernel(recipe["trace"], n, collect=False) > 0
         if n > 0:
-            self.launch(recipe["name"], n, extra, atomic_choice(self.cfg, recipe["atomic_views"], self.views,
-                                                                 self.b, n))
+            choice = (0, 0, 0) if sequential else atomic_choice(self.cfg, recipe["atomic_views"], self.views,
+                                                                self.b, n)
+            self.launch(recipe["name"], n, extra, choice, sequential=sequential)
             for ap in recipe["apply"]:
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:
@@ -675,7 +693,7 @@ class _Run:
     # -- conflict detector -----------------------------------------------------------------
     TRIPLES_FIRST = 1 << 18  # triples the first collect pass has room for (6 MB)
 
-    def trace_kernel(self, recipe, n: int):
+    def trace_kernel(self, recipe, n: int, collect: bool = True) -> int:
         """Reference: _Tracer + the instrumented replay of parallel_for (runtime.py:198-227,
         574-585): one record per location touched by two or more distinct iterations of this
         kernel with a plain write among the accesses.  Here: a dry replay of the kernel tags
@@ -705,8 +723,9 @@ class _Run:
             dev.download(host, counts.ptr)
 
         replay(0, 0, 0)
-        if host[0] == 0:
-            return
+        conflicts = int(host[0])
+        if conflicts == 0 or not collect:
+            return conflicts
         cap = self.TRIPLES_FIRST
         while True:
             triples = _DeviceBuffer(dev, 24 * cap)
@@ -719,7 +738,7 @@ class _Run:
         rows = np.zeros((produced, 3), dtype=np.int64)
         dev.download(rows, triples.ptr)
         if produced == 0:
-            return
+            return conflicts
         # sort by (view, offset, iteration) and drop repeats (an iteration may touch a location
         # several times); offsets stay below 2^40 elements, so (view, offset) is one 64-bit key
         key = ((rows[:, 0] & 0xFFFFFFFF) << 40) | rows[:, 1]
@@ -740,6 +759,7 @@ class _Run:
         ]
         found.sort(key=lambda r: (r.view, r.offset))  # the reference sorts its log by (view, offset)
         self.conflicts.extend(found)
+        return conflicts
 
     def do_deepcopy(self, s):
         d = self.views[s.dst]
@@ -898,11 +918,11 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
         hit = fused.match(fn)
         if hit is not None and hit.applicable(views):
             return ExecResult(hit.run(dev, views, scalars, cfg))
-    if cfg.policy in ("fused", "compiled") and not cfg.check_finite:
+    plan = _plan_for(fn)
+    if cfg.policy in ("fused", "compiled") and not cfg.check_finite and not plan.carried:
         from . import compiled
 
         return ExecResult(compiled.run(dev, fn, views, scalars, cfg))
-    plan = _plan_for(fn)
     return ExecResult(_Run(dev, plan, views, scalars, cfg).go())
 
 

@@ -76,3 +76,26 @@ def test_literals_are_exact():
     for v in (0.1, 1.5, -0.25, 3.0, 1e-300, 5e-324, -0.0):
         text = codegen.c_double(v).strip("()")
         assert float.fromhex(text) == v and np.signbit(float.fromhex(text)) == np.signbit(v)
+
+
+def test_order_dependent_kernels_are_recognised():
+    """carries_across_iterations: index expressions that let two iterations meet at one location
+    with a plain write among the accesses (reference scan, tests/test_runtime.py:101-115)."""
+    def flag(body, params="v: view<f64,1>, w: view<f64,1>, m: view<f64,2>, idx: view<f64,1>"):
+        p = krn.parse("fn f(%s) { parallel_for i in 0..extent(v,0) { %s } }" % (params, body))
+        return codegen.carries_across_iterations(p.functions[0].body[0])
+
+    assert flag("if (i != 0) { v(i) = v(i - 1) + i; }")          # scan
+    assert flag("w(0) = v(i);")                                   # every iteration writes one location
+    assert flag("w(idx(i)) = v(i);")                              # through a View: nothing known
+    assert flag("w(i) = v(i); w(i + 1) += 1.0;")                  # two writes one row apart
+    assert flag("m(i, 0) = m(i + 1, 0);")
+    assert not flag("v(i) = 3.0 * v(i);")
+    assert not flag("w(i) = v(i + 1) - v(i - 1);")                # neighbours of a View that is only read
+    assert not flag("m(i, 0) = v(i); m(i, 1) = m(i, 0) * m(i, 2);")   # literal columns of the own row
+    assert not flag("w(2 * i) = v(i); w(2 * i + 1) = v(i);")      # interleaved, never the same element
+    assert not flag("atomic_add(w(idx(i)), v(i)); v(i) = 0.0;")   # atomics are not plain writes
+    for stem in CORPUS:
+        prog = krn.load_program(stem)
+        for fn in (prog.functions[0], _grad(stem)):
+            assert not _plan_for(fn).carried

@@ -304,3 +304,43 @@ def test_compiled_modules_are_cached_on_disk(tmp_path, monkeypatch):
     other = tmp_path / "cache2"
     compile_once()
     assert not other.exists()
+
+
+def test_order_dependent_kernels_run_in_iteration_order():
+    """The reference at threads=1 (its default) runs iterations 0..n-1 in order and its tests rely
+    on it (tests/test_runtime.py:101-115: a scan completes).  Kernels whose index expressions allow
+    two iterations to meet at a plainly written location are checked by the tag replay and, when
+    they really do, run on one thread; otherwise in parallel.  Oracle = the sequential interpreter."""
+    import paper_2507_13204_b200 as krn
+    from oracle import interp
+
+    scan = """fn f(v: view<f64, 1>) -> f64 {
+        parallel_for i in 0..extent(v, 0) { if (i != 0) { v(i) = v(i - 1) + i; } }
+        return v(extent(v, 0) - 1); }"""
+    v = krn.ViewStorage.from_values("v", [0.0, 0.0, 0.0])
+    assert krn.execute(krn.parse(scan), "f", {"v": v}).value == 3.0      # the reference's own case
+    rng = np.random.default_rng(8)
+    cases = [
+        (scan, {"v": rng.normal(size=3000)}),
+        ("""fn f(v: view<f64,1>, acc: view<f64,1>) -> f64 {
+            parallel_for i in 0..extent(v,0) { acc(0) = v(i); acc(1) += v(i) * acc(0); } return acc(1); }""",
+         {"v": rng.normal(size=777), "acc": np.zeros(2)}),
+        # scatter through an index View: a permutation (parallel) and a map with repeats (in order)
+        ("""fn f(v: view<f64,1>, idx: view<f64,1>, out: view<f64,1>) -> f64 {
+            parallel_for i in 0..extent(idx,0) { out(idx(i)) = v(i) + out(idx(i)); } return out(0); }""",
+         {"v": rng.normal(size=5000), "idx": rng.permutation(5000).astype(np.float64), "out": rng.normal(size=5000)}),
+        ("""fn f(v: view<f64,1>, idx: view<f64,1>, out: view<f64,1>) -> f64 {
+            parallel_for i in 0..extent(idx,0) { out(idx(i)) = v(i) + 0.5 * out(idx(i)); atomic_add(out(i), 1.0); }
+            return out(0); }""",
+         {"v": rng.normal(size=5000), "idx": rng.integers(0, 50, size=5000).astype(np.float64),
+          "out": rng.normal(size=5000)}),
+    ]
+    for policy in ("fused", "compiled", "statements"):
+        for src, data in cases:
+            want = {k: a.copy() for k, a in data.items()}
+            fo = interp.run(krn.parse(src), "f", want)
+            call = {k: krn.ViewStorage.from_values(k, a) for k, a in data.items()}
+            f = krn.execute(krn.parse(src), "f", call, krn.ExecutionConfig(policy=policy)).value
+            assert f == fo, (policy, src)
+            for k in data:
+                assert np.array_equal(call[k].buffer, want[k]), (policy, k, src)
