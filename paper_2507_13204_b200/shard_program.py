@@ -204,6 +204,14 @@ def _inside_index(root, node) -> bool:
 
 
 def check_shardable(fn) -> None:
+    from .codegen import carries_across_iterations
+
+    for s in walk_statements(fn.body):
+        if kind(s) == "ParallelFor" and carries_across_iterations(s):
+            # its result is defined by ONE sweep over the whole range in iteration order
+            # (runtime._Run.do_kernel): rows cannot be cut across ranks
+            raise NotShardable(f"line {getattr(s.span, 'line', 0)}: iterations of this kernel may meet at a plainly "
+                               "written location; its result depends on their order")
     classify(fn)
 
 

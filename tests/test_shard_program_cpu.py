@@ -340,3 +340,16 @@ def test_random_programs_sharded_against_the_whole_problem():
 
     run()
     assert ran[0] >= 60
+
+
+def test_order_dependent_kernels_are_refused():
+    """A kernel whose iterations may meet at a plainly written location has a result defined by one
+    in-order sweep over the whole range (runtime._Run.do_kernel): it cannot be cut across ranks."""
+    import paper_2507_13204_b200 as krn
+    from paper_2507_13204_b200 import shard_program as sp
+
+    scan = krn.parse("fn f(v: view<f64,1>) -> f64 { parallel_for i in 0..extent(v,0) { if (i != 0) { "
+                     "v(i) = v(i - 1) + i; } } return v(extent(v,0) - 1); }")
+    with pytest.raises(sp.NotShardable, match="depends on their order"):
+        sp.check_shardable(scan.functions[0])
+    sp.check_shardable(krn.load_program("stencil_smooth").functions[0])   # neighbours of a read-only View: fine
