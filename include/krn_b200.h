@@ -173,6 +173,10 @@ int krn_module_launch(krn_ctx *ctx, krn_module *m, const char *name, size_t n_it
  * a parallel_for kernel's iterations in order on one thread, for kernels whose result depends on it) */
 int krn_module_launch_exact(krn_ctx *ctx, krn_module *m, const char *name, size_t blocks,
                             unsigned threads_per_block, size_t shared_bytes, void **args);
+/* registers per thread, local (stack / spill) bytes per thread and static shared memory of a compiled
+ * kernel: the host retunes generated kernels with them (occupancy bound of window kernels) */
+int krn_module_kernel_info(krn_module *m, const char *name, int *registers, int *local_bytes,
+                           int *static_shared_bytes);
 /* shared_bytes: dynamic shared memory (<= 48 KB), used by the shared-memory-privatised
  * accumulation policy of atomic_add targets with few rows */
 

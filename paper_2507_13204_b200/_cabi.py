@@ -72,6 +72,7 @@ SIGNATURES = {
     "krn_module_destroy": (_i, [_vp]),
     "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),
     "krn_module_launch_exact": (_i, [_vp, _vp, C.c_char_p, _sz, C.c_uint, _sz, _pp]),
+    "krn_module_kernel_info": (_i, [_vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "krn_status_reset": (_i, [_vp]),
     "krn_run_begin": (_i, [_vp, _pp, C.POINTER(C.c_size_t)]),
     "krn_reduce_workspace": (_i, [_vp, _sz, _pp, _pp, _pp]),

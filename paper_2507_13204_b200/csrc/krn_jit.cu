@@ -48,6 +48,7 @@ struct Api {
     CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              CUstream, void **, void **) = nullptr;
     CUresult (*GetErrorString)(CUresult, const char **) = nullptr;
+    CUresult (*FuncGetAttribute)(int *, CUfunction_attribute, CUfunction) = nullptr;
 } api;
 
 void *open_first(const std::vector<const char *> &names)
@@ -92,6 +93,7 @@ int load_api()
     KRN_SYM(drv, ModuleGetFunction, "cuModuleGetFunction")
     KRN_SYM(drv, LaunchKernel, "cuLaunchKernel")
     KRN_SYM(drv, GetErrorString, "cuGetErrorString")
+    KRN_SYM(drv, FuncGetAttribute, "cuFuncGetAttribute")
 #undef KRN_SYM
     int major = 0, minor = 0;
     if (api.Version(&major, &minor) == NVRTC_SUCCESS) api.ld256 = major > 12 || (major == 12 && minor >= 9);
@@ -259,6 +261,20 @@ static int find_function(krn_module *m, const char *name, CUfunction *out)
         it = m->functions.emplace(name, f).first;
     }
     *out = it->second;
+    return KRN_OK;
+}
+
+extern "C" int krn_module_kernel_info(krn_module *m, const char *name, int *registers, int *local_bytes,
+                                      int *static_shared_bytes)
+{
+    KRN_REQUIRE(m && name && registers && local_bytes && static_shared_bytes, "null argument");
+    CUfunction f;
+    int rc = find_function(m, name, &f);
+    if (rc) return rc;
+    CUresult r = api.FuncGetAttribute(registers, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
+    if (r == CUDA_SUCCESS) r = api.FuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
+    if (r == CUDA_SUCCESS) r = api.FuncGetAttribute(static_shared_bytes, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, f);
+    if (r != CUDA_SUCCESS) return driver_fail("cuFuncGetAttribute", r);
     return KRN_OK;
 }
 

@@ -195,6 +195,13 @@ class Device:
             m = self._modules[source] = h
         return m
 
+    def kernel_info(self, module, name: str) -> tuple:
+        """(registers per thread, local bytes per thread, static shared bytes) of a compiled kernel."""
+        regs, local, smem = C.c_int(), C.c_int(), C.c_int()
+        _cabi.check(self.lib.krn_module_kernel_info(module, name.encode(), C.byref(regs), C.byref(local),
+                                                    C.byref(smem)))
+        return regs.value, local.value, smem.value
+
 
 # ---------------------------------------------------------------------------
 # View storage

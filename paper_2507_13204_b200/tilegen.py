@@ -175,7 +175,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     gather = group.gather
     L: list = []
     w = L.append
-    w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
+    w(f"#ifndef KRN_MINB_{name}\n#define KRN_MINB_{name}\n#endif")  # see window_kernel
+    w(f'extern "C" __global__ void __launch_bounds__(256 KRN_MINB_{name}) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
       "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
       "unsigned int *ticket, double *red_out, int accumulate, int steps)")
     w("{")
@@ -515,7 +516,10 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     LO, UP = _guard_margins(group, an)
     L: list = []
     w = L.append
-    w(f'extern "C" __global__ void __launch_bounds__(256) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
+    # the occupancy bound is a macro the host may define ahead of the source after looking at the
+    # compiled kernel's register count (compiled.retuned_source)
+    w(f"#ifndef KRN_MINB_{name}\n#define KRN_MINB_{name}\n#endif")
+    w(f'extern "C" __global__ void __launch_bounds__(256 KRN_MINB_{name}) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
       "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
       "unsigned int *ticket, double *red_out, int accumulate, int steps, double *alt0, double *alt1, "
       "double *alt2, double *alt3)")
