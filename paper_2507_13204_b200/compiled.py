@@ -129,6 +129,9 @@ class CompiledPlan:
 _plans: dict = {}
 
 
+RETUNE_MIN_ELEMENTS = 1 << 20
+
+
 def retuned_module(dev, plan: CompiledPlan):
     """The plan's module with the occupancy bound of its fused kernels set one block per SM above
     what the compiler chose on its own.  These kernels are latency bound at 2-5 resident blocks
@@ -356,7 +359,9 @@ class _CompiledRun:
         from .runtime import _DeviceBuffer
 
         dev = self.dev
-        self.mod = retuned_module(dev, self.plan)
+        # small problems are launch-latency bound: the compiler's own allocation, one compilation
+        big = any(v.size >= RETUNE_MIN_ELEMENTS for v in self.views.values())
+        self.mod = retuned_module(dev, self.plan) if big else dev.module(self.plan.source)
         # status word and scalar slots live side by side in the context: one memset starts the run
         slots, cap = C.c_void_p(), C.c_size_t()
         _cabi.check(dev.lib.krn_run_begin(dev.h, C.byref(slots), C.byref(cap)))

@@ -181,3 +181,39 @@ def test_fewer_launches_than_statements():
     # halo recompute turns the whole generated gradient into one launch, like the hand-written kernel
     assert counts["fused"] == 1 and counts["compiled"] == 1 and counts["pointwise"] == 3, counts
     assert counts["statements"] >= 9, counts
+
+
+def test_occupancy_retuning_changes_no_bits(monkeypatch):
+    """compiled.retuned_module: the generated headline gradient is recompiled with an occupancy
+    bound one block per SM above the compiler's own choice; results are the same bits as without
+    (register allocation does not touch fp64 arithmetic), and the bound is never below that choice."""
+    from oracle import cport
+    from paper_2507_13204_b200 import compiled
+
+    lap = krn.load_program("laplacian")
+    gp = krn.differentiate(lap, "normRes1DLaplacianSQ", ("x", "b"))
+    gfn = gp.function("normRes1DLaplacianSQ_grad")
+    n = compiled.RETUNE_MIN_ELEMENTS + 70001
+    rng = np.random.default_rng(21)
+    x, b = rng.normal(size=n), rng.normal(size=n)
+    xo, dxo, dbo = x.copy(), np.zeros(n), np.zeros(n)
+    cport.laplacian_grad(xo, b.copy(), dxo, dbo, 1.0)
+    outs = []
+    for retune in ("1", "0"):
+        monkeypatch.setenv("KRN_RETUNE", retune)
+        compiled._plans.clear()
+        call = {"x": ViewStorage.from_values("x", x), "b": ViewStorage.from_values("b", b),
+                "_d_x": ViewStorage.zeros("_d_x", (n,)), "_d_b": ViewStorage.zeros("_d_b", (n,))}
+        krn.execute(gp, gfn.name, call, ExecutionConfig(policy="compiled"))
+        assert_bits(call["_d_x"].buffer, dxo, "_d_x")
+        assert_bits(call["_d_b"].buffer, dbo, "_d_b")
+        plan = compiled.plan_for(gfn)
+        (source,) = plan._tuned.values()
+        outs.append(source)
+        dev = krn.Device.get()
+        name = next(st[2]["name"] for st in plan.steps if st[0] == "group")
+        regs_base = dev.kernel_info(dev.module(plan.source), name)[0]
+        regs_now, local_now, _ = dev.kernel_info(dev.module(source), name)
+        assert regs_now <= regs_base and local_now <= dev.kernel_info(dev.module(plan.source), name)[1] + 64
+    assert outs[0].startswith("#define KRN_MINB_") and outs[1] == compiled.plan_for(gfn).source
+    compiled._plans.clear()
