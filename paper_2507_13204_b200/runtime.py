@@ -677,7 +677,9 @@ class _Run:
                 extra[2] = C.c_void_p(ostage.ptr)
         sequential = False
         if n > 0 and self.cfg.conflict_detect:
-            self.trace_kernel(recipe["trace"], n)
+            # a kernel with conflicts then runs in iteration order (deterministic: the values of the
+            # reference's plain threads=1 run; its instrumented run uses a seeded shuffle instead)
+            sequential = self.trace_kernel(recipe["trace"], n) > 0
         elif n > 1 and recipe["carried"]:
             # Order-dependent as far as the index expressions tell.  The reference (threads=1, its
             # default) runs iterations 0..n-1 one after the other (runtime.py:586-593) and its
@@ -938,9 +940,9 @@ def detect_conflicts(program, fn_name: str, inputs: dict, cfg: ExecutionConfig |
     is a plain (non-atomic) write (reference: runtime.py:709-726).  The reference replays each
     kernel sequentially in a shuffled order and logs every access in a dictionary; here a dry
     replay of the kernel on the device tags the locations (`_Run.trace_kernel`).  The function is
-    executed as well (inputs are mutated, like the reference's instrumented run); for a racy
-    program the values are those of an unordered parallel run rather than of the reference's
-    seeded shuffle, the report is the same."""
+    executed as well (inputs are mutated, like the reference's instrumented run); a kernel with
+    conflicts runs in iteration order, so a racy program leaves the values of the reference's plain
+    threads=1 run rather than those of its seeded shuffle; the report is the same."""
     base = cfg or ExecutionConfig()
     cfg = _dc.replace(base, conflict_detect=True, policy="statements", synchronous=True)
     return execute(program, fn_name, inputs, cfg).conflicts
