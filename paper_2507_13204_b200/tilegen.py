@@ -532,7 +532,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     if plan.get("gather_cols"):
         w(f"    __shared__ double G_all_[8][{128 * plan['gather_cols']}];")
         w("    double *G_ = G_all_[warp_];")
-        w(f"    double gn_[{8 * plan['gather_cols']}];  // the warp's tree nodes, step-major")
+        w(f"    __shared__ double s_gn[{64 * plan['gather_cols']}];  // [warp][step][subtree]: the block's tree nodes, in order")
     # which lanes of the halo slot run statement k (it covers [j0 - hlo_k, j0 + 128 + hhi_k))
     for k, (hlo, hhi) in enumerate(wp.halo):
         if hlo or hhi:
@@ -786,8 +786,9 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("        }")
         w("        __syncwarp();")
         for k in range(gcols):
-            w(f"        gn_[t * {gcols} + {k}] = krn_warp_tree4(G_[{128 * k} + lane_], G_[{128 * k + 32} + lane_], "
-              f"G_[{128 * k + 64} + lane_], G_[{128 * k + 96} + lane_]);")
+            w(f"        {{ const double nd_ = krn_warp_tree4(G_[{128 * k} + lane_], G_[{128 * k + 32} + lane_], "
+              f"G_[{128 * k + 64} + lane_], G_[{128 * k + 96} + lane_]); "
+              f"if (lane_ == 0) s_gn[(warp_ * steps + t) * {gcols} + {k}] = nd_; }}")
         w("    }")
     elif gather is not None:
         src = gather[0].src
@@ -815,16 +816,23 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     if gather is not None and gcols:
         C_ = gcols
         w("    {")
-        w(f"        // the warp's {C_} x steps nodes start at a node index that is a multiple of `steps`: fold log2(steps) levels")
-        w(f"        for (int cnt = {C_} * steps; cnt > {C_}; cnt >>= 1)")
-        w("            for (int i = 0; i < cnt / 2; ++i) gn_[i] = gn_[2 * i] + gn_[2 * i + 1];")
-        w(f"        __shared__ double s_g[{8 * C_}];")
-        w(f"        if (lane_ == 0) for (int k = 0; k < {C_}; ++k) s_g[warp_ * {C_} + k] = gn_[k];")
+        # lane 0 of every warp parked its C x steps nodes at [warp][step][subtree]: 8 * steps * C
+        # consecutive nodes of the tree, in order.  Warp 0 folds log2(8 * steps) levels, every level
+        # in parallel (read all pairs, then write), down to the block's C nodes.
         w("        __syncthreads();")
-        w("        if (threadIdx.x == 0) {  // 8 warps x C nodes -> C nodes of the block (three exact levels)")
-        w(f"            for (int cnt = {8 * C_}; cnt > {C_}; cnt >>= 1)")
-        w("                for (int i = 0; i < cnt / 2; ++i) s_g[i] = s_g[2 * i] + s_g[2 * i + 1];")
-        w(f"            for (int k = 0; k < {C_}; ++k) partials[(krn_i64)blockIdx.x * {C_} + k] = s_g[k];")
+        w("        if (warp_ == 0) {")
+        w(f"            for (int cnt = {8 * C_} * steps; cnt > {C_}; cnt >>= 1) {{")
+        w(f"                double pair_[{C_}];")
+        w("#pragma unroll")
+        w(f"                for (int u = 0; u < {C_}; ++u) {{ const int i = lane_ + 32 * u; "
+          "if (i < cnt / 2) pair_[u] = s_gn[2 * i] + s_gn[2 * i + 1]; }")
+        w("                __syncwarp();")
+        w("#pragma unroll")
+        w(f"                for (int u = 0; u < {C_}; ++u) {{ const int i = lane_ + 32 * u; "
+          "if (i < cnt / 2) s_gn[i] = pair_[u]; }")
+        w("                __syncwarp();")
+        w("            }")
+        w(f"            if (lane_ < {C_}) partials[(krn_i64)blockIdx.x * {C_} + lane_] = s_gn[lane_];")
         w("        }")
         w("        if (krn_last_block(ticket, gridDim.x)) {")
         w("            // nodes past the end of the flattened View were computed from padding leaves and equal")
