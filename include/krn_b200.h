@@ -112,6 +112,22 @@ int krn_reduce_pairwise(krn_ctx *ctx, const double *d_v, size_t n, double *d_out
 /* check_finite: *d_flag |= 1 when any element is NaN/Inf   (runtime.py:669-676) */
 int krn_check_finite(krn_ctx *ctx, const double *d_v, size_t n, int *d_flag);
 
+/* ---- deferred atomic_add, applied in the reference's order ---------------------------
+ * The reference queues every atomic_add of a kernel and applies the queue sorted by
+ * (iteration, program order): `flat[offset] += value`, one after the other
+ * (runtime.py:430-447, 615-620) - each location is a left fold in a fixed order, hence
+ * bit-reproducible.  krn_ordered_accumulate does exactly that for `records` queue entries that
+ * are ALREADY in queue order (record r = iteration * groups + group):
+ *     d_target[d_keys[r]] += d_vals[r*width + 0]; ... += d_vals[r*width + width-1];
+ * by a stable radix sort on the key followed by an in-order fold of every run of equal keys
+ * and one plain store per location (no atomics; identical bits on every run).  A key >=
+ * target_size (krn_memset the key array to 0xFF first) marks a site that did not execute.
+ * target_size and records must be below 2^32 - 1; width is 1..4. */
+int krn_ordered_accumulate(krn_ctx *ctx, double *d_target, size_t target_size, const uint32_t *d_keys,
+                           const double *d_vals, size_t records, int width);
+/* cudaMemsetAsync on the context's stream */
+int krn_memset(krn_ctx *ctx, void *d_ptr, int byte, size_t bytes);
+
 /* ---- headline objective: normRes1DLaplacianSQ and its generated gradient ----
  * (programs/laplacian.krn; gradient text tests/test_adjoint.py:43-94)
  *

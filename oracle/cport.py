@@ -25,6 +25,8 @@ def lib():
         L.krn_oracle_laplacian_grad.restype = None
         L.krn_oracle_laplacian_grad.argtypes = [_dp, _dp, _dp, _dp, C.c_size_t, C.c_double, _dp]
         L.krn_oracle_threads.restype = C.c_int
+        L.krn_oracle_apply_queue.restype = None
+        L.krn_oracle_apply_queue.argtypes = [_dp, C.c_size_t, C.POINTER(C.c_uint32), _dp, C.c_size_t, C.c_int]
         _lib = L
     return _lib
 
@@ -55,3 +57,13 @@ def laplacian_grad(x, b, dx, db, seed: float = 1.0) -> None:
 def threads() -> int:
     """OpenMP threads the order-free loops of the C port use."""
     return int(lib().krn_oracle_threads())
+
+
+def apply_queue(target, keys, vals, width: int = 1) -> None:
+    """The reference's apply loop over an already ordered queue of atomic_add records
+    (runtime.py:615-620): target[keys[r]] += vals[r, w] for w in order, r in order."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint32)
+    vals = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
+    assert vals.size == keys.size * width and target.flags.c_contiguous
+    lib().krn_oracle_apply_queue(_p(target.reshape(-1)), target.size, keys.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                 _p(vals), keys.size, width)

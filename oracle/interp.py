@@ -270,7 +270,12 @@ class Machine:
             if any(d < 0 for d in dims):
                 raise ShapeMismatch(f"view '{s.name}': negative extent {dims}")
             self.views[s.name] = np.zeros(dims, dtype=np.float64)
-        elif k in ("DeclScalar", "AssignScalar", "AssignView", "AtomicAdd", "If"):
+        elif k == "If":
+            # function scope: the body may hold any statement (reference runtime.py:548-550, self.body(b))
+            if self.compare(s.cond):
+                for inner in s.body:
+                    self.statement(inner)
+        elif k in ("DeclScalar", "AssignScalar", "AssignView", "AtomicAdd"):
             self.element(s, in_kernel=False)
         elif k == "ParallelFor":
             self.kernel(s)

@@ -145,3 +145,16 @@ void krn_oracle_laplacian_grad(double *x, const double *b, double *dx, double *d
         dx[j0] += 3.0 * r0;
     }
 }
+
+/* ---- deferred atomic_add queue, applied in order (runtime.py:615-620) -------------------
+ * records r = 0..records-1 are already in (iteration, program order); record r adds its
+ * `width` values, one after the other, to target[keys[r]].  keys[r] >= target_size marks a
+ * site that did not execute. */
+void krn_oracle_apply_queue(double *target, size_t target_size, const uint32_t *keys, const double *vals,
+                            size_t records, int width)
+{
+    for (size_t r = 0; r < records; ++r) {
+        if (keys[r] >= target_size) continue;
+        for (int w = 0; w < width; ++w) target[keys[r]] = target[keys[r]] + vals[r * (size_t)width + w];
+    }
+}

@@ -66,6 +66,7 @@ class Site:
     mode: str = "atomic"  # "gather" | "atomic" | "staged_atomic"
     merged: tuple = ()  # sites folded into this one (merge_adjacent_atomics)
     absorbed: bool = False  # this site's contribution travels with an earlier site
+    ord: object = None  # (key offset, value offset, groups, width, group): record layout of the ordered policy
 
 
 def _unit_affine(idx, counter):
@@ -152,7 +153,7 @@ def merge_adjacent_atomics(body, by_id) -> None:
         k = kind(s)
         st = by_id.get(id(s)) if k == "AtomicAdd" else None
         if st is not None and st.mode == "atomic":
-            if head is not None and head.stmt.target == s.target:
+            if head is not None and head.stmt.target == s.target and len(head.merged) + 1 < ORDERED_WIDTH:
                 head.merged += (st,)
                 st.absorbed = True
             else:
@@ -161,6 +162,32 @@ def merge_adjacent_atomics(body, by_id) -> None:
         head = None
         if k == "If":
             merge_adjacent_atomics(s.body, by_id)
+
+
+ORDERED_WIDTH = 4  # values one record of the ordered policy carries (krn_ordered_accumulate: width <= 4)
+
+
+def assign_ordered(site_lists) -> list:
+    """Record layout of the ordered accumulation policy (csrc/krn_ordered.cu) for the kernels
+    that share one launch.  Per kernel and target View with hardware-atomic sites: the sites in
+    program order form `groups` record slots per iteration (a head site and the sites merged
+    into it share one record of `width` values), record number = iteration * groups + group -
+    the reference's queue order (runtime.py:430-447: appended per iteration in program order,
+    sorted by (iteration, sequence number)).  Offsets are in units of the trip count."""
+    entries, key_off, val_off = [], 0, 0
+    for sites in site_lists:
+        by_view: dict = {}
+        for st in sites:
+            if st.mode in ("atomic", "staged_atomic") and not st.absorbed:
+                by_view.setdefault(st.view, []).append(st)
+        for view, heads in by_view.items():
+            groups, width = len(heads), max(1 + len(st.merged) for st in heads)
+            for g, st in enumerate(heads):
+                st.ord = (key_off, val_off, groups, width, g)
+            entries.append(dict(view=view, groups=groups, width=width, key_off=key_off, val_off=val_off))
+            key_off += groups
+            val_off += groups * width
+    return entries
 
 
 def _never_same_location(t1, t2) -> bool:
@@ -279,6 +306,9 @@ struct Env {
     krn_i64 priv_rows;  // accumulation policy of atomic_add targets (chosen by the host per launch):
     int apol;           //   0 plain RED.ADD.F64, 1 warp-aggregated, 2 shared-memory privatised, 3 leader-aggregated
     int priv_vid;       //   view whose rows are privatised when apol == 2
+    unsigned *okeys;    // apol == 4 (ordered): the kernel only records (target offset, values) per site group,
+    double *ovals;      //   krn_ordered_accumulate applies them afterwards in the reference's order
+    krn_i64 on;         //   trip count of the kernel (records of one group: on)
 };
 extern __shared__ double krn_priv[];
 __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, double t)
@@ -287,6 +317,19 @@ __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, doub
     else if (E.apol == 1) krn_red_add_aggregated(&E.v[v][o], t);
     else if (E.apol == 3) krn_red_add_leader(&E.v[v][o], t);
     else krn_red_add(&E.v[v][o], t);
+}
+// ordered policy: record r = i * G + g of the target's queue (layout: codegen.assign_ordered); values
+// beyond the group's own sites are -0.0, the additive identity (x + -0.0 == x bit for bit, -0.0 included)
+__device__ __forceinline__ void krn_ord_put(const Env &E, krn_i64 ko, krn_i64 vo, int G, int W, int g, krn_i64 i,
+                                            krn_i64 o, double a, double b, double c, double d)
+{
+    const krn_i64 r = i * G + g;
+    E.okeys[ko * E.on + r] = (unsigned)o;
+    double *p = E.ovals + vo * E.on + r * W;
+    p[0] = a;
+    if (W > 1) p[1] = b;
+    if (W > 2) p[2] = c;
+    if (W > 3) p[3] = d;
 }
 // -0.0 is the additive identity: a privatised row that still holds it received nothing
 __device__ __forceinline__ void krn_priv_begin(const Env &E)
@@ -615,10 +658,17 @@ class ModuleBuilder:
                     f"double t_ = {self.value(s.value, local)}; if (bad) {stop} ")
             site = sites.get(id(s)) if sites else None
             if site is not None and site.absorbed:
-                return  # its value was added to the preceding site's (merge_adjacent_atomics)
+                return  # its value travels with the preceding site's (merge_adjacent_atomics)
+            extra = []
             if site is not None and site.merged:
-                for m in site.merged:
-                    head += f"{{ double u_ = {self.value(m.stmt.value, local)}; if (bad) {stop} t_ = t_ + u_; }} "
+                for j, m in enumerate(site.merged):
+                    head += f"double u{j}_ = {self.value(m.stmt.value, local)}; if (bad) {stop} "
+                    extra.append(f"u{j}_")
+            ordered = None
+            if site is not None and site.ord is not None:
+                ko, vo, G, W, g = site.ord
+                vals = (["t_"] + extra + ["-0.0"] * ORDERED_WIDTH)[:ORDERED_WIDTH]
+                ordered = f"krn_ord_put(E, {ko}, {vo}, {G}, {W}, {g}, i, o_, {', '.join(vals)});"
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
             elif site.mode == "gather" and site.index in self.stage_windows:
@@ -628,10 +678,15 @@ class ModuleBuilder:
             elif site.mode == "gather":
                 out.append(head + f"stage[{site.index} * n + i] = t_; }}")
             elif site.mode == "staged_atomic":
-                out.append(head + f"stage[{site.index} * n + i] = t_; "
-                                  f"ostage[{site.index} * n + i] = o_; }}")
+                out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
+                           f"{{ stage[{site.index} * n + i] = t_; ostage[{site.index} * n + i] = o_; }} }}")
             else:
-                out.append(head + f"krn_scatter(E, {v}, o_, t_); }}")
+                # hardware reductions are exact only up to reassociation, so adjacent sites on one
+                # location issue one reduction with the sum of their values; the ordered policy
+                # keeps them apart (d + a) + b
+                total = "".join(f" t_ = t_ + {u};" for u in extra)
+                out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
+                           f"{{{total} krn_scatter(E, {v}, o_, t_); }} }}")
         elif k == "If":
             out.append(f"{pad}if {self.compare(s.cond, local)} {{")
             self.guards.append(s.cond)
@@ -646,6 +701,7 @@ class ModuleBuilder:
 
     def kernel(self, loop, name: str) -> dict:
         sites = plan_atomics(loop)
+        ordered = assign_ordered([sites])
         by_id = {id(st.stmt): st for st in sites}
         staged = [st for st in sites if st.mode in ("gather", "staged_atomic")]
         needs_offsets = any(st.mode == "staged_atomic" for st in sites)
@@ -667,11 +723,11 @@ class ModuleBuilder:
             # offsets column when present, else re-evaluate guards in the apply kernel
             for st in staged:
                 if st.mode == "staged_atomic":
-                    src.append(f"        ostage[{st.index} * n + i] = -1;")
+                    src.append(f"        if (E.apol != 4) ostage[{st.index} * n + i] = -1;")
         src += body + ["    }", "    krn_priv_end(E);" if any(st.mode == "atomic" for st in sites) else "", "}"]
         self.parts.append("\n".join(src))
         recipe = dict(name=name, sites=sites, n_staged=len(sites) if staged else 0,
-                      needs_offsets=needs_offsets, apply=[],
+                      needs_offsets=needs_offsets, apply=[], ordered=ordered,
                       atomic_views=sorted({st.view for st in sites if st.mode == "atomic"}))
         # apply kernels
         gather_views: dict = {}

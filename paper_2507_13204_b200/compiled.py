@@ -321,7 +321,7 @@ class _CompiledRun:
         return True
 
     # ---- launching -----------------------------------------------------------------------
-    def env(self, ptrs: dict, needed=None, atomic=(0, 0, 0)) -> bytes:
+    def env(self, ptrs: dict, needed=None, atomic=(0, 0, 0, 0, 0, 0)) -> bytes:
         """Kernel argument block.  `ptrs`: explicit device pointers (promoted Views);
         `needed`: the other Views the kernel touches - only those are materialised on the
         device (None = every View of the function, for kernels that are not analysed)."""
@@ -342,7 +342,7 @@ class _CompiledRun:
         for name, slot in b.hslots.items():
             h[slot] = float(self.H.get(name, 0.0))
         self._shared = 8 * atomic[0] if atomic[1] == 2 else 0
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqii", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h, *atomic)
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqiiQQq", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h, *atomic)
 
     def launch_raw(self, name, grid_items, env_bytes, extra):
         env = C.create_string_buffer(env_bytes)
@@ -370,6 +370,11 @@ class _CompiledRun:
         else:
             self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
             dev.fill(self.S.ptr, self.plan.nslots, 0.0)
+        # scalar parameters the function redefines with device data (a gather into the parameter,
+        # arithmetic on View elements) live in the slot array: start them at the caller's value
+        for p in self.plan.fn.params:
+            if not p.is_view and p.name not in self.plan.an.host_scalars:
+                dev.fill(self.S.ptr + 8 * self.b.slot(p.name), 1, float(self.H[p.name]))
         for step in self.plan.steps:
             getattr(self, "do_" + step[0])(*step[1:])
         return self.finish()
@@ -461,9 +466,8 @@ class _CompiledRun:
             recipe["_needed"] = needed
         from .runtime import atomic_choice
 
-        env = self.env(ptrs, needed - set(ptrs),
-                       atomic_choice(self.cfg, recipe["atomic_views"], self.views, self.b, n_launch,
-                                     recipe.get("static_smem", 0)))
+        choice, ordered = atomic_choice(dev, self.cfg, recipe, self.views, self.b, n, recipe.get("static_smem", 0))
+        env = self.env(ptrs, needed - set(ptrs), choice)
         extra = [n, n_launch, n_safe, C.c_uint(zero_mask), C.c_void_p(stage_ptr), ld]
         # steps per warp (a power of two: a block is a node of the reduction tree).  Measured on B200 at
         # 134 M rows (tools/corpus_bench.py): kernels that end in a fused reduction pay a block-level
@@ -487,6 +491,8 @@ class _CompiledRun:
         self.launch_tile(recipe["name"], nblocks, env, extra)
         for name, buf in alt_bufs.items():
             self.views[name]._adopt(buf)
+        if ordered is not None:
+            ordered.apply()
 
     def launch_tile(self, name, nblocks, env_bytes, extra):
         # krn_module_launch sizes a grid-stride grid; tile kernels need exactly ceil(threads/256) blocks
@@ -516,12 +522,16 @@ class _CompiledRun:
             from .runtime import atomic_choice
 
             needed = _views_in_stmts([loop])
-            self.launch_raw(recipe["name"], n, self.env({}, needed, atomic_choice(
-                self.cfg, recipe["atomic_views"], self.views, self.b, n)), extra)
+            choice, ordered = atomic_choice(self.dev, self.cfg, recipe, self.views, self.b, n)
+            self.launch_raw(recipe["name"], n, self.env({}, needed, choice), extra)
             for ap in recipe["apply"]:
+                if ordered is not None and ap["over"] == "iterations":
+                    continue  # the staged contributions went to the ordered queue instead
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:
                     self.launch_raw(ap["name"], count, self.env({}, needed), extra)
+            if ordered is not None:
+                ordered.apply()
 
     def do_deepcopy(self, s):
         from .runtime import ShapeMismatch

@@ -151,7 +151,10 @@ class _Bound:
         if n == 0:
             return None if self.m.grad else 0.0
         if (self.m.grad and synchronous and cfg is not None and cfg.stream_host_io
-                and n >= self.STREAM_MIN_ROWS and not x._dev_ok and not b._dev_ok):
+                and n >= self.STREAM_MIN_ROWS and not x._dev_ok and not b._dev_ok
+                and all(views[name].extents[0] == n for name in self.roles.values())):
+            # (Views longer than x - legal: only rows [0, n) are touched - take the resident path,
+            # which keeps their tails; the chunk buffers of the pipeline are sized by n)
             return self.run_streamed(dev, views)
         x_in = x.device_ptr(dev, write=False)
         b_ptr = b.device_ptr(dev, write=False)
@@ -171,8 +174,10 @@ class _Bound:
         dx, db = self._shadows(views)
         dx_zero = bool(dx is not None and dx._zero)
         db_zero = bool(db is not None and db._zero)
-        dx_ptr = dx.device_ptr(dev, discard=dx_zero) if dx is not None else 0
-        db_ptr = db.device_ptr(dev, discard=db_zero) if db is not None else 0
+        # the kernel writes rows [0, n) only: a lazily zero shadow with MORE rows must really hold
+        # its zeros beyond them (the read of the zeros is still skipped)
+        dx_ptr = dx.device_ptr(dev, discard=dx_zero and dx.extents[0] == n) if dx is not None else 0
+        db_ptr = db.device_ptr(dev, discard=db_zero and db.extents[0] == n) if db is not None else 0
         _cabi.check(lib.krn_laplacian_grad(dev.h, C.c_void_p(x_in), C.c_void_p(x_out.ptr), C.c_void_p(b_ptr),
                                            C.c_void_p(dx_ptr), C.c_void_p(db_ptr), int(dx_zero), int(db_zero),
                                            n, 0, n, None, float(self.m.seed)))

@@ -423,23 +423,27 @@ class Analysis:
                 for inner in walk_statements(s.body):
                     if kind(inner) in ("DeclScalar", "AssignScalar"):
                         device.add(inner.name)  # guarded function-scope scalars: keep on the device
-        host = {p.name for p in self.fn.params if not p.is_view}
+        # A scalar PARAMETER starts out host-known (the caller's value) but stays so only while
+        # every definition of it is host-evaluable too: `alpha = parallel_sum(x)` or
+        # `alpha = alpha + x(0)` move it to the device (its slot is initialised with the caller's
+        # value, compiled._CompiledRun.go), exactly like any other scalar.
+        params = {p.name for p in self.fn.params if not p.is_view}
         changed = True
-        cand = set(defs) - device
+        cand = (set(defs) | params) - device
         while changed:
             changed = False
             for name in list(cand):
-                for e in defs[name]:
+                for e in defs.get(name, ()):
                     ok = True
                     for n in walk_expr(e):
                         kk = kind(n)
-                        if kk == "ViewAccess" or (kk == "ScalarVar" and n.name not in cand and n.name not in host):
+                        if kk == "ViewAccess" or (kk == "ScalarVar" and n.name not in cand):
                             ok = False
                     if not ok:
                         cand.discard(name)
                         changed = True
                         break
-        return host | cand
+        return cand
 
     def _live_scalars(self) -> set:
         """Scalars that are ever read (anywhere): a gather into a scalar outside this

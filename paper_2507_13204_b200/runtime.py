@@ -434,8 +434,14 @@ class ExecutionConfig:
     # chunks and overlap upload / kernel / download of the shadows (fused.run_streamed)
     stream_host_io: bool = False
     # how atomic_add contributions to non-injective targets are accumulated (generated kernels):
-    # "red" hardware fp64 reductions, "warp" warp-aggregated, "smem" block-privatised in shared
-    # memory (targets of <= 6144 elements), "auto" = smem for small hot targets, else red
+    # "ordered" the reference's own order - queue sorted by (iteration, program order), applied as a
+    # left fold per location (runtime.py:615-620) - through a stable radix sort by target and a
+    # segmented in-order fold (csrc/krn_ordered.cu): bit-identical to the reference, identical from
+    # run to run; "red" hardware fp64 reductions, "warp" warp-aggregated, "lead" leader-aggregated,
+    # "smem" block-privatised in shared memory (targets of <= 6144 elements): exact up to
+    # reassociation (relative 1e-12).  "auto" = "ordered" when deterministic_reduction is set (the
+    # reference's default and its determinism contract), else smem for small hot
+    # targets and lead for the rest
     atomic_policy: str = "auto"
     # fusion pass: also merge statements across neighbour dependencies (a stencil after an in-place
     # update, deferred atomics and the rows they land on) by recomputing the few halo iterations
@@ -447,8 +453,8 @@ class ExecutionConfig:
             raise ValueError("threads must be >= 1")
         if self.policy not in ("fused", "compiled", "statements"):
             raise ValueError("policy must be 'fused', 'compiled' or 'statements'")
-        if self.atomic_policy not in ("auto", "red", "warp", "smem", "lead"):
-            raise ValueError("atomic_policy must be 'auto', 'red', 'warp', 'smem' or 'lead'")
+        if self.atomic_policy not in ("auto", "ordered", "red", "warp", "smem", "lead"):
+            raise ValueError("atomic_policy must be 'auto', 'ordered', 'red', 'warp', 'smem' or 'lead'")
 
 
 def effective_threads(cfg: ExecutionConfig) -> int:
@@ -555,16 +561,56 @@ def _plan_for(fn, trace: bool = False) -> _Plan:
 SMEM_PRIVATE_MAX = 6144  # doubles: 48 KB of dynamic shared memory
 
 
-def atomic_choice(cfg, atomic_views, views, builder, n, static_smem: int = 0):
-    """(rows, policy, view id) for Env: how a kernel accumulates its direct atomic_add
-    contributions.  Privatisation pays when the target is small and hit often: every block
-    folds its contributions in shared memory and issues at most one RED per row."""
+NO_ATOMICS = (0, 0, 0, 0, 0, 0)
+ORDERED_LIMIT = 0xFFFFFFFF - 1  # 32-bit keys and record numbers (krn_ordered_accumulate)
+
+
+class OrderedStage:
+    """Queue of one launch's deferred atomic_add records under the ordered policy: the kernel
+    writes (target offset, values) per site group at record = iteration * groups + group
+    (codegen.assign_ordered), `apply` hands each target's queue to krn_ordered_accumulate."""
+
+    def __init__(self, dev: Device, entries, views: dict, n: int):
+        self.dev, self.entries, self.views, self.n = dev, entries, views, n
+        groups = sum(e["groups"] for e in entries)
+        self.keys = _DeviceBuffer(dev, 4 * n * groups)
+        self.vals = _DeviceBuffer(dev, 8 * n * sum(e["groups"] * e["width"] for e in entries))
+        # all-ones key = "this site did not execute" (guarded sites, iterations that failed a check)
+        _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.keys.ptr), 0xFF, 4 * n * groups))
+
+    @staticmethod
+    def feasible(entries, views: dict, n: int) -> bool:
+        return all(views[e["view"]].size < ORDERED_LIMIT and n * e["groups"] < ORDERED_LIMIT for e in entries)
+
+    def apply(self):
+        dev, n = self.dev, self.n
+        for e in self.entries:
+            v = self.views[e["view"]]
+            _cabi.check(dev.lib.krn_ordered_accumulate(
+                dev.h, C.c_void_p(v.device_ptr(dev)), v.size, C.c_void_p(self.keys.ptr + 4 * e["key_off"] * n),
+                C.c_void_p(self.vals.ptr + 8 * e["val_off"] * n), n * e["groups"], e["width"]))
+
+
+def atomic_choice(dev, cfg, recipe, views, builder, n, static_smem: int = 0):
+    """(Env tail, OrderedStage or None): how a kernel accumulates its hardware-atomic
+    atomic_add sites.  Env tail = (privatised rows, policy, privatised view id, key queue,
+    value queue, trip count)."""
+    entries = recipe.get("ordered") or []
+    want = cfg.atomic_policy
+    if entries and n > 0 and (want == "ordered" or (want == "auto" and cfg.deterministic_reduction)):
+        if OrderedStage.feasible(entries, views, n):
+            stage = OrderedStage(dev, entries, views, n)
+            return (0, 4, 0, stage.keys.ptr, stage.vals.ptr, n), stage
+        if want == "ordered":
+            raise ValueError("atomic_policy='ordered' needs targets and queues of fewer than 2^32 - 2 entries")
+    if want in ("ordered", "auto") and cfg.deterministic_reduction and entries:
+        want = "lead"  # targets beyond 32-bit keys: hardware reductions, exact up to reassociation
+    atomic_views = recipe.get("atomic_views") or []
     if not atomic_views:
-        return (0, 0, 0)
+        return NO_ATOMICS, None
     name = atomic_views[0]
     rows = views[name].size
-    want = cfg.atomic_policy
-    if want == "auto":
+    if want in ("auto", "ordered"):
         # measured (tools/atomic_policies.py, profiles/r1_atomic_policies.json): privatisation wins by
         # 2-20x on small targets; leader aggregation costs nothing on spread-out targets and removes
         # the same-address serialisation of a hot row
@@ -575,7 +621,7 @@ def atomic_choice(cfg, atomic_views, views, builder, n, static_smem: int = 0):
         # the kernel's own shared memory (windows, reduction scratch) and the privatised rows
         # together exceed what a launch gets without opting in: aggregate in the warp instead
         want = "lead"
-    return (rows, {"red": 0, "warp": 1, "smem": 2, "lead": 3}[want], builder.vid(name))
+    return (rows, {"red": 0, "warp": 1, "smem": 2, "lead": 3}[want], builder.vid(name), 0, 0, 0), None
 
 
 def _scalar_src(dev, plan, S, src):
@@ -617,7 +663,7 @@ class _Run:
         self.kernel_index = 0
         self.conflicts: list = []
 
-    def env(self, atomic=(0, 0, 0)) -> bytes:
+    def env(self, atomic=NO_ATOMICS) -> bytes:
         nv = max(len(self.b.views), 1)
         ptrs, e0, e1 = [0] * nv, [0] * nv, [0] * nv
         for i, name in enumerate(self.b.views):
@@ -627,10 +673,10 @@ class _Run:
                 e0[i] = v.extents[0]
                 e1[i] = v.extents[1] if len(v.extents) == 2 else 1
         nh = max(len(self.b.hslots), 1)  # Env.H: unused on the statement path, but part of the layout
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqii", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqiiQQq", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
                            *([0.0] * nh), *atomic)
 
-    def launch(self, name: str, n: int, extra=(), atomic=(0, 0, 0), sequential=False):
+    def launch(self, name: str, n: int, extra=(), atomic=NO_ATOMICS, sequential=False):
         env = C.create_string_buffer(self.env(atomic))
         holders = [env]
         args = [C.addressof(env)]
@@ -689,13 +735,16 @@ class _Run:
             # otherwise run the kernel on ONE thread, in order - slow, and exactly the reference.
             sequential = self.trace_kernel(recipe["trace"], n, collect=False) > 0
         if n > 0:
-            choice = (0, 0, 0) if sequential else atomic_choice(self.cfg, recipe["atomic_views"], self.views,
-                                                                self.b, n)
+            choice, ordered = (NO_ATOMICS, None) if sequential else atomic_choice(self.dev, self.cfg, recipe, self.views, self.b, n)
             self.launch(recipe["name"], n, extra, choice, sequential=sequential)
             for ap in recipe["apply"]:
+                if ordered is not None and ap["over"] == "iterations":
+                    continue  # the staged contributions went to the ordered queue instead
                 count = self.views[ap["view"]].extents[0] if ap["over"] == "rows" else n
                 if count > 0:
                     self.launch(ap["name"], count, extra)
+            if ordered is not None:
+                ordered.apply()
         self.kernel_index += 1
         self.guard()
 
@@ -905,6 +954,62 @@ def _bind(fn, inputs: dict):
     return views, scalars
 
 
+def _pure_element(stmts) -> bool:
+    return all(kind(s) in codegen._ELEMENT and (kind(s) != "If" or _pure_element(s.body)) for s in stmts)
+
+
+class _Extents:
+    __slots__ = ("extents",)
+
+    def __init__(self, extents):
+        self.extents = extents
+
+
+_specialised: dict = {}
+
+
+def _specialise(fn, views: dict):
+    """Function-scope `if` blocks whose body holds more than element statements (a parallel_for,
+    a bulk builtin, a View declaration): the reference simply executes the body when the condition
+    holds (runtime.py:548-550).  Conditions are index comparisons over extents and literals - host
+    data - so they are decided here and the taken bodies spliced into a straight-line function,
+    which every execution policy then plans as usual (memoised per function and outcome)."""
+    if not any(kind(s) == "If" and not _pure_element(s.body) for s in fn.body):
+        return fn
+    ext = {k: _Extents(v.extents) for k, v in views.items()}
+    outcomes: list = []
+
+    def walk(body):
+        out = []
+        for s in body:
+            k = kind(s)
+            if k == "DeclView":
+                try:
+                    args = iter(s.dyn_args)
+                    ext[s.name] = _Extents(tuple(e.size if kind(e) == "StaticExtent" else int(_index_value(next(args), ext))
+                                                 for e in s.descriptor.extents))
+                except (TypeError, KeyError):
+                    pass
+            if k == "If" and not _pure_element(s.body):
+                a, b = _index_value(s.cond.lhs, ext), _index_value(s.cond.rhs, ext)
+                taken = {"<": a < b, "<=": a <= b, ">": a > b, ">=": a >= b, "==": a == b, "!=": a != b}[s.cond.op]
+                outcomes.append(taken)
+                if taken:
+                    out.extend(walk(s.body))
+                continue
+            out.append(s)
+        return out
+
+    body = walk(fn.body)
+    key = (id(fn), tuple(outcomes))
+    hit = _specialised.get(key)
+    if hit is not None and hit[0] is fn:
+        return hit[1]
+    new = _dc.replace(fn, body=tuple(body))
+    _specialised[key] = (fn, new)
+    return new
+
+
 def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = None) -> ExecResult:
     """Run ``fn_name`` on the GPU.  View inputs are mutated in place (their
     device storage is; ``.buffer`` shows the result).  Synchronous, like the
@@ -916,6 +1021,7 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
     if fn is None:
         raise KeyError(f"no function named '{fn_name}'")
     views, scalars = _bind(fn, inputs)
+    fn = _specialise(fn, views)
     dev = Device.get(cfg.device)
     if cfg.conflict_detect:
         # statement granularity (a kernel of the report = a parallel_for of the source), every

@@ -185,6 +185,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     # chunk of the reduction tree); `steps` > 1 amortises block start-up and the block-level
     # combine on bandwidth-bound sizes
     direct = sorted({st.view for l in group.ops for st in l.sites if st.mode == "atomic"})
+    from . import codegen
+    ordered = codegen.assign_ordered([l.sites for l in group.ops if l.what == "kernel"])
     if direct:
         w("    krn_priv_begin(E);")
     w("    const int lane_ = threadIdx.x & 31;")
@@ -388,7 +390,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
                 gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct,
-                static_smem=_TREE_SMEM if gather is not None else 0)
+                ordered=ordered, static_smem=_TREE_SMEM if gather is not None else 0)
 
 
 # ---------------------------------------------------------------------------------------
@@ -513,6 +515,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 stage_reg_sites.add(st.index)
     gather = group.gather
     direct = sorted({st.view for l in group.ops for st in l.sites if st.mode == "atomic"})
+    from . import codegen
+    ordered = codegen.assign_ordered([l.sites for l in group.ops if l.what == "kernel"])
     LO, UP = _guard_margins(group, an)
     L: list = []
     w = L.append
@@ -856,7 +860,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     every = promoted + windows
     return dict(name=name, promoted=every, stage_cols=plan["stage_cols"], has_stage=bool(plan["stage_cols"]),
                 gather=gather, max_shift=plan["max_shift"],
-                elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct,
+                elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct, ordered=ordered,
                 window=True, alt=alts, hlo=HLO, hhi=HHI, gather_cols=gcols,
                 static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (_TREE_SMEM if gather is not None else 0)
                 + 8 * (8 * 128 + 8) * gcols)

@@ -22,7 +22,7 @@ def _index_maps(n, rows, rng):
     }
 
 
-@pytest.mark.parametrize("apol", ["auto", "red", "warp", "smem", "lead"])
+@pytest.mark.parametrize("apol", ["auto", "ordered", "red", "warp", "smem", "lead"])
 @pytest.mark.parametrize("policy", ["compiled", "statements"])
 def test_gather_indirect_gradient_all_policies(policy, apol):
     from oracle import interp
@@ -38,11 +38,13 @@ def test_gather_indirect_gradient_all_policies(policy, apol):
             got = {"x": ViewStorage.from_values("x", x), "idx": ViewStorage.from_values("idx", idx.astype(np.float64)),
                    "_d_x": ViewStorage.zeros("_d_x", (rows,))}
             krn.execute(gp, "gatherSquares_grad", got, ExecutionConfig(policy=policy, atomic_policy=apol))
+            if apol in ("auto", "ordered"):  # the reference's order: same bits
+                assert np.array_equal(got["_d_x"].buffer, want["_d_x"]), (policy, apol, n, rows, label)
             err = np.abs(got["_d_x"].buffer - want["_d_x"])
             assert np.all(err <= 1e-12 * np.abs(want["_d_x"])), (policy, apol, n, rows, label, err.max())
 
 
-@pytest.mark.parametrize("apol", ["red", "warp", "smem", "lead"])
+@pytest.mark.parametrize("apol", ["ordered", "red", "warp", "smem", "lead"])
 def test_integer_contributions_are_exact(apol):
     """reference tests/test_runtime.py:150-164, generalised: sums of small integers are exact in
     any order, so every policy must return the same bits"""
@@ -71,11 +73,13 @@ def test_rank2_target_privatised():
     idx, v = rng.integers(0, rows, size=n).astype(np.float64), rng.normal(size=n)
     want = {"idx": idx.copy(), "v": v.copy(), "m": np.ones((rows, 3))}
     interp.run(p, "f", want)
-    for apol in ("red", "smem", "warp"):
+    for apol in ("red", "smem", "warp", "ordered"):
         got = {"idx": ViewStorage.from_values("idx", idx), "v": ViewStorage.from_values("v", v),
                "m": ViewStorage.from_values("m", np.ones((rows, 3)))}
         krn.execute(p, "f", got, ExecutionConfig(atomic_policy=apol))
         assert np.allclose(got["m"].buffer, want["m"], rtol=1e-12, atol=1e-12), apol
+        if apol == "ordered":
+            assert np.array_equal(got["m"].buffer, want["m"])
 
 
 def test_privatised_rows_next_to_the_kernels_own_shared_memory():
@@ -100,9 +104,10 @@ def test_privatised_rows_next_to_the_kernels_own_shared_memory():
     a, idx = rng.normal(size=n), rng.integers(0, rows, size=n).astype(np.float64)
     want = {"a": a.copy(), "idx": idx.copy(), "acc": np.zeros(rows)}
     wv = interp.run(p, "f", want)
-    for apol in ("auto", "smem"):
+    for apol, det in (("auto", True), ("auto", False), ("smem", True)):
         got = {"a": ViewStorage.from_values("a", a), "idx": ViewStorage.from_values("idx", idx),
                "acc": ViewStorage.zeros("acc", (rows,))}
-        v = krn.execute(p, "f", got, ExecutionConfig(policy="compiled", atomic_policy=apol)).value
+        v = krn.execute(p, "f", got, ExecutionConfig(policy="compiled", atomic_policy=apol,
+                                                     deterministic_reduction=det)).value
         assert v == wv
         assert np.array_equal(got["acc"].buffer, want["acc"]) and np.array_equal(got["a"].buffer, want["a"])

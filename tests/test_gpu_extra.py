@@ -55,7 +55,7 @@ def _gradient_cases():
     for stem in EXTRA:
         if not bool(g[f"{stem}/has_grad"]):
             continue  # the reference's transform rejects the program (or it returns nothing)
-        for apol in (["auto", "red", "warp", "smem", "lead"] if stem in ATOMIC_TARGETS else ["auto"]):
+        for apol in (["auto", "ordered", "red", "warp", "smem", "lead"] if stem in ATOMIC_TARGETS else ["auto"]):
             out.append((stem, apol))
     return out
 
@@ -79,7 +79,7 @@ def test_gradient_matches_reference(extra_golden, stem, n, policy, apol):  # noq
         if not isinstance(v, ViewStorage):
             continue
         want = extra_golden[f"{key}/grad/after/{k}"]
-        if k in ATOMIC_TARGETS.get(stem, ()):
+        if k in ATOMIC_TARGETS.get(stem, ()) and apol not in ("auto", "ordered"):
             # BASELINE.json: relative 1e-12, stated because the order of atomics is not deterministic
             err = np.abs(v.buffer - want)
             assert np.all(err <= 1e-12 * np.maximum(np.abs(want), 1.0)), (key, policy, apol, k, err.max())
@@ -106,7 +106,7 @@ def test_rank2_scatter_with_integer_contributions_is_exact():
     want[:, 2] += 3.0 * counts
     want[0, 1] += 2.0 * n
     for policy in ("compiled", "statements"):
-        for apol in ("red", "warp", "smem", "lead", "auto"):
+        for apol in ("red", "warp", "smem", "lead", "auto", "ordered"):
             acc = ViewStorage.from_values("acc", np.full((rows, 3), 0.25))
             krn.execute(p, "f", {"idx": ViewStorage.from_values("idx", idx.astype(np.float64)), "acc": acc},
                         ExecutionConfig(policy=policy, atomic_policy=apol))
