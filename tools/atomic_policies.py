@@ -43,7 +43,7 @@ def main():
             iv = ViewStorage.from_values("idx", idx.astype(np.float64))
             iv.device_ptr(dev, write=False)
             want = None
-            for apol in ("red", "lead", "warp", "smem"):
+            for apol in ("ordered", "red", "lead", "warp", "smem"):
                 if apol == "smem" and rows > 6144:
                     continue
                 if args.only and args.only != f"{rows}:{label}:{apol}":
@@ -59,6 +59,13 @@ def main():
                     dev.record(e1)
                     ts.append(dev.elapsed_ms(e0, e1))
                 got = acc.buffer.copy()
+                if apol == "ordered":
+                    # two runs of the ordered policy must agree bit for bit (the last two repetitions ran
+                    # on fresh zero targets): checked against one more run
+                    again = ViewStorage.zeros("acc", (rows,))
+                    krn.execute(prog, "scatter", {"idx": iv, "v": v, "acc": again},
+                                ExecutionConfig(atomic_policy=apol, device=dev))
+                    assert np.array_equal(again.buffer, got), "ordered policy is not reproducible"
                 if want is None:
                     want = np.bincount(idx, weights=v.peek(), minlength=rows)
                 err = float(np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)))
