@@ -118,11 +118,12 @@ int krn_check_finite(krn_ctx *ctx, const double *d_v, size_t n, int *d_flag);
  * (runtime.py:430-447, 615-620) - each location is a left fold in a fixed order, hence
  * bit-reproducible.  krn_ordered_accumulate does exactly that for `records` queue entries that
  * are ALREADY in queue order (record r = iteration * groups + group):
- *     d_target[d_keys[r]] += d_vals[r*width + 0]; ... += d_vals[r*width + width-1];
- * by a stable radix sort on the key followed by an in-order fold of every run of equal keys
- * and one plain store per location (no atomics; identical bits on every run).  A key >=
- * target_size (krn_memset the key array to 0xFF first) marks a site that did not execute.
- * target_size and records must be below 2^32 - 1; width is 1..4. */
+ *     d_target[d_keys[r]] += d_vals[0*records + r]; ... += d_vals[(width-1)*records + r];
+ * (values are planes of `records` doubles).  Records are partitioned stably by target bucket
+ * (radix passes in HBM), each bucket is folded in order inside shared memory, and every
+ * location is written with one plain store: no atomics, identical bits on every run.  A key
+ * must be < target_size or all ones (krn_memset the key array to 0xFF first): the mark of a
+ * site that did not execute.  target_size <= 2^31, records < 2^32 - 1, width 1..4. */
 int krn_ordered_accumulate(krn_ctx *ctx, double *d_target, size_t target_size, const uint32_t *d_keys,
                            const double *d_vals, size_t records, int width);
 /* cudaMemsetAsync on the context's stream */

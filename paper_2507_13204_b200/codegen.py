@@ -323,13 +323,13 @@ __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, doub
 __device__ __forceinline__ void krn_ord_put(const Env &E, krn_i64 ko, krn_i64 vo, int G, int W, int g, krn_i64 i,
                                             krn_i64 o, double a, double b, double c, double d)
 {
-    const krn_i64 r = i * G + g;
+    const krn_i64 r = i * G + g, plane = E.on * G;  // values are planes of on * G doubles
     E.okeys[ko * E.on + r] = (unsigned)o;
-    double *p = E.ovals + vo * E.on + r * W;
+    double *p = E.ovals + vo * E.on + r;
     p[0] = a;
-    if (W > 1) p[1] = b;
-    if (W > 2) p[2] = c;
-    if (W > 3) p[3] = d;
+    if (W > 1) p[plane] = b;
+    if (W > 2) p[2 * plane] = c;
+    if (W > 3) p[3 * plane] = d;
 }
 // -0.0 is the additive identity: a privatised row that still holds it received nothing
 __device__ __forceinline__ void krn_priv_begin(const Env &E)

@@ -8,27 +8,35 @@
 // (acceptance C5).
 //
 // Here: the generated kernel writes one record per executed site group,
-//     key[r]            = flat offset of the target element (uint32)
-//     val[r*width + w]  = the values of the group's sites, program order
+//     key[r]               = flat offset of the target element (uint32)
+//     val[w * records + r] = the values of the group's sites, program order
 // at r = iteration * groups + group, so record order IS the reference's queue
-// order.  krn_ordered_accumulate then
-//   1. sorts (key, r) by key with a STABLE least-significant-digit radix sort
-//      (per pass: per-tile digit histogram -> exclusive scan of the
-//      [digit][tile] table -> scatter that ranks equal digits in tile order,
-//      through shared memory so that runs leave the SM coalesced),
-//   2. folds every run of equal keys, in order, starting from the target's
-//      current value, and stores the result with ONE plain store per location.
-// No atomics on the target, nothing depends on the schedule: the result is
-// bit-identical to the reference and identical from run to run.  Runs longer
-// than kLongAfter records (a hot location) are folded by a whole block that
-// streams the values through shared memory ahead of the one thread adding
-// them; the chain of dependent fp64 additions itself is the definition of the
-// result and cannot be shortened.
+// order.  krn_ordered_accumulate then brings every location's records together
+// WITHOUT changing their relative order and folds them in that order:
 //
-// All kernels are HBM-bound integer/byte work (no tensor-core shape): per pass
-// 4 B/record (histogram) + 8 B read + 8 B written; the fold reads 8 B/record of
-// (key, r), gathers the values (one 32 B sector per record) and updates the
-// target in ascending address order.
+//   A. bucket partition in HBM.  The targets are cut into buckets of 2^LB
+//      consecutive elements (LB <= 12: a bucket's targets fit in 32 KB of shared
+//      memory).  One or two STABLE least-significant-digit passes over the bits
+//      [LB, LB + high) of the key - up to 10 bits each - move (key, values) so
+//      that the records of a bucket are contiguous and still in queue order.
+//      Per pass: per-tile digit histogram -> exclusive scan of the [digit][tile]
+//      table -> scatter that ranks equal digits in tile order (ballots, no
+//      atomics) and leaves the tile through shared memory as coalesced runs.
+//   B. one block per bucket: the bucket's targets are loaded into shared
+//      memory, its records are streamed in chunks; every chunk is sorted
+//      stably by the low key bits INSIDE shared memory (one or two 6-7 bit
+//      ranking passes over packed (key, slot) words) and each run of equal keys
+//      is folded in order onto the target element; the targets are written
+//      back with plain coalesced stores.
+//
+// No atomics on the target, nothing depends on the schedule: the result is
+// bit-identical to the reference and identical from run to run.  A location
+// that receives very many records is a long chain of dependent fp64 additions
+// by definition of the result; it bounds the time of its bucket's block.
+//
+// All kernels are integer/byte streaming work (no tensor-core shape).  HBM
+// traffic per record of width W: pass = 4 B (histogram) + 2 x (4 + 8 W) B;
+// final = (4 + 8 W) B read + 16 B per touched target.
 #include "krn_common.cuh"
 #include "krn_prelude.cuh"
 
@@ -39,12 +47,17 @@ typedef unsigned int u32;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                 // records per thread and tile
-constexpr int kTile = kThreads * kItems;   // 4096 records: 32 KB of (key, r) in shared memory
+constexpr int kTile = kThreads * kItems;   // 4096 records per tile of a partition pass
 constexpr int kWarpSpan = 32 * kItems;     // consecutive records ranked by one warp
 constexpr int kScanChunk = kThreads * 8;
-constexpr int kLongAfter = 64;             // a run still open after this many records goes to a block
-constexpr int kLongChunk = 1024;           // records a block stages per round of the long fold
 constexpr int kMaxWidth = 4;
+constexpr int kMaxPassBits = 10;           // digits of a partition pass
+constexpr int kMaxLocalBits = 12;          // low key bits resolved inside shared memory
+constexpr int kChunk = 2048;               // records a bucket's block stages per round
+constexpr int kSlotBits = 11;              // log2(kChunk): packed word = (low key << kSlotBits) | slot
+constexpr int kChunkSpan = kChunk / kWarps;  // consecutive chunk records ranked by one warp
+constexpr int kLocalPassBits = 6;
+constexpr u32 kNone = 0xffffffffu;
 
 __device__ __forceinline__ u32 lanemask_lt()
 {
@@ -53,9 +66,10 @@ __device__ __forceinline__ u32 lanemask_lt()
     return m;
 }
 
-// Lanes of the warp holding the same `bits`-bit digit as the caller (valid lanes only): one ballot per
+// Lanes of the warp holding the same digit as the caller (valid lanes only): one ballot per
 // bit.  (match.any does the same in one instruction but its cost grows with the number of distinct
-// values in the warp - measured here: 166 us per 16.7 M-record pass against ballots' constant time.)
+// values in the warp - measured: 166 us per 16.7 M-record pass against 110 us with ballots; shared
+// memory atomics cost 2 cycles per lane and bounded the histogram at 115 us per pass.)
 template <int BITS>
 __device__ __forceinline__ u32 same_digit_lanes(u32 d, bool valid)
 {
@@ -68,6 +82,55 @@ __device__ __forceinline__ u32 same_digit_lanes(u32 d, bool valid)
     }
     return peers;
 }
+// run-time digit width up to kLocalPassBits (uniform across the block)
+__device__ __forceinline__ u32 same_digit_lanes_rt(u32 d, bool valid, int bits)
+{
+    u32 peers = __ballot_sync(KRN_FULL_MASK, valid);
+#pragma unroll
+    for (int b = 0; b < 6; ++b) {
+        if (b < bits) {
+            const bool bit = (d >> b) & 1u;
+            const u32 with = __ballot_sync(KRN_FULL_MASK, bit);
+            peers &= bit ? with : ~with;
+        }
+    }
+    return peers;
+}
+
+// Exclusive scan over `radix` per-digit totals held in shared memory (radix <= 1024, a power of two
+// or less than kThreads): thread t owns the digits [t*per, (t+1)*per).  out[d] = sum of tot[< d].
+__device__ __forceinline__ void digit_scan(const u32 *tot, u32 *out, int radix, u32 *s_wsum)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (radix + kThreads - 1) / kThreads;
+    u32 mine[4];
+    u32 sum = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int d = threadIdx.x * per + u;
+        mine[u] = (u < per && d < radix) ? tot[d] : 0u;
+        sum += mine[u];
+    }
+    u32 inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(KRN_FULL_MASK, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    u32 run = inc - sum;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w)
+        if (w < warp) run += s_wsum[w];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int d = threadIdx.x * per + u;
+        if (u < per && d < radix) out[d] = run;
+        run += mine[u];
+    }
+    __syncthreads();
+}
 
 // ---- pass step 1: digit histogram of every tile ---------------------------------------
 // table[digit * tiles + tile]: scanned in this order it yields, for every (digit, tile), the
@@ -78,10 +141,11 @@ __global__ void __launch_bounds__(kThreads)
 ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__restrict__ table)
 {
     // per-warp counters, bumped by the lowest lane of every group of equal digits with a plain
-    // read-modify-write: shared-memory atomics cost 2 cycles per lane and would bound the pass
+    // read-modify-write
     constexpr u32 mask = (1u << BITS) - 1u;
-    __shared__ u32 s_cnt[kWarps][1 << BITS];
-    for (int k = threadIdx.x; k < kWarps << BITS; k += kThreads) (&s_cnt[0][0])[k] = 0;
+    constexpr int kRadix = 1 << BITS;
+    __shared__ u32 s_cnt[kWarps][kRadix];
+    for (int k = threadIdx.x; k < kWarps * kRadix; k += kThreads) (&s_cnt[0][0])[k] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = size_t(blockIdx.x) * kTile + size_t(warp) * kWarpSpan;
@@ -100,11 +164,11 @@ ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__re
         __syncwarp();
     }
     __syncthreads();
-    if (threadIdx.x <= mask) {
+    for (int d = threadIdx.x; d < kRadix; d += kThreads) {
         u32 total = 0;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) total += s_cnt[w][threadIdx.x];
-        table[size_t(threadIdx.x) * tiles + blockIdx.x] = total;
+        for (int w = 0; w < kWarps; ++w) total += s_cnt[w][d];
+        table[size_t(d) * tiles + blockIdx.x] = total;
     }
 }
 
@@ -205,39 +269,41 @@ __global__ void __launch_bounds__(kThreads) scan_apply(u32 *data, size_t count, 
 
 // ---- pass step 3: stable scatter ------------------------------------------------------------
 // Warp w of the tile ranks records [w*512, (w+1)*512) of the tile, 32 consecutive records per
-// round: lanes with the same digit find each other (match.any); their rank within the round is
-// the number of lower lanes among them, and the warp's running count of the digit (shared
-// memory, updated by the lowest lane) orders the rounds.  Tile order = (warp, round, lane), so
-// equal digits keep their input order.  The records are then placed in shared memory in digit
-// order and leave the tile as runs of consecutive destinations.
+// round: the lanes holding the same digit find each other with ballots; their rank within the
+// round is the number of lower lanes among them, and the warp's running count of the digit
+// (shared memory, bumped by the lowest lane) orders the rounds.  Tile order = (warp, round, lane),
+// so equal digits keep their input order.  Keys, then every value plane in turn, are placed in
+// shared memory in digit order and leave the tile as runs of consecutive destinations.
+// Values are planes: vals[w * m + record].
 template <int BITS>
 __global__ void __launch_bounds__(kThreads)
-ord_scatter(const u32 *__restrict__ keys_in, const u32 *__restrict__ idx_in, u32 *__restrict__ keys_out,
-            u32 *__restrict__ idx_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles)
+ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in, u32 *__restrict__ keys_out,
+            double *__restrict__ vals_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles, int width)
 {
     constexpr u32 mask = (1u << BITS) - 1u;
     constexpr int kRadix = 1 << BITS;
-    __shared__ u32 s_cnt[kWarps][kRadix];  // per-warp digit counts, then the warp's first slot of the digit in the tile
-    __shared__ u32 s_first[kRadix];        // first slot of the digit in the sorted tile
-    __shared__ u32 s_dest[kRadix];         // global destination of that slot
-    __shared__ u32 s_key[kTile];
-    __shared__ u32 s_idx[kTile];
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    double *s_val = reinterpret_cast<double *>(ord_smem);   // [kTile]
+    u32 *s_key = reinterpret_cast<u32 *>(s_val + kTile);     // [kTile]
+    u32 *s_g = s_key + kTile;                                // [kTile] global destination of every sorted slot
+    u32 *s_cnt = s_g + kTile;      // [kWarps][kRadix] per-warp digit counts, then the warp's first slot of the digit
+    u32 *s_tot = s_cnt + kWarps * kRadix;  // [kRadix] records of the digit in the tile
+    u32 *s_first = s_tot + kRadix;          // [kRadix] first slot of the digit in the sorted tile
+    u32 *s_dest = s_first + kRadix;         // [kRadix] global destination of that slot
     __shared__ u32 s_wsum[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = size_t(blockIdx.x) * kTile;
     const u32 live = u32(m - base < size_t(kTile) ? m - base : size_t(kTile));  // records of this tile
-    for (int k = threadIdx.x; k < kWarps * kRadix; k += kThreads) (&s_cnt[0][0])[k] = 0;
+    for (int k = threadIdx.x; k < kWarps * kRadix; k += kThreads) s_cnt[k] = 0;
     __syncthreads();
 
-    u32 key[kItems], idx[kItems];
-    unsigned short rank[kItems];
+    u32 key[kItems];
+    unsigned short slot[kItems];
     const u32 lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const u32 t = u32(warp) * kWarpSpan + u32(r) * 32 + lane;  // position in the tile
-        const bool valid = t < live;
-        key[r] = valid ? keys_in[base + t] : 0xffffffffu;
-        idx[r] = valid ? (idx_in != nullptr ? idx_in[base + t] : u32(base + t)) : 0u;
+        key[r] = t < live ? keys_in[base + t] : 0u;
     }
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
@@ -248,145 +314,248 @@ ord_scatter(const u32 *__restrict__ keys_in, const u32 *__restrict__ idx_in, u32
         const int leader = valid ? __ffs(peers) - 1 : lane;
         u32 before = 0;
         if (valid && lane == leader) {
-            before = s_cnt[warp][d];
-            s_cnt[warp][d] = before + (u32)__popc(peers);
+            before = s_cnt[warp * kRadix + d];
+            s_cnt[warp * kRadix + d] = before + (u32)__popc(peers);
         }
         before = __shfl_sync(KRN_FULL_MASK, before, leader);
-        rank[r] = (unsigned short)(before + (u32)__popc(peers & lt));
+        slot[r] = (unsigned short)(before + (u32)__popc(peers & lt));
         __syncwarp();  // the next round's leader of this digit may be another lane
     }
     __syncthreads();
 
-    // per digit: exclusive prefix over the warps, tile total, then an exclusive scan over the digits
-    const u32 d_me = threadIdx.x;  // kThreads >= kRadix
-    u32 total = 0;
-    if (d_me <= mask) {
+    // per digit: exclusive prefix over the warps and the tile total; then an exclusive scan over the digits
+    for (int d = threadIdx.x; d < kRadix; d += kThreads) {
+        u32 total = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            const u32 c = s_cnt[w][d_me];
-            s_cnt[w][d_me] = total;
+            const u32 c = s_cnt[w * kRadix + d];
+            s_cnt[w * kRadix + d] = total;
             total += c;
         }
-    }
-    u32 inc = total;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(KRN_FULL_MASK, inc, o);
-        if (lane >= o) inc += t;
-    }
-    if (lane == 31) s_wsum[warp] = inc;
-    __syncthreads();
-    u32 wbase = 0;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w)
-        if (w < warp) wbase += s_wsum[w];
-    if (d_me <= mask) {
-        const u32 first = wbase + inc - total;
-        s_first[d_me] = first;
-        s_dest[d_me] = table[size_t(d_me) * tiles + blockIdx.x];
+        s_tot[d] = total;
+        s_dest[d] = table[size_t(d) * tiles + blockIdx.x];
     }
     __syncthreads();
+    digit_scan(s_tot, s_first, kRadix, s_wsum);
 
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const u32 t = u32(warp) * kWarpSpan + u32(r) * 32 + lane;
         if (t < live) {
             const u32 d = (key[r] >> shift) & mask;
-            const u32 slot = s_first[d] + s_cnt[warp][d] + rank[r];
-            s_key[slot] = key[r];
-            s_idx[slot] = idx[r];
+            const u32 s = s_first[d] + s_cnt[warp * kRadix + d] + slot[r];
+            slot[r] = (unsigned short)s;
+            s_key[s] = key[r];
         }
     }
     __syncthreads();
+    // sorted slot s leaves the tile to s_g[s] (computed once, reused by every value plane)
     for (u32 s = threadIdx.x; s < live; s += kThreads) {
         const u32 k = s_key[s];
         const u32 d = (k >> shift) & mask;
-        const size_t g = size_t(s_dest[d]) + (s - s_first[d]);
+        const u32 g = s_dest[d] + (s - s_first[d]);
+        s_g[s] = g;
         keys_out[g] = k;
-        idx_out[g] = s_idx[s];
+    }
+    for (int w = 0; w < width; ++w) {
+        const double *__restrict__ src = vals_in + size_t(w) * m + base;
+        double *__restrict__ dst = vals_out + size_t(w) * m;
+#pragma unroll
+        for (int r = 0; r < kItems; ++r) {
+            const u32 t = u32(warp) * kWarpSpan + u32(r) * 32 + lane;
+            if (t < live) s_val[slot[r]] = src[t];
+        }
+        __syncthreads();
+        for (u32 s = threadIdx.x; s < live; s += kThreads) dst[s_g[s]] = s_val[s];
+        __syncthreads();
     }
 }
 
-// ---- fold --------------------------------------------------------------------------------------
-// One thread per sorted position; the thread at the head of a run of equal keys folds the run in
-// order, from the target's current value:  acc = target; acc += v(r0, 0); acc += v(r0, 1); ...
+// ---- bucket boundaries -----------------------------------------------------------------------
+// records are sorted by bucket id = (key >> lb) & hmask: first / one-past-last position per bucket
 __global__ void __launch_bounds__(kThreads)
-ord_fold(const u32 *__restrict__ keys, const u32 *__restrict__ idx, const double *__restrict__ vals, int width,
-         size_t m, double *target, u32 target_size, u32 *long_list, u32 *long_count)
+ord_mark(const u32 *__restrict__ keys, size_t m, int lb, u32 hmask, u32 *__restrict__ start, u32 *__restrict__ end)
 {
-    const size_t p = size_t(blockIdx.x) * kThreads + threadIdx.x;
+    // 4 consecutive records per thread (one 128-bit load; the buffers are 256-byte aligned)
+    const size_t p = (size_t(blockIdx.x) * kThreads + threadIdx.x) * 4;
     if (p >= m) return;
-    const u32 key = keys[p];
-    if (key >= target_size) return;  // a site that did not execute
-    if (p > 0 && keys[p - 1] == key) return;
-    double acc = target[key];
-    size_t q = p;
-    for (int step = 0; step < kLongAfter; ++step) {
-        const size_t r = idx[q];
-        for (int w = 0; w < width; ++w) acc = acc + vals[r * width + w];
-        ++q;
-        if (q >= m || keys[q] != key) {
-            target[key] = acc;
-            return;
-        }
+    u32 k[6];  // k[0] = predecessor of record p, k[5] = successor of record p + 3
+    if (p + 4 <= m) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(keys + p);
+        k[1] = q.x, k[2] = q.y, k[3] = q.z, k[4] = q.w;
+    } else {
+        for (int u = 0; u < 4; ++u) k[1 + u] = p + u < m ? keys[p + u] : 0u;
     }
-    long_list[atomicAdd(long_count, 1u)] = u32(p);  // restarted from the beginning by a block
+    k[0] = p > 0 ? keys[p - 1] : 0u;
+    k[5] = p + 4 < m ? keys[p + 4] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (p + u >= m) break;
+        const u32 b = (k[1 + u] >> lb) & hmask;
+        if (p + u == 0 || ((k[u] >> lb) & hmask) != b) start[b] = u32(p + u);
+        if (p + u + 1 == m || ((k[2 + u] >> lb) & hmask) != b) end[b] = u32(p + u + 1);
+    }
 }
 
-// Long runs: the block stages kLongChunk records per round in shared memory - the loads of the
-// next round are in flight while thread 0 adds the current one - and thread 0 performs the fold.
-__global__ void __launch_bounds__(kThreads)
-ord_fold_long(const u32 *__restrict__ keys, const u32 *__restrict__ idx, const double *__restrict__ vals, int width,
-              size_t m, double *target, const u32 *__restrict__ long_list, const u32 *__restrict__ long_count)
+// ---- phase B: one block per bucket ---------------------------------------------------------
+// Stable ranking pass over the packed words in[0, cnt) by `bits` bits at `shift`, inside shared
+// memory (same scheme as the tile scatter: a warp owns kChunkSpan consecutive words).
+__device__ __forceinline__ void local_pass(const u32 *in, u32 *out, int cnt, int shift, int bits, u32 *s_cnt,
+                                           u32 *s_tot, u32 *s_first, u32 *s_wsum)
 {
-    __shared__ double s_v[kLongChunk * kMaxWidth];
-    constexpr int kPer = kLongChunk / kThreads;
-    const u32 runs = *long_count;
-    for (u32 s = blockIdx.x; s < runs; s += gridDim.x) {
-        const size_t p = long_list[s];
-        const u32 key = keys[p];
-        double acc = threadIdx.x == 0 ? target[key] : 0.0;
-        double v[kPer][kMaxWidth];
-        bool same[kPer];
-        size_t q0 = p;
-        auto fetch = [&](size_t from) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int radix = 1 << bits;
+    const u32 mask = u32(radix) - 1u, lt = lanemask_lt();
+    for (int k = threadIdx.x; k < kWarps * radix; k += kThreads) s_cnt[k] = 0;
+    __syncthreads();
+    constexpr int kRounds = kChunkSpan / 32;
+    u32 word[kRounds];
+    unsigned short rank[kRounds];
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                const size_t q = from + threadIdx.x + size_t(j) * kThreads;
-                same[j] = q < m && keys[q] == key;
-                if (same[j]) {
-                    const size_t r = idx[q];
-#pragma unroll
-                    for (int w = 0; w < kMaxWidth; ++w)
-                        if (w < width) v[j][w] = vals[r * width + w];
-                }
-            }
-        };
-        fetch(q0);
-        for (;;) {
-            int count = 0;
-#pragma unroll
-            for (int j = 0; j < kPer; ++j) {
-                if (same[j]) {
-#pragma unroll
-                    for (int w = 0; w < kMaxWidth; ++w)
-                        if (w < width) s_v[(threadIdx.x + j * kThreads) * width + w] = v[j][w];
-                }
-                count += __syncthreads_count(same[j]);
-            }
-            q0 += kLongChunk;
-            const bool more = count == kLongChunk && q0 < m;  // sorted keys: the run is a prefix of the chunk
-            if (more) fetch(q0);
-            if (threadIdx.x == 0) {
-                const int terms = count * width;
-#pragma unroll 8
-                for (int k = 0; k < terms; ++k) acc = acc + s_v[k];
-            }
-            __syncthreads();
-            if (!more) break;
+    for (int r = 0; r < kRounds; ++r) {
+        const int q = warp * kChunkSpan + r * 32 + lane;
+        const bool valid = q < cnt;
+        word[r] = valid ? in[q] : 0u;
+        const u32 d = (word[r] >> shift) & mask;
+        const u32 peers = same_digit_lanes_rt(d, valid, bits);
+        const int leader = valid ? __ffs(peers) - 1 : lane;
+        u32 before = 0;
+        if (valid && lane == leader) {
+            before = s_cnt[warp * radix + d];
+            s_cnt[warp * radix + d] = before + (u32)__popc(peers);
         }
-        if (threadIdx.x == 0) target[key] = acc;
+        before = __shfl_sync(KRN_FULL_MASK, before, leader);
+        rank[r] = (unsigned short)(before + (u32)__popc(peers & lt));
+        __syncwarp();
     }
+    __syncthreads();
+    for (int d = threadIdx.x; d < radix; d += kThreads) {
+        u32 total = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const u32 c = s_cnt[w * radix + d];
+            s_cnt[w * radix + d] = total;
+            total += c;
+        }
+        s_tot[d] = total;
+    }
+    __syncthreads();
+    digit_scan(s_tot, s_first, radix, s_wsum);
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int q = warp * kChunkSpan + r * 32 + lane;
+        if (q < cnt) {
+            const u32 d = (word[r] >> shift) & mask;
+            out[s_first[d] + s_cnt[warp * radix + d] + rank[r]] = word[r];
+        }
+    }
+    __syncthreads();
+}
+
+// Bucket b owns targets [b << lb, (b + 1) << lb) and the records [start[b], end[b]) (all of them
+// valid: the all-ones mark of a site that did not execute lies in a bucket of its own beyond the
+// last target).  Dynamic shared memory: tile[1 << lb] doubles, vals[width][kChunk] doubles,
+// two word arrays [kChunk], ranking counters.
+template <int WIDTH>
+__global__ void __launch_bounds__(kThreads)
+ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, size_t m,
+                double *__restrict__ target, size_t target_size, int lb, const u32 *__restrict__ start,
+                const u32 *__restrict__ end)
+{
+    constexpr int width = WIDTH;
+    const u32 b = blockIdx.x;
+    const u32 s0 = start[b];
+    if (s0 == kNone) return;
+    const size_t t0 = size_t(b) << lb;
+    if (t0 >= target_size) return;  // sites that did not execute
+    const u32 e0 = end[b];
+    const int tn = int(target_size - t0 < (size_t(1) << lb) ? target_size - t0 : (size_t(1) << lb));
+
+    extern __shared__ __align__(16) unsigned char ord_smem[];
+    double *tile = reinterpret_cast<double *>(ord_smem);   // [1 << lb]
+    double *cv = tile + (size_t(1) << lb);                   // [width][kChunk]
+    u32 *wa = reinterpret_cast<u32 *>(cv + size_t(width) * kChunk);  // [kChunk]
+    u32 *wb = wa + kChunk;                                   // [kChunk]
+    u32 *s_cnt = wb + kChunk;                                // [kWarps][1 << kLocalPassBits]
+    u32 *s_tot = s_cnt + (kWarps << kLocalPassBits);         // [1 << kLocalPassBits]
+    u32 *s_first = s_tot + (1 << kLocalPassBits);            // [1 << kLocalPassBits]
+    __shared__ u32 s_wsum[kWarps];
+
+    for (int k = threadIdx.x; k < tn; k += kThreads) tile[k] = target[t0 + k];
+    const int passes = (lb + kLocalPassBits - 1) / kLocalPassBits;
+    const int pbits = passes ? (lb + passes - 1) / passes : 0;
+    for (u32 c = s0; c < e0; c += kChunk) {
+        const int cnt = int(e0 - c < u32(kChunk) ? e0 - c : u32(kChunk));
+        __syncthreads();  // the previous chunk's fold is done with wa/wb/cv (and the tile is loaded)
+        for (int q = threadIdx.x; q < cnt; q += kThreads) {
+            u32 kl = keys[c + q] - u32(t0);
+            if (kl >= u32(tn)) kl = u32(tn) - 1u;  // cannot happen for keys < target_size: never leave the tile
+            wa[q] = (kl << kSlotBits) | u32(q);
+#pragma unroll
+            for (int w = 0; w < width; ++w) cv[w * kChunk + q] = vals[size_t(w) * m + c + q];
+        }
+        __syncthreads();
+        const u32 *fin = wa;
+        if (passes >= 1) {
+            local_pass(wa, wb, cnt, kSlotBits, pbits, s_cnt, s_tot, s_first, s_wsum);
+            fin = wb;
+        }
+        if (passes >= 2) {
+            local_pass(wb, wa, cnt, kSlotBits + pbits, pbits, s_cnt, s_tot, s_first, s_wsum);
+            fin = wa;
+        }
+        // fold: the thread at the head of a run of equal keys adds the run, in order
+        for (int q = threadIdx.x; q < cnt; q += kThreads) {
+            const u32 k = fin[q] >> kSlotBits;
+            if (q > 0 && (fin[q - 1] >> kSlotBits) == k) continue;
+            double acc = tile[k];
+            int j = q;
+            // long runs (a hot location): the chain of dependent additions is the definition of the
+            // result; the words and values of the NEXT 8 records are fetched while the current 8 are added
+            if (width == 1) {
+                double v[8];
+                bool have = j + 8 <= cnt && (fin[j + 7] >> kSlotBits) == k;
+                if (have) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = cv[fin[j + u] & u32(kChunk - 1)];
+                }
+                while (have) {
+                    const int jn = j + 8;
+                    const bool have_n = jn + 8 <= cnt && (fin[jn + 7] >> kSlotBits) == k;
+                    double vn[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) vn[u] = have_n ? cv[fin[jn + u] & u32(kChunk - 1)] : 0.0;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = acc + v[u];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = vn[u];
+                    j = jn;
+                    have = have_n;
+                }
+            } else {
+                while (j + 8 <= cnt && (fin[j + 7] >> kSlotBits) == k) {
+                    u32 sl[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) sl[u] = fin[j + u] & u32(kChunk - 1);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+                        for (int w = 0; w < width; ++w) acc = acc + cv[w * kChunk + sl[u]];
+                    }
+                    j += 8;
+                }
+            }
+            while (j < cnt && (fin[j] >> kSlotBits) == k) {
+                const u32 sl = fin[j] & u32(kChunk - 1);
+#pragma unroll
+                for (int w = 0; w < width; ++w) acc = acc + cv[w * kChunk + sl];
+                ++j;
+            }
+            tile[k] = acc;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < tn; k += kThreads) target[t0 + k] = tile[k];
 }
 
 #define KRN_BITS_SWITCH(bits, CALL) \
@@ -398,7 +567,9 @@ ord_fold_long(const u32 *__restrict__ keys, const u32 *__restrict__ idx, const d
     case 5: CALL(5); break;         \
     case 6: CALL(6); break;         \
     case 7: CALL(7); break;         \
-    default: CALL(8); break;        \
+    case 8: CALL(8); break;         \
+    case 9: CALL(9); break;         \
+    default: CALL(10); break;       \
     }
 
 void launch_hist(int bits, unsigned tiles, cudaStream_t st, const u32 *keys, size_t m, int shift, u32 ntiles, u32 *table)
@@ -408,12 +579,26 @@ void launch_hist(int bits, unsigned tiles, cudaStream_t st, const u32 *keys, siz
 #undef KRN_CALL
 }
 
-void launch_scatter(int bits, unsigned tiles, cudaStream_t st, const u32 *keys_in, const u32 *idx_in, u32 *keys_out,
-                    u32 *idx_out, const u32 *table, size_t m, int shift, u32 ntiles)
+size_t scatter_smem(int bits)
 {
-#define KRN_CALL(B) ord_scatter<B><<<tiles, kThreads, 0, st>>>(keys_in, idx_in, keys_out, idx_out, table, m, shift, ntiles)
+    return size_t(kTile) * 16 + (size_t(kWarps + 3) << bits) * 4;
+}
+
+cudaError_t launch_scatter(int bits, unsigned tiles, cudaStream_t st, const u32 *keys_in, const double *vals_in,
+                           u32 *keys_out, double *vals_out, const u32 *table, size_t m, int shift, u32 ntiles, int width)
+{
+    const size_t smem = scatter_smem(bits);
+    cudaError_t e = cudaSuccess;
+#define KRN_CALL(B)                                                                                              \
+    do {                                                                                                         \
+        e = cudaFuncSetAttribute(ord_scatter<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
+        if (e == cudaSuccess)                                                                                    \
+            ord_scatter<B><<<tiles, kThreads, smem, st>>>(keys_in, vals_in, keys_out, vals_out, table, m, shift, \
+                                                          ntiles, width);                                        \
+    } while (0)
     KRN_BITS_SWITCH(bits, KRN_CALL)
 #undef KRN_CALL
+    return e;
 }
 
 inline int bit_length(size_t x)
@@ -444,47 +629,63 @@ extern "C" int krn_ordered_accumulate(krn_ctx *ctx, double *d_target, size_t tar
     KRN_REQUIRE(width >= 1 && width <= kMaxWidth, "width must be 1..4");
     if (records == 0 || target_size == 0) return KRN_OK;
     KRN_REQUIRE(d_target && d_keys && d_vals, "null pointer");
-    KRN_REQUIRE(target_size < 0xffffffffull, "target too large for 32-bit keys");
+    KRN_REQUIRE(target_size <= 0x80000000ull, "target too large (at most 2^31 elements)");
     KRN_REQUIRE(records < 0xffffffffull, "too many records for 32-bit record numbers");
 
-    // keys 0..target_size-1 and the all-ones mark of a site that did not execute must stay apart
-    // in the bits that are sorted: bit_length(target_size) bits, split evenly over the passes
-    const int nbits = bit_length(target_size);
-    const int passes = (nbits + 7) / 8;
-    const int bits = (nbits + passes - 1) / passes;
-    const u32 mask = (1u << bits) - 1u;
+    // Buckets of 2^lb targets; `high` bits above them are sorted in HBM.  At least 2^10 buckets when
+    // the target is large enough (one block per bucket must fill the machine); the all-ones key of a
+    // site that did not execute must fall into a bucket beyond the last real one.
+    const int nbits = bit_length(target_size - 1);  // bits of the largest real key
+    int lb = nbits - kMaxPassBits;
+    if (lb < 0) lb = 0;
+    if (lb > kMaxLocalBits) lb = kMaxLocalBits;
+    int high = nbits - lb;
+    if (high < 1) high = 1;
+    while (((size_t(1) << high) - 1) <= ((target_size - 1) >> lb)) ++high;
+    const int passes = (high + kMaxPassBits - 1) / kMaxPassBits;
+    const int bits = (high + passes - 1) / passes;
+    const size_t buckets = size_t(1) << (bits * passes);  // bucket ids the passes can produce
+    const u32 hmask = u32(buckets - 1);
     const size_t tiles = (records + kTile - 1) / kTile;
-    const size_t table_len = (size_t(mask) + 1) * tiles;
+    const size_t table_len = (size_t(1) << bits) * tiles;
     const size_t sums_len = (table_len + kScanChunk - 1) / kScanChunk;
-    const size_t long_cap = records / kLongAfter + 1;
 
     auto round256 = [](size_t b) { return (b + 255) / 256 * 256; };
-    const size_t rec_bytes = round256(records * sizeof(u32));
-    const size_t total = 4 * rec_bytes + round256(table_len * 4) + round256(sums_len * 4) + round256(long_cap * 4) + 256;
+    const size_t key_bytes = round256(records * sizeof(u32));
+    const size_t val_bytes = round256(records * size_t(width) * sizeof(double));
+    const int nbuf = passes > 1 ? 2 : 1;
+    const size_t total = nbuf * (key_bytes + val_bytes) + round256(table_len * 4) + round256(sums_len * 4) +
+                         2 * round256(buckets * 4);
     char *ws = nullptr;
     KRN_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws), total, ctx->stream));
-    u32 *key_buf[2] = {reinterpret_cast<u32 *>(ws), reinterpret_cast<u32 *>(ws + rec_bytes)};
-    u32 *idx_buf[2] = {reinterpret_cast<u32 *>(ws + 2 * rec_bytes), reinterpret_cast<u32 *>(ws + 3 * rec_bytes)};
-    char *cursor = ws + 4 * rec_bytes;
+    char *cursor = ws;
+    u32 *key_buf[2] = {nullptr, nullptr};
+    double *val_buf[2] = {nullptr, nullptr};
+    for (int k = 0; k < nbuf; ++k) {
+        key_buf[k] = reinterpret_cast<u32 *>(cursor);
+        cursor += key_bytes;
+        val_buf[k] = reinterpret_cast<double *>(cursor);
+        cursor += val_bytes;
+    }
     u32 *table = reinterpret_cast<u32 *>(cursor);
     cursor += round256(table_len * 4);
     u32 *sums = reinterpret_cast<u32 *>(cursor);
     cursor += round256(sums_len * 4);
-    u32 *long_list = reinterpret_cast<u32 *>(cursor);
-    cursor += round256(long_cap * 4);
-    u32 *long_count = reinterpret_cast<u32 *>(cursor);
+    u32 *start = reinterpret_cast<u32 *>(cursor);
+    cursor += round256(buckets * 4);
+    u32 *end = reinterpret_cast<u32 *>(cursor);
 
     int rc = KRN_OK;
     auto fail = [&](cudaError_t e, const char *what) {
         krn_set_error("%s failed: %s", what, cudaGetErrorString(e));
         rc = KRN_E_CUDA;
     };
-    const u32 *src_keys = d_keys;
-    const u32 *src_idx = nullptr;
-    cudaError_t e = cudaMemsetAsync(long_count, 0, sizeof(u32), ctx->stream);
+    cudaError_t e = cudaMemsetAsync(start, 0xFF, buckets * 4, ctx->stream);
     if (e != cudaSuccess) fail(e, "cudaMemsetAsync");
+    const u32 *src_keys = d_keys;
+    const double *src_vals = d_vals;
     for (int pass = 0; pass < passes && rc == KRN_OK; ++pass) {
-        const int shift = pass * bits;
+        const int shift = lb + pass * bits;
         launch_hist(bits, unsigned(tiles), ctx->stream, src_keys, records, shift, u32(tiles), table);
         ctx->launches++;
         if (table_len <= size_t(kScanChunk) * 32) {
@@ -496,22 +697,38 @@ extern "C" int krn_ordered_accumulate(krn_ctx *ctx, double *d_target, size_t tar
             scan_apply<<<unsigned(sums_len), kThreads, 0, ctx->stream>>>(table, table_len, sums);
             ctx->launches += 3;
         }
-        u32 *dst_keys = key_buf[pass & 1], *dst_idx = idx_buf[pass & 1];
-        launch_scatter(bits, unsigned(tiles), ctx->stream, src_keys, src_idx, dst_keys, dst_idx, table, records, shift,
-                       u32(tiles));
+        u32 *dst_keys = key_buf[pass & 1];
+        double *dst_vals = val_buf[pass & 1];
+        e = launch_scatter(bits, unsigned(tiles), ctx->stream, src_keys, src_vals, dst_keys, dst_vals, table, records,
+                           shift, u32(tiles), width);
         ctx->launches++;
         src_keys = dst_keys;
-        src_idx = dst_idx;
-        if ((e = cudaGetLastError()) != cudaSuccess) fail(e, "radix pass launch");
+        src_vals = dst_vals;
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) fail(e, "partition pass launch");
     }
     if (rc == KRN_OK) {
-        const size_t blocks = (records + kThreads - 1) / kThreads;
-        ord_fold<<<unsigned(blocks), kThreads, 0, ctx->stream>>>(src_keys, src_idx, d_vals, width, records, d_target,
-                                                                u32(target_size), long_list, long_count);
-        ord_fold_long<<<unsigned(ctx->sms * 2), kThreads, 0, ctx->stream>>>(src_keys, src_idx, d_vals, width, records,
-                                                                            d_target, long_list, long_count);
+        const size_t blocks = (records + 4 * kThreads - 1) / (4 * kThreads);
+        ord_mark<<<unsigned(blocks), kThreads, 0, ctx->stream>>>(src_keys, records, lb, hmask, start, end);
+        const size_t smem = (size_t(1) << lb) * 8 + size_t(width) * kChunk * 8 + 2 * size_t(kChunk) * 4 +
+                            (size_t(kWarps + 2) << kLocalPassBits) * 4;
+        // real buckets only: ids beyond the last target hold sites that did not execute
+        const size_t real = ((target_size - 1) >> lb) + 1;
+#define KRN_FOLD(W)                                                                                                  \
+    do {                                                                                                             \
+        e = cudaFuncSetAttribute(ord_bucket_fold<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
+        if (e == cudaSuccess)                                                                                        \
+            ord_bucket_fold<W><<<unsigned(real), kThreads, smem, ctx->stream>>>(src_keys, src_vals, records, d_target, \
+                                                                                target_size, lb, start, end);        \
+    } while (0)
+        switch (width) {
+        case 1: KRN_FOLD(1); break;
+        case 2: KRN_FOLD(2); break;
+        case 3: KRN_FOLD(3); break;
+        default: KRN_FOLD(4); break;
+        }
+#undef KRN_FOLD
         ctx->launches += 2;
-        if ((e = cudaGetLastError()) != cudaSuccess) fail(e, "fold launch");
+        if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) fail(e, "fold launch");
     }
     cudaFreeAsync(ws, ctx->stream);
     return rc;

@@ -562,7 +562,7 @@ SMEM_PRIVATE_MAX = 6144  # doubles: 48 KB of dynamic shared memory
 
 
 NO_ATOMICS = (0, 0, 0, 0, 0, 0)
-ORDERED_LIMIT = 0xFFFFFFFF - 1  # 32-bit keys and record numbers (krn_ordered_accumulate)
+ORDERED_LIMIT = 1 << 31  # 32-bit keys and record numbers (krn_ordered_accumulate)
 
 
 class OrderedStage:
@@ -580,7 +580,7 @@ class OrderedStage:
 
     @staticmethod
     def feasible(entries, views: dict, n: int) -> bool:
-        return all(views[e["view"]].size < ORDERED_LIMIT and n * e["groups"] < ORDERED_LIMIT for e in entries)
+        return all(views[e["view"]].size <= ORDERED_LIMIT and n * e["groups"] < ORDERED_LIMIT for e in entries)
 
     def apply(self):
         dev, n = self.dev, self.n
@@ -602,7 +602,7 @@ def atomic_choice(dev, cfg, recipe, views, builder, n, static_smem: int = 0):
             stage = OrderedStage(dev, entries, views, n)
             return (0, 4, 0, stage.keys.ptr, stage.vals.ptr, n), stage
         if want == "ordered":
-            raise ValueError("atomic_policy='ordered' needs targets and queues of fewer than 2^32 - 2 entries")
+            raise ValueError("atomic_policy='ordered' needs targets and queues of at most 2^31 entries")
     if want in ("ordered", "auto") and cfg.deterministic_reduction and entries:
         want = "lead"  # targets beyond 32-bit keys: hardware reductions, exact up to reassociation
     atomic_views = recipe.get("atomic_views") or []

@@ -24,7 +24,8 @@ def _accumulate(target, keys, vals, width):
     lib = dev.lib
     t = np.ascontiguousarray(target, dtype=np.float64).copy()
     k = np.ascontiguousarray(keys, dtype=np.uint32)
-    v = np.ascontiguousarray(vals, dtype=np.float64).reshape(-1)
+    # the oracle takes record-major values (r * width + w), the library takes planes (w * records + r)
+    v = np.ascontiguousarray(np.asarray(vals, dtype=np.float64).reshape(-1, width).T).reshape(-1)
     bufs = []
     for a in (t, k, v):
         p = dev.alloc(max(a.nbytes, 8))

@@ -1,7 +1,7 @@
 """Device time of krn_ordered_accumulate (csrc/krn_ordered.cu) alone, through the raw C ABI:
 records already staged in HBM, CUDA events around the call, across queue lengths, target sizes
 and key distributions; achieved GB/s over the ALGORITHMIC bytes of the call:
-per record 4 B key + 8*width B values read, per distinct target 16 B read-modify-write.
+per record 4 B key + 8*width B values (planes) read, per distinct target 16 B read-modify-write.
 
     python tools/ordered_bench.py [--records 16777216] [--json out.json] [--only rows:map]
 """
