@@ -255,6 +255,10 @@ def main():
     x_out = torch.empty_like(x)
     f = torch.zeros(1, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
+    # N > 1: the ranks map each other's x and b once (CUDA IPC: peer memory over NVLink); the boundary
+    # steps of the kernels read their halo rows through those pointers, so a gradient step is one launch
+    # and no collective (x and b stay as they are between steps: no fence inside the timed region)
+    shard.attach(x, b)
 
     def barrier():
         if dist is not None:

@@ -173,6 +173,33 @@ size_t krn_laplacian_partial_span(size_t n_global);
  * bit-identical to the single-device (and the reference's) result for any number of shards. */
 int krn_laplacian_partials(krn_ctx *ctx, double *d_out, size_t count);
 
+/* ---- sharded mode without per-step collectives: peer memory ---------------------------
+ * (the reference has no counterpart: its thread pool shares one address space,
+ * runtime.py:594-613.)  A rank exports the device allocations holding its x and b once
+ * (krn_ipc_export: the 64-byte CUDA IPC handle of the allocation containing d_ptr and d_ptr's
+ * offset inside it), hands the 72 bytes to its neighbours by any means (one all_gather at set-up),
+ * and each neighbour maps it (krn_ipc_open: peer access over NVLink is enabled by the mapping;
+ * two processes on one device work too).  The *_peers kernels then read their halo rows straight
+ * from the neighbours' buffers:
+ *   d_x_prev_end / d_b_prev_end  one past the LAST row of the previous shard's x / b
+ *                                (NULL when offset == 0)
+ *   d_x_next / d_b_next          the FIRST row of the next shard's x / b
+ *                                (NULL when offset + n_local == n_global)
+ * A gradient step is then exactly one launch and no collective.  The caller fences (a barrier
+ * across the ranks) only when a neighbour has rewritten the rows being read. */
+int krn_ipc_export(krn_ctx *ctx, const void *d_ptr, unsigned char handle[64], size_t *offset);
+int krn_ipc_open(krn_ctx *ctx, const unsigned char handle[64], size_t offset, void **d_base, void **d_ptr);
+int krn_ipc_close(krn_ctx *ctx, void *d_base);   /* synchronous */
+int krn_laplacian_primal_peers(krn_ctx *ctx, const double *d_x_in, double *d_x_out, const double *d_b,
+                               size_t n_local, size_t offset, size_t n_global,
+                               const double *d_x_prev_end, const double *d_b_prev_end,
+                               const double *d_x_next, const double *d_b_next, double *d_f, int accumulate);
+int krn_laplacian_grad_peers(krn_ctx *ctx, const double *d_x_in, double *d_x_out, const double *d_b,
+                             double *d_dx, double *d_db, int dx_zero, int db_zero, size_t n_local,
+                             size_t offset, size_t n_global, const double *d_x_prev_end,
+                             const double *d_b_prev_end, const double *d_x_next, const double *d_b_next,
+                             double seed);
+
 /* ---- generated kernels (parallel_for bodies compiled from the program tree;
  *      replaces _Compiler/_Interpreter.parallel_for, runtime.py:230-447, 567-624)
  * `cuda_source` is CUDA C++ for sm_100a; it may #include "krn_prelude.cuh"

@@ -70,6 +70,11 @@ SIGNATURES = {
     "krn_laplacian_grad": (_i, [_vp, _dp, _dp, _dp, _dp, _dp, _i, _i, _sz, _sz, _sz, _dp, _d]),
     "krn_laplacian_partial_span": (_sz, [_sz]),
     "krn_laplacian_partials": (_i, [_vp, _dp, _sz]),
+    "krn_ipc_export": (_i, [_vp, _vp, _vp, C.POINTER(C.c_size_t)]),
+    "krn_ipc_open": (_i, [_vp, _vp, _sz, _pp, _pp]),
+    "krn_ipc_close": (_i, [_vp, _vp]),
+    "krn_laplacian_primal_peers": (_i, [_vp, _dp, _dp, _dp, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _i]),
+    "krn_laplacian_grad_peers": (_i, [_vp, _dp, _dp, _dp, _dp, _dp, _i, _i, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _d]),
     "krn_module_compile": (_i, [_vp, C.c_char_p, _pp]),
     "krn_module_destroy": (_i, [_vp]),
     "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),

@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 LIB = os.path.join(PKG, "libkrn_b200.so")
-SOURCES = ["krn_context.cu", "krn_builtins.cu", "krn_laplacian.cu", "krn_jit.cu", "krn_ordered.cu"]
+SOURCES = ["krn_context.cu", "krn_builtins.cu", "krn_laplacian.cu", "krn_jit.cu", "krn_ordered.cu", "krn_peer.cu"]
 HEADERS = ["krn_common.cuh", "krn_prelude.cuh", os.path.join("..", "..", "include", "krn_b200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -46,6 +46,10 @@ struct Shard {
     const double *x;     // original x, local rows
     const double *b;
     const double *halo;  // x[-2], x[-1], b[-1], x[n], x[n+1], b[n] (local indexing) or null
+    // neighbour shards addressed directly (their own buffers, mapped into this process: peer memory
+    // over NVLink, or the same device): xp[-1] / bp[-1] is the previous shard's last row, xn[0] / bn[0]
+    // the next shard's first row.  Null: the halo array is used instead.
+    const double *xp, *bp, *xn, *bn;
     krn_i64 n_local;
     krn_i64 offset;
     krn_i64 n_global;
@@ -54,14 +58,14 @@ struct Shard {
 // original x / b at local row i in [-2, n_local + 2); caller guarantees the global row exists
 __device__ __forceinline__ double x_at(const Shard &s, krn_i64 i)
 {
-    if (i < 0) return s.halo[2 + i];
-    if (i >= s.n_local) return s.halo[3 + (i - s.n_local)];
+    if (i < 0) return s.xp ? s.xp[i] : s.halo[2 + i];
+    if (i >= s.n_local) return s.xn ? s.xn[i - s.n_local] : s.halo[3 + (i - s.n_local)];
     return krn_ld1(s.x + i);
 }
 __device__ __forceinline__ double b_at(const Shard &s, krn_i64 i)
 {
-    if (i < 0) return s.halo[2];
-    if (i >= s.n_local) return s.halo[5];
+    if (i < 0) return s.bp ? s.bp[i] : s.halo[2];
+    if (i >= s.n_local) return s.bn ? s.bn[i - s.n_local] : s.halo[5];
     return krn_ld1(s.b + i);
 }
 
@@ -410,14 +414,15 @@ void dispatch(krn_ctx *ctx, dim3 grid, const Shard &s, double *x_out, double *dx
 template <bool GRAD>
 int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, double *dx, double *db,
            int dx_zero, int db_zero, size_t n_local, size_t offset, size_t n_global, const double *halo,
-           double seed, double *f, int accumulate)
+           double seed, double *f, int accumulate, const double *xp = nullptr, const double *bp = nullptr,
+           const double *xn = nullptr, const double *bn = nullptr)
 {
     KRN_REQUIRE(ctx != nullptr, "null context");
     KRN_REQUIRE(x_in && x_out && b, "null view pointer");
     KRN_REQUIRE(x_in != x_out, "x_out must not alias x_in");
     KRN_REQUIRE(offset + n_local <= n_global, "shard exceeds the problem");
-    KRN_REQUIRE(halo != nullptr || (offset == 0 && n_local == n_global),
-                "a shard that is not the whole problem needs halo rows");
+    KRN_REQUIRE(halo != nullptr || ((offset == 0 || (xp && bp)) && (offset + n_local == n_global || (xn && bn))),
+                "a shard that is not the whole problem needs halo rows or its neighbours' buffers");
     KRN_REQUIRE(n_global < (size_t(1) << 62), "problem too large");
     if (!GRAD) KRN_REQUIRE(f != nullptr, "null result pointer");
     if (n_local == 0) {
@@ -432,7 +437,7 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
         int rc = krn_reserve_partials(ctx, blocks);
         if (rc) return rc;
     }
-    Shard s{x_in, b, halo, (krn_i64)n_local, (krn_i64)offset, (krn_i64)n_global};
+    Shard s{x_in, b, halo, xp, bp, xn, bn, (krn_i64)n_local, (krn_i64)offset, (krn_i64)n_global};
     bool vec = krn_aligned32(x_in) && krn_aligned32(x_out) && krn_aligned32(b) &&
                (dx == nullptr || krn_aligned32(dx)) && (db == nullptr || krn_aligned32(db));
     dim3 grid((unsigned)blocks);
@@ -465,6 +470,26 @@ extern "C" int krn_laplacian_grad(krn_ctx *ctx, const double *d_x_in, double *d_
 {
     return launch<true>(ctx, d_x_in, d_x_out, d_b, d_dx, d_db, dx_zero, db_zero, n_local, offset,
                         n_global, d_halo, seed, nullptr, 0);
+}
+
+extern "C" int krn_laplacian_primal_peers(krn_ctx *ctx, const double *d_x_in, double *d_x_out, const double *d_b,
+                                          size_t n_local, size_t offset, size_t n_global,
+                                          const double *d_x_prev_end, const double *d_b_prev_end,
+                                          const double *d_x_next, const double *d_b_next, double *d_f,
+                                          int accumulate)
+{
+    return launch<false>(ctx, d_x_in, d_x_out, d_b, nullptr, nullptr, 0, 0, n_local, offset, n_global, nullptr,
+                         1.0, d_f, accumulate, d_x_prev_end, d_b_prev_end, d_x_next, d_b_next);
+}
+
+extern "C" int krn_laplacian_grad_peers(krn_ctx *ctx, const double *d_x_in, double *d_x_out, const double *d_b,
+                                        double *d_dx, double *d_db, int dx_zero, int db_zero, size_t n_local,
+                                        size_t offset, size_t n_global, const double *d_x_prev_end,
+                                        const double *d_b_prev_end, const double *d_x_next,
+                                        const double *d_b_next, double seed)
+{
+    return launch<true>(ctx, d_x_in, d_x_out, d_b, d_dx, d_db, dx_zero, db_zero, n_local, offset, n_global,
+                        nullptr, seed, nullptr, 0, d_x_prev_end, d_b_prev_end, d_x_next, d_b_next);
 }
 
 extern "C" int krn_laplacian_partials(krn_ctx *ctx, double *d_out, size_t count)

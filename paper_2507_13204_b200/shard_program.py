@@ -391,9 +391,46 @@ def _edge_rows(v, start: int, count: int) -> np.ndarray:
     return np.array(v.peek()[start:start + count])
 
 
+def _put_rows(dev, dst_ptr: int, rows) -> None:
+    """ghost rows into an extended View: device to device when they arrived as a CUDA tensor (the
+    all-gather's output), from the host otherwise"""
+    if hasattr(rows, "data_ptr"):
+        dev.copy(dst_ptr, rows.data_ptr(), rows.numel())
+    else:
+        dev.upload(dst_ptr, np.ascontiguousarray(rows))
+
+
+def _streams(dev):
+    """(torch's current stream, the library context's stream as a torch stream) or (None, None)
+    when they are one and the same timeline"""
+    import ctypes as C
+
+    import torch
+
+    cur = torch.cuda.current_stream(dev.ordinal)
+    sp = C.c_void_p()
+    dev.lib.krn_ctx_stream(dev.h, C.byref(sp))
+    if (sp.value or 0) == cur.cuda_stream:
+        return None, None
+    return cur, torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", dev.ordinal))
+
+
+def torch_after_library(dev) -> None:
+    cur, ext = _streams(dev)
+    if ext is not None:
+        cur.wait_stream(ext)
+
+
+def library_after_torch(dev) -> None:
+    cur, ext = _streams(dev)
+    if ext is not None:
+        ext.wait_stream(cur)
+
+
 def _extended_on_device(v, below, above):
     """A new View = [ghost rows from below | v | ghost rows from above], assembled in HBM: the own
-    rows are copied device to device, only the few ghost rows travel from the host."""
+    rows are copied device to device, and so are the ghost rows when the exchange delivered them
+    as device tensors (TorchComm.exchange_rows_device)."""
     from .runtime import Device, ViewStorage, _DeviceBuffer
 
     dev = v._dev.dev if (v._dev is not None and v._dev_ok) else Device.get()
@@ -404,10 +441,10 @@ def _extended_on_device(v, below, above):
     ext = ViewStorage._blank(v.name, (rows,) + tuple(v.extents[1:]))
     ext._dev = _DeviceBuffer(dev, 8 * rows * cols)
     if glo:
-        dev.upload(ext._dev.ptr, np.ascontiguousarray(below))
+        _put_rows(dev, ext._dev.ptr, below)
     dev.copy(ext._dev.ptr + 8 * glo * cols, v.device_ptr(dev, write=False), v.size)
     if ghi:
-        dev.upload(ext._dev.ptr + 8 * (glo + v.extents[0]) * cols, np.ascontiguousarray(above))
+        _put_rows(dev, ext._dev.ptr + 8 * (glo + v.extents[0]) * cols, above)
     ext._dev_ok, ext._host_ok, ext._zero = True, False, False
     return ext
 
@@ -454,6 +491,27 @@ class TorchComm:
         above = everyone[self.rank + 1, 0] if self.rank < self.world - 1 else None
         return below, above
 
+    def exchange_rows_device(self, view, dev, ghost: int):
+        """Device-resident twin of exchange_rows: the first / last `ghost` rows of `view` are
+        sliced out of its HBM buffer (a torch tensor aliasing it), all-gathered on the device
+        (NCCL over NVLink; gloo moves CUDA tensors too) and returned as CUDA tensors - nothing
+        passes through the host.  Stream order: torch's stream waits for the library's before the
+        slices are read; the caller lets the library wait for torch before it copies the rows."""
+        if self.world == 1:
+            return None, None
+        import torch
+
+        t = device_tensor(view, dev, write=False).reshape(view.extents[0], -1)
+        torch_after_library(dev)
+        rows = t.shape[0]
+        mine = torch.cat([t[:ghost].reshape(-1), t[rows - ghost:].reshape(-1)])
+        everyone = torch.empty(self.world * mine.numel(), dtype=mine.dtype, device=mine.device)
+        self.dist.all_gather_into_tensor(everyone, mine, group=self.group)
+        everyone = everyone.view(self.world, 2, -1)
+        below = everyone[self.rank - 1, 1] if self.rank > 0 else None
+        above = everyone[self.rank + 1, 0] if self.rank < self.world - 1 else None
+        return below, above
+
     def allreduce_array(self, arr: np.ndarray) -> None:
         """In-place sum of a replicated View's copies, given as a host array (gloo)."""
         if self.world == 1:
@@ -475,17 +533,15 @@ class TorchComm:
         if self.world == 1:
             return
         if self.dist.get_backend(self.group) == "nccl":
-            import torch
-
             dev = view._dev.dev if (view._dev is not None and view._dev_ok) else None
             if dev is None:
                 from .runtime import Device
 
                 dev = Device.get()
             t = device_tensor(view, dev)
-            dev.sync()  # the library's stream and torch's are different timelines
+            torch_after_library(dev)  # the library's stream and torch's are different timelines:
             self.dist.all_reduce(t, group=self.group)
-            torch.cuda.synchronize()
+            library_after_torch(dev)  # ordered by events, no host synchronisation
         else:
             self.allreduce_array(view.buffer)
 
@@ -498,12 +554,12 @@ class _CudaArray:
                                          "version": 3, "strides": None}
 
 
-def device_tensor(view, dev):
-    """A torch CUDA tensor that ALIASES the View's device buffer (no copy); the View's host copy is
-    marked stale because the tensor may be written through."""
+def device_tensor(view, dev, write: bool = True):
+    """A torch CUDA tensor that ALIASES the View's device buffer (no copy); with `write` the View's
+    host copy is marked stale because the tensor may be written through."""
     import torch
 
-    ptr = view.device_ptr(dev, write=True)
+    ptr = view.device_ptr(dev, write=write)
     return torch.as_tensor(_CudaArray(ptr, view.extents), device=torch.device("cuda", dev.ordinal))
 
 
@@ -616,16 +672,31 @@ class ShardedProgram:
             if own < G:
                 raise NotShardable(f"a rank needs at least {G} rows of its own, got {own}")
             on_device = _execute_override is None
+            resident = on_device and hasattr(self.comm, "exchange_rows_device")
+            if resident:
+                from .runtime import Device
+
+                dev = Device.get(cfg.device)
+            keep = []  # gathered tensors stay alive until the library's copies of their rows are ordered
             for name in sharded:
                 v = views[name]
-                first, last = (_edge_rows(v, 0, G), _edge_rows(v, own - G, G)) if on_device else \
-                    (v.buffer[:G].copy(), v.buffer[own - G:].copy())
-                below, above = self.comm.exchange_rows(first, last)
+                if resident:
+                    # edge rows sliced, gathered and copied inside HBM
+                    below, above = self.comm.exchange_rows_device(v, dev, G)
+                    keep.append((below, above))
+                    library_after_torch(dev)
+                else:
+                    first, last = (_edge_rows(v, 0, G), _edge_rows(v, own - G, G)) if on_device else \
+                        (v.buffer[:G].copy(), v.buffer[own - G:].copy())
+                    below, above = self.comm.exchange_rows(first, last)
                 glo, ghi = (G if below is not None else 0), (G if above is not None else 0)
                 originals[name] = v
                 views[name] = _extended_on_device(v, below, above) if on_device else ViewStorage.from_values(
                     name, np.concatenate(([below] if below is not None else []) + [v.buffer] +
                                          ([above] if above is not None else [])))
+            if resident and keep:
+                torch_after_library(dev)  # torch may recycle the gathered buffers only after the copies
+                del keep
         programs = self._build(glo, own, ghi)
 
         # scatter targets are replicated: rank 0 keeps the caller's values, the others start from zero,

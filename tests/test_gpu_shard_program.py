@@ -112,6 +112,63 @@ def test_two_processes_over_gloo():
     assert_bits(np.concatenate([got[0][2], got[1][2]]), want["v"], "v")
 
 
+def _ghost_worker(rank, world, port, n, out):
+    """the headline gradient (ghost rows: 2 either side) through ShardedProgram with the default
+    torch.distributed comm: the edge rows are sliced, all-gathered and copied INSIDE device memory"""
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_13204_b200.sharded import partition
+
+        torch.cuda.set_device(0)
+        prog = krn.load_program("laplacian")
+        gp = krn.differentiate(prog, "normRes1DLaplacianSQ", ("x", "b"))
+        rng = np.random.default_rng(12)
+        x, b, dx, db = (rng.normal(size=n) for _ in range(4))
+        lo, ln = partition(n, world)[rank]
+        sp = shard_program.ShardedProgram(gp, "normRes1DLaplacianSQ_grad", n, lo)
+        assert sp.ghost == 2 and hasattr(sp.comm, "exchange_rows_device")
+        seen = {"host": 0}
+        real = sp.comm.exchange_rows
+        sp.comm.exchange_rows = lambda *a: seen.__setitem__("host", seen["host"] + 1) or real(*a)
+        local = {k: ViewStorage.from_values(k, v[lo:lo + ln].copy()) for k, v in
+                 (("x", x), ("b", b), ("_d_x", dx), ("_d_b", db))}
+        for v in local.values():
+            v.device_ptr(krn.Device.get())  # resident before the call, as in a real run
+        sp.run(local)
+        assert seen["host"] == 0, "ghost rows travelled through the host"
+        out.put((rank, {k: v.buffer.copy() for k, v in local.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ghost_rows_stay_on_the_device(world):
+    import torch.multiprocessing as mp
+
+    n = 30_011
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_ghost_worker, args=(r, world, port, n, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    prog = krn.load_program("laplacian")
+    gp = krn.differentiate(prog, "normRes1DLaplacianSQ", ("x", "b"))
+    rng = np.random.default_rng(12)
+    x, b, dx, db = (rng.normal(size=n) for _ in range(4))
+    _, want = _whole(gp, "normRes1DLaplacianSQ_grad", {"x": x, "b": b, "_d_x": dx, "_d_b": db}, "compiled")
+    for k in ("x", "_d_x", "_d_b"):
+        assert_bits(np.concatenate([got[r][k] for r in range(world)]), want[k], f"world={world} {k}")
+
+
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("stem", ["gather_indirect", "gather_rows_rank2"])
 def test_replicated_views_and_their_scattered_shadows(stem, world):
