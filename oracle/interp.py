@@ -86,8 +86,9 @@ class Machine:
     caller), function-scope scalars, and the deferred-atomic queue of the
     kernel in flight."""
 
-    def __init__(self, fn, check_finite=False, deterministic=True):
+    def __init__(self, fn, check_finite=False, deterministic=True, threads=1):
         self.fn = fn
+        self.threads = max(1, int(threads))
         self.views: dict = {}
         self.scalars: dict = {}
         self.check_finite = check_finite
@@ -318,6 +319,9 @@ class Machine:
             random.Random(self.rng_seed + self.kernel_index).shuffle(order)
             self.trace = {}
         try:
+            if self.threads > 1 and n >= 2 * self.threads and self.rng_seed is None:
+                self.queue = self.kernel_on_pool(loop, n)
+                order = ()
             for i in order:
                 self.local = {loop.counter: i}
                 self.iteration, self.seq = i, 0
@@ -338,6 +342,33 @@ class Machine:
             flat[off] += v
         self.guard_views()
 
+    def kernel_on_pool(self, loop, n):
+        """threads > 1: the reference cuts [0, n) into `threads` contiguous chunks and runs them on
+        a thread pool, every chunk with its own iteration context but the SAME view storage; plain
+        writes land immediately, atomic contributions are queued per chunk and merged (the sort by
+        (iteration, sequence) at the kernel boundary makes the result independent of the schedule)
+        [runtime.py:594-613].  Python threads share the interpreter lock, so this costs rather
+        than saves time - which is exactly what the reference's bench shows."""
+        import copy
+        from concurrent.futures import ThreadPoolExecutor
+
+        T = self.threads
+        bounds = [(n * t) // T for t in range(T + 1)]
+
+        def chunk(t):
+            w = copy.copy(self)
+            w.queue, w.local = [], {}
+            for i in range(bounds[t], bounds[t + 1]):
+                w.local = {loop.counter: i}
+                w.iteration, w.seq = i, 0
+                for s in loop.body:
+                    w.element(s, in_kernel=True)
+            return w.queue
+
+        with ThreadPoolExecutor(max_workers=T) as pool:
+            parts = list(pool.map(chunk, range(T)))
+        return [q for part in parts for q in part]
+
     # ---- optional finiteness traps ----------------------------------------------------
 
     def guard_views(self):
@@ -351,13 +382,14 @@ class Machine:
             raise NonFiniteDetected(f"non-finite scalar {float(v)!r}")
 
 
-def run(program, fn_name: str, inputs: dict, *, check_finite=False, deterministic=True):
+def run(program, fn_name: str, inputs: dict, *, check_finite=False, deterministic=True, threads=1):
     """Execute ``fn_name`` on ``inputs`` (name -> float64 ndarray | float).
-    Arrays are mutated in place.  Returns the function value (None if void)."""
+    Arrays are mutated in place.  Returns the function value (None if void).  ``threads``: the
+    reference's thread-pool execution of kernels (same results, see Machine.kernel_on_pool)."""
     fn = program.function(fn_name)
     if fn is None:
         raise KeyError(f"no function named '{fn_name}'")
-    return Machine(fn, check_finite, deterministic).run(inputs)
+    return Machine(fn, check_finite, deterministic, threads).run(inputs)
 
 
 def detect(program, fn_name: str, inputs: dict, *, rng_seed: int = 0):

@@ -38,6 +38,8 @@ def inputs_for(fn, n, rows, rng):
             out[p.name] = rng.integers(0, rows, size=n).astype(np.float64)
         elif p.name == "q" and any(q.name == "idx" for q in fn.params):
             out[p.name] = rng.normal(size=(rows, 3))
+        elif p.name == "fine":
+            out[p.name] = rng.normal(size=2 * n + 1)  # read at 2*i - 1 .. 2*i + 1 for i < n
         elif p.type.rank == 2:
             out[p.name] = rng.normal(size=(n, 3))
         else:

@@ -63,7 +63,7 @@ class Site:
     view: str
     offset: object = None  # int c when the row index is `counter + c`
     column: object = None  # int or None (rank-1)
-    mode: str = "atomic"  # "gather" | "atomic" | "staged_atomic"
+    mode: str = "atomic"  # "gather" | "direct" | "atomic" | "staged_atomic"
     merged: tuple = ()  # sites folded into this one (merge_adjacent_atomics)
     absorbed: bool = False  # this site's contribution travels with an earlier site
     ord: object = None  # (key offset, value offset, groups, width, group): record layout of the ordered policy
@@ -86,6 +86,49 @@ def _constant(idx):
     except (TypeError, ValueError):
         return None
     return const if not terms else None
+
+
+def _affine(idx, counter):
+    """``a * counter + c (+ counter-free symbolic terms)`` -> (a, c, symbolic terms), a != 0; else None."""
+    try:
+        const, terms = normalize_index(idx)
+    except (TypeError, ValueError):
+        return None
+    a, rest = 0, []
+    for atom, coef in terms:
+        if atom == ("counter", counter):
+            a = coef
+        elif atom[0] in ("counter", "view"):
+            return None
+        else:
+            rest.append((atom, coef))
+    return (a, const, tuple(rest)) if a != 0 else None
+
+
+def _injective(group, counter) -> bool:
+    """True when no two DIFFERENT iterations of the kernel can name one location through the sites of
+    `group` (all on one View): every row index is ``a*i + c_k`` with one common stride a and one common
+    symbolic part, and two sites either name the same location in the same iteration (equal c, equal
+    column) or can never meet (different literal columns, or c_k - c_l not a multiple of a).  This is
+    the injectivity refinement of the reference's conservative race rule 2 (analysis.py:204-248,
+    271-303: `normalize_index` is the information source)."""
+    forms = []
+    for st in group:
+        idx = st.stmt.target.indices
+        f = _affine(idx[0], counter)
+        col = _constant(idx[1]) if len(idx) == 2 else 0
+        if f is None or col is None:
+            return False
+        forms.append((f, col))
+    (a, _, sym), _ = forms[0]
+    for (fa, fc, fs), col in forms:
+        if fa != a or fs != sym:
+            return False
+    for i, ((_, c1, _), col1) in enumerate(forms):
+        for (_, c2, _), col2 in forms[i + 1:]:
+            if col1 == col2 and c1 != c2 and (c1 - c2) % abs(a) == 0:
+                return False
+    return True
 
 
 def plan_atomics(loop) -> list:
@@ -132,9 +175,16 @@ def plan_atomics(loop) -> list:
             st.column = _constant(idx[1]) if len(idx) == 2 else None
             if st.offset is None or (len(idx) == 2 and st.column is None):
                 gather = False
+        # every location has ONE writing iteration (strided / reversed / column-disjoint affine maps the
+        # reference flags conservatively): that iteration adds its contributions itself, in program
+        # order - plain read-modify-write, no staging, no atomics, bit-identical.  Not when the kernel
+        # also reads the View (deferral: reads must see pre-kernel values).
+        direct = not gather and view not in touched_plainly and _injective(group, loop.counter)
         for st in group:
             if gather:
                 st.mode = "gather"
+            elif direct:
+                st.mode = "direct"
             else:
                 st.mode = "staged_atomic" if view in touched_plainly else "atomic"
     merge_adjacent_atomics(loop.body, {id(st.stmt): st for st in sites})
@@ -677,6 +727,11 @@ class ModuleBuilder:
                 out.append(head + f"T{site.index}[e] = t_; }}")  # tile kernel: staging column in registers
             elif site.mode == "gather":
                 out.append(head + f"stage[{site.index} * n + i] = t_; }}")
+            elif site.mode == "direct":
+                # window kernels re-run statements on halo iterations (slot e == 4): those belong to a
+                # neighbouring warp, which performs the update itself
+                own = "if (e < 4) " if self.in_tile else ""
+                out.append(head + f"{own}E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
             elif site.mode == "staged_atomic":
                 out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
                            f"{{ stage[{site.index} * n + i] = t_; ostage[{site.index} * n + i] = o_; }} }}")

@@ -183,10 +183,11 @@ class Facts:
     affine: bool = True    # every access is `counter + c` on a rank-1 View, writes at c = 0, reads proven in range
     offsets: frozenset = frozenset()
     rd: bool = False
+    direct: bool = False   # touched ONLY by "direct" atomic sites (one writing iteration per location)
 
     def merged(self, o: "Facts") -> "Facts":
         return Facts(self.pw and o.pw, self.wr or o.wr, self.at or o.at, self.affine and o.affine,
-                     self.offsets | o.offsets, self.rd or o.rd)
+                     self.offsets | o.offsets, self.rd or o.rd, self.direct and o.direct)
 
 
 def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
@@ -194,10 +195,11 @@ def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
     (`stage_name`): written pointwise by the producer, read at -offset by the apply loop."""
     out: dict = {}
 
-    def note(view, pw, wr, at, affine, c, rd):
-        f = out.get(view, Facts())
+    def note(view, pw, wr, at, affine, c, rd, direct=False):
+        f = out.get(view, Facts(direct=True))
         offs = f.offsets | ({c} if c is not None else set())
-        out[view] = Facts(f.pw and pw, f.wr or wr, f.at or at, f.affine and affine, frozenset(offs), f.rd or rd)
+        out[view] = Facts(f.pw and pw, f.wr or wr, f.at or at, f.affine and affine, frozenset(offs), f.rd or rd,
+                          f.direct and direct)
 
     if loop.what == "apply":
         view, sites, producer = loop.apply_of
@@ -210,11 +212,15 @@ def loop_facts(loop: "LoopOp", an: "Analysis") -> dict:
     except (TypeError, ValueError):
         trip = None
     staged_views = {st.view for st in loop.sites if st.mode == "gather"}
+    direct_views = {st.view for st in loop.sites if st.mode == "direct"}
     for st in loop.sites:
         if st.mode == "gather":
             note(stage_name(st.index, loop), True, True, False, True, 0, False)
     for a, guards in guarded_accesses(loop):
         if a.atomic and a.view in staged_views:
+            continue
+        if a.atomic and a.view in direct_views:
+            note(a.view, False, True, True, False, None, False, direct=True)
             continue
         pw = _is_pointwise(a, loop.counter)
         c = codegen._unit_affine(a.indices[0], loop.counter) if len(a.indices) == 1 else None
@@ -261,7 +267,9 @@ def window_plan(ops: list, an: "Analysis"):
     for f in per:
         for v, x in f.items():
             G[v] = G[v].merged(x) if v in G else x
-    windowed = [v for v, f in G.items() if f.wr and not f.pw and not v.startswith("__stage")]
+    # (a View reached only through "direct" atomic sites is updated in global memory by its one
+    # writing iteration - own iterations only, see below - and takes no part in the windows)
+    windowed = [v for v, f in G.items() if f.wr and not f.pw and not v.startswith("__stage") and not f.direct]
     for v in windowed:
         f = G[v]
         if not f.affine or f.at or an.rank.get(v) != 1:
@@ -295,10 +303,12 @@ def window_plan(ops: list, an: "Analysis"):
         if hlo == 0 and hhi == 0:
             continue
         # an op that runs on halo iterations must leave no trace outside registers and windows
-        if any(st.mode != "gather" for st in ops[k].sites):
+        # ("direct" sites write global memory, but only from the iteration's OWN slot: codegen guards
+        # them with e < 4 inside window kernels, so re-running the statement on halo rows is harmless)
+        if any(st.mode not in ("gather", "direct") for st in ops[k].sites):
             return None
         for v, f in per[k].items():
-            if f.wr and v not in in_kernel:
+            if f.wr and v not in in_kernel and not f.direct:
                 return None
             if False:
                 return None  # its apply loop runs in another launch: contributions must be stored exactly once

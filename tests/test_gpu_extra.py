@@ -144,3 +144,38 @@ def test_taped_gradients_on_the_gpu(policy, n):
             want = {k: v.buffer for k, v in ref.items()}
         for k in want:
             assert_bits(got[k].buffer, want[k], f"{name} {policy} n={n} {k}")
+
+
+@pytest.mark.parametrize("policy", sorted(POLICIES))
+@pytest.mark.parametrize("stem,wrt", [("stride2_scatter", ("fine", "w")), ("stride2_collide", ("fine", "w")),
+                                      ("rank2_row_offset", ("m", "r"))])
+def test_affine_maps_beyond_unit_stride_on_fresh_inputs(stem, wrt, policy):
+    """general affine gather form: stride-2 maps with one writing iteration per location
+    (direct read-modify-write), stride-2 maps where two iterations meet (ordered policy), row offsets
+    onto a rank-2 target (gather form) - bit-identical to the CPU oracle at sizes the stored vectors
+    do not cover, one launch for the gradients that need no sort"""
+    from oracle import interp
+
+    prog = krn.load_program(stem)
+    fn = prog.functions[0]
+    gp = krn.differentiate(prog, fn.name, wrt)
+    gfn = gp.functions[-1]
+    dev = krn.Device.get()
+    for n in (3, 257, 4099, 40_001):
+        rng = np.random.default_rng(n)
+        data = {}
+        for p in fn.params:
+            data[p.name] = rng.normal(size=(2 * n + 1) if p.name == "fine" else ((n, 3) if p.type.rank == 2 else n))
+        for sp, w in zip(gfn.params[len(fn.params):], wrt):
+            data[sp.name] = rng.normal(size=np.shape(data[w]))
+        want = {k: v.copy() for k, v in data.items()}
+        interp.run(gp, gfn.name, want)
+        got = _views(data)
+        before = dev.launches()
+        cfg = POLICIES[policy]
+        krn.execute(gp, gfn.name, got, cfg)
+        launches = dev.launches() - before
+        for k, v in got.items():
+            assert_bits(v.buffer, want[k], f"{stem} {policy} n={n} {k}")
+        if policy in ("fused", "compiled") and stem != "stride2_collide":
+            assert launches == 1, (stem, policy, n, launches)
