@@ -207,6 +207,9 @@ int krn_laplacian_grad_peers(krn_ctx *ctx, const double *d_x_in, double *d_x_out
  * cached on disk under $KRN_CACHE_DIR (default ~/.cache/krn_b200; empty = off),
  * keyed by source, prelude, options and NVRTC version. */
 int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_module **out);
+/* which run-time compiler the process ended up with (a Python environment may have loaded an older
+ * libnvrtc first) and whether generated kernels use the 256-bit accesses (PTX ISA 8.8, NVRTC >= 12.9) */
+int krn_jit_info(int *nvrtc_major, int *nvrtc_minor, int *ld256);
 int krn_module_destroy(krn_module *m);
 /* launch `name` over `n_iterations` (grid sized by the library: a multiple of
  * the SM count); args = array of pointers to the kernel's arguments */

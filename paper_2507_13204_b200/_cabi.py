@@ -76,6 +76,7 @@ SIGNATURES = {
     "krn_laplacian_primal_peers": (_i, [_vp, _dp, _dp, _dp, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _dp, _i]),
     "krn_laplacian_grad_peers": (_i, [_vp, _dp, _dp, _dp, _dp, _dp, _i, _i, _sz, _sz, _sz, _dp, _dp, _dp, _dp, _d]),
     "krn_module_compile": (_i, [_vp, C.c_char_p, _pp]),
+    "krn_jit_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "krn_module_destroy": (_i, [_vp]),
     "krn_module_launch": (_i, [_vp, _vp, C.c_char_p, _sz, _sz, _pp]),
     "krn_module_launch_exact": (_i, [_vp, _vp, C.c_char_p, _sz, C.c_uint, _sz, _pp]),

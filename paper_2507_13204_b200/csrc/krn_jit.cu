@@ -182,6 +182,16 @@ void write_file_atomically(const std::string &path, const std::vector<char> &dat
 
 }  // namespace
 
+extern "C" int krn_jit_info(int *nvrtc_major, int *nvrtc_minor, int *ld256)
+{
+    KRN_REQUIRE(nvrtc_major && nvrtc_minor && ld256, "null argument");
+    int rc = load_api();
+    if (rc) return rc;
+    api.Version(nvrtc_major, nvrtc_minor);
+    *ld256 = api.ld256 ? 1 : 0;
+    return KRN_OK;
+}
+
 extern "C" int krn_module_compile(krn_ctx *ctx, const char *cuda_source, krn_module **out)
 {
     KRN_REQUIRE(ctx && cuda_source && out, "null argument");

@@ -36,6 +36,8 @@
 #include "krn_common.cuh"
 #include "krn_prelude.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 constexpr int kThreads = 256;
@@ -377,7 +379,15 @@ int steps_for(size_t n_global, bool grad)
     // a ticket and a partial per block: 4 steps balance that against the sweep (6.52 TB/s); small
     // problems are latency bound and spread over as many blocks as possible.
     if (grad) return 1;
-    return n_global <= (size_t(1) << 20) ? 1 : 4;
+    if (const char *e = getenv("KRN_LAP_STEPS")) return atoi(e);  // experiments (tools/sweep_mid.py)
+    // mid sizes, measured (tools/sweep_mid.py, device time incl. ~6 us of launch + event cost, L2 flushed):
+    //   rows      0.5 M   0.7 M    1 M     2 M     3 M     10 M
+    //   1 step    11.4    12.5    14.3    19.5    26.6    61.5 us
+    //   2 steps   12.3    12.4    13.2    18.4    23.5    52.2
+    //   4 steps   12.3    13.2    14.3    16.4    22.6    49.3
+    if (n_global < 768 * 1024) return 1;
+    if (n_global < 1536 * 1024) return 2;
+    return 4;
 }
 
 template <bool GRAD, int STEPS>
@@ -443,6 +453,10 @@ int launch(krn_ctx *ctx, const double *x_in, double *x_out, const double *b, dou
     dim3 grid((unsigned)blocks);
     if (steps == 1)
         dispatch<GRAD, 1>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
+    else if (steps == 2)
+        dispatch<GRAD, 2>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
+    else if (steps == 8)
+        dispatch<GRAD, 8>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
     else
         dispatch<GRAD, 4>(ctx, grid, s, x_out, dx, db, dx_zero, db_zero, seed, vec, f, accumulate);
     KRN_LAUNCH_CHECK(ctx);

@@ -570,7 +570,7 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
         else:
             raise TypeError(f"cannot execute {k}")
     flush()
-    return _drop_dead_fills(ops, fn)
+    return _drop_dead_fills(ops, fn, an)
 
 
 def _op_views(op) -> set:
@@ -611,11 +611,47 @@ def _op_views(op) -> set:
     return out
 
 
-def _drop_dead_fills(ops: list, fn) -> list:
-    """`deep_copy(local, scalar)` whose destination nothing reads afterwards is dead: locals die
-    at the return (runtime.py: DeclView storage is dropped), and a fill cannot raise.  The
-    generated gradients end with such fills (the reversal of `deep_copy(t, 0.0)` zeroes the
-    shadow of a View that is never used again)."""
+def _cannot_raise(loop: "LoopOp", an) -> bool:
+    """True when no access of the loop can leave its View and no bulk statement can meet
+    mismatching extents - i.e. executing the statement is unobservable apart from the values it
+    writes.  Proven for accesses at exactly the running index (literal column 0 of a rank-2 row
+    excluded: column extents are run-time data) over a range that IS the View's first extent."""
+    if loop.what == "apply":
+        return False
+    try:
+        trip = an.trip(loop.upper)
+    except (TypeError, ValueError):
+        return False
+    if loop.what in ("deepcopy", "suminto") and isinstance(loop.origin.src, str):
+        try:
+            if an.trip(N.Extent(loop.origin.src, 0)) != an.trip(N.Extent(loop.origin.dst, 0)):
+                return False  # ShapeMismatch is decided at run time
+        except (TypeError, ValueError):
+            return False
+    if loop.sites:
+        return False
+    for a in loop.accesses():
+        if an.rank.get(a.view, 1) != 1 or len(a.indices) != 1:
+            return False
+        if kind(a.indices[0]) != "Counter" or a.indices[0].name != loop.counter:
+            return False
+        try:
+            if an.trip(N.Extent(a.view, 0)) != trip:
+                return False
+        except (TypeError, ValueError):
+            return False
+    return True
+
+
+def _drop_dead_fills(ops: list, fn, an=None) -> list:
+    """Dead statements: a statement all of whose results nothing reads afterwards, and whose
+    execution cannot raise, is unobservable - locals die at the return (runtime.py: DeclView
+    storage is dropped).  The generated gradients carry such statements: the verbatim forward
+    sweep computes Views only the (dead) forward reduction reads (`w` and `total` in
+    mean_shift_grad), and the reversal of `deep_copy(t, 0.0)` zeroes the shadow of a View that is
+    never used again.  Backward liveness over the op list: fills of dead locals, loop-shaped
+    statements that write only dead locals through provably in-range accesses (`_cannot_raise`),
+    gathers into scalars nobody reads, and pure scalar statements."""
     local = {s.name for s in walk_statements(fn.body) if kind(s) == "DeclView"}
     needed: set = set()
     needed_scalars: set = set()
@@ -647,14 +683,24 @@ def _drop_dead_fills(ops: list, fn) -> list:
             written = {x.name for x in stmts if kind(x) in ("DeclScalar", "AssignScalar")}
             if pure and not (written & needed_scalars):
                 continue
-        needed_scalars |= scalar_reads(op)
+        if op[0] == "gather" and op[1].dst not in needed_scalars:
+            continue  # a sum nobody reads (a gather cannot raise)
         stmt = op[1].origin if op[0] == "loop" and op[1].what == "deepcopy" else op[1] if op[0] == "raw" else None
         if stmt is not None and kind(stmt) == "DeepCopy" and not isinstance(stmt.src, str):
             if stmt.dst in local and stmt.dst not in needed:
                 continue  # dead
+            needed_scalars |= scalar_reads(op)
             needed.discard(stmt.dst)  # fully overwritten here: earlier contents are not needed
             kept.append(op)
             continue
+        if op[0] == "loop" and an is not None and op[1].what in ("kernel", "suminto", "deepcopy"):
+            written = {a.view for a in op[1].accesses() if a.write}
+            if written and written <= local and not (written & needed) and _cannot_raise(op[1], an):
+                continue  # writes only locals nothing reads afterwards
+        needed_scalars |= scalar_reads(op)
+        if op[0] == "gather" and not op[2]:
+            needed_scalars.discard(op[1].dst)  # assigned here (not accumulated): earlier values are dead
+            needed_scalars |= scalar_reads(op) - {op[1].dst}
         needed |= _op_views(op)
         kept.append(op)
     kept.reverse()
