@@ -409,6 +409,11 @@ def main():
             "compulsory_bytes_accumulate": GRAD_BYTES_PER_ROW / PRIMAL_BYTES_PER_ROW,
             "compulsory_bytes_zero_shadows": GRAD_ZERO_BYTES_PER_ROW / PRIMAL_BYTES_PER_ROW,
         }
+        ja, jb, jc = C.c_int(), C.c_int(), C.c_int()
+        _cabi.check(lib.krn_jit_info(C.byref(ja), C.byref(jb), C.byref(jc)))
+        line["generated_kernels"] = {"nvrtc": f"{ja.value}.{jb.value}", "ld256": bool(jc.value),
+                                     "note": "run-time compiler the generated kernels of this run went through; "
+                                             "ld256 = 256-bit global accesses (PTX ISA 8.8) in generated code"}
         line["sweep"] = sweep(dev, torch)
         line["two_d_views"] = two_d_views(krn, dev, torch)
         line["statements_policy_large_n"] = stm
@@ -502,13 +507,21 @@ def two_d_views(krn, dev, torch, rows=1 << 24):
         wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
         gp = krn.differentiate(prog, fn.name, wrt)
         gfn = gp.functions[-1]
-        cfg = krn.ExecutionConfig(policy="compiled", synchronous=False, device=dev)
-        best = {"primal": [], "grad": []}
+        # accumulation of the adjoint's atomic_add queue: "ordered" = the reference's order (stable
+        # partition by target + in-order fold, bit-identical and reproducible; the default under
+        # deterministic_reduction=True), "hardware" = fp64 reductions in L2 (exact up to reassociation)
+        variants = {"ordered": krn.ExecutionConfig(policy="compiled", synchronous=False, device=dev)}
+        if stem == "gather_rows_rank2":
+            variants["hardware"] = krn.ExecutionConfig(policy="compiled", synchronous=False, device=dev,
+                                                       deterministic_reduction=False)
+        best = {"primal": []}
+        best.update({"grad_" + k: [] for k in variants})
         launches = {}
         for rep in range(4):
-            for which in ("primal", "grad"):
+            for which in best:
                 call = {k: v.copy() for k, v in base.items()}
-                if which == "grad":
+                cfg = variants["ordered"] if which == "primal" else variants[which[5:]]
+                if which != "primal":
                     for sp, w in zip(gfn.params[len(fn.params):], wrt):
                         call[sp.name] = ViewStorage.zeros(sp.name, base[w].extents)
                 dev.sync()
@@ -523,15 +536,37 @@ def two_d_views(krn, dev, torch, rows=1 << 24):
                 best[which].append(e0.elapsed_time(e1))
                 launches[which] = dev.launches() - l0
                 del call
-        tp, tg = min(best["primal"][1:]), min(best["grad"][1:])
+        tp, tg = min(best["primal"][1:]), min(best["grad_ordered"][1:])
         out[stem] = {"rows": rows, "columns": 3, "primal_ms": tp, "grad_ms": tg, "ratio": tg / tp,
-                     "primal_launches": launches["primal"], "grad_launches": launches["grad"],
+                     "primal_launches": launches["primal"], "grad_launches": launches["grad_ordered"],
                      "primal_compulsory_gbs": bytes_primal * rows / tp / 1e6,
                      "grad_compulsory_gbs": bytes_grad * rows / tg / 1e6,
                      "gradient_entries_per_s": (3 * rows + rows) / tg * 1e3}
+        if "grad_hardware" in best:
+            th = min(best["grad_hardware"][1:])
+            out[stem]["accumulation"] = {
+                "ordered": {"grad_ms": tg, "launches": launches["grad_ordered"], "bit_identical_to_reference": True,
+                            "compulsory_gbs": bytes_grad * rows / tg / 1e6},
+                "hardware_atomics": {"grad_ms": th, "launches": launches["grad_hardware"],
+                                     "bit_identical_to_reference": False, "compulsory_gbs": bytes_grad * rows / th / 1e6},
+                "counters": profiled_two_d(rows)}
     out["note"] = ("compulsory bytes per row: rowscale 32 / 64, gather_rows 40 / 96 (3 gathered + 3 scattered "
-                   "columns of a randomly indexed row: sector- and atomic-bound, not HBM-bound)")
+                   "columns of a randomly indexed row).  Neither accumulation is HBM-bound: hardware reductions are "
+                   "bound by L2 atomic throughput on 32 B sectors (one sector per 8 B contribution), the ordered "
+                   "policy by the instruction issue of its stable partition passes (see DESIGN.md 4.7)")
     return out
+
+
+def profiled_two_d(rows):
+    """L2 reduction sectors and DRAM bytes of the gather_rows_rank2 gradient under both accumulation
+    policies, from the committed ncu capture (profiles/r2_two_d_views_counters.json) when it was taken
+    at this size; None otherwise."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_two_d_views_counters.json")) as f:
+            rec = json.load(f)
+        return rec if rec.get("rows") == rows else None
+    except Exception:
+        return None
 
 
 def profiled_traffic(rows):

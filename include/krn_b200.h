@@ -126,6 +126,12 @@ int krn_check_finite(krn_ctx *ctx, const double *d_v, size_t n, int *d_flag);
  * site that did not execute.  target_size <= 2^31, records < 2^32 - 1, width 1..4. */
 int krn_ordered_accumulate(krn_ctx *ctx, double *d_target, size_t target_size, const uint32_t *d_keys,
                            const double *d_vals, size_t records, int width);
+/* The same for a rows x ncols target whose records name a ROW (key) and carry one value per plane for
+ * the literal column cols[l] of that row (sites atomic_add(v(r, c0), .), atomic_add(v(r, c1), .), ... of
+ * one iteration travel as ONE record): d_target[key*ncols + cols[l]] += d_vals[l*records + r].
+ * rows <= 2^31, planes 1..4. */
+int krn_ordered_accumulate_rows(krn_ctx *ctx, double *d_target, size_t rows, int ncols, const int *cols, int planes,
+                                const uint32_t *d_keys, const double *d_vals, size_t records);
 /* cudaMemsetAsync on the context's stream */
 int krn_memset(krn_ctx *ctx, void *d_ptr, int byte, size_t bytes);
 

@@ -65,6 +65,7 @@ SIGNATURES = {
     "krn_reduce_pairwise": (_i, [_vp, _dp, _sz, _dp, _i]),
     "krn_check_finite": (_i, [_vp, _dp, _sz, _vp]),
     "krn_ordered_accumulate": (_i, [_vp, _dp, _sz, _vp, _dp, _sz, _i]),
+    "krn_ordered_accumulate_rows": (_i, [_vp, _dp, _sz, _i, C.POINTER(_i), _i, _vp, _dp, _sz]),
     "krn_memset": (_i, [_vp, _vp, _i, _sz]),
     "krn_laplacian_primal": (_i, [_vp, _dp, _dp, _dp, _sz, _sz, _sz, _dp, _dp, _i]),
     "krn_laplacian_grad": (_i, [_vp, _dp, _dp, _dp, _dp, _dp, _i, _i, _sz, _sz, _sz, _dp, _d]),

@@ -67,6 +67,7 @@ class Site:
     merged: tuple = ()  # sites folded into this one (merge_adjacent_atomics)
     absorbed: bool = False  # this site's contribution travels with an earlier site
     ord: object = None  # (key offset, value offset, groups, width, group): record layout of the ordered policy
+    lanes: bool = False  # head of a run of sites on the literal columns of ONE row of a rank-2 View (`merged`)
 
 
 def _unit_affine(idx, counter):
@@ -197,17 +198,34 @@ def merge_adjacent_atomics(body, by_id) -> None:
     - issue ONE reduction with the sum of their values.  Nothing can observe the location in
     between (an "atomic"-mode target is neither read nor plainly written by the kernel), and the
     policy is exact only up to reassociation anyway (d + (a + b) for (d + a) + b); gather-mode
-    sites, which are bit-identical to the interpreter, are never merged."""
+    sites, which are bit-identical to the interpreter, are never merged.  Under the ordered policy
+    the merged sites stay apart as the values of one record.
+
+    Sites that follow each other directly and name DIFFERENT literal columns of one row of a rank-2
+    View (`atomic_add(_d_q(idx(i), 0), .); atomic_add(_d_q(idx(i), 1), .); ...`) are grouped the
+    same way (`lanes`): one record per row under the ordered policy instead of one per element."""
     head = None
     for s in body:
         k = kind(s)
         st = by_id.get(id(s)) if k == "AtomicAdd" else None
         if st is not None and st.mode == "atomic":
-            if head is not None and head.stmt.target == s.target and len(head.merged) + 1 < ORDERED_WIDTH:
-                head.merged += (st,)
-                st.absorbed = True
-            else:
-                head = st
+            idx = s.target.indices
+            if head is not None and len(head.merged) + 1 < ORDERED_WIDTH:
+                hidx = head.stmt.target.indices
+                if not head.lanes and head.stmt.target == s.target:
+                    head.merged += (st,)
+                    st.absorbed = True
+                    continue
+                col, hcols = (_constant(idx[1]) if len(idx) == 2 else None), None
+                if len(idx) == 2 and len(hidx) == 2 and head.stmt.target.view == s.target.view and hidx[0] == idx[0] \
+                        and (head.lanes or not head.merged):
+                    hcols = [_constant(hidx[1])] + [_constant(m.stmt.target.indices[1]) for m in head.merged]
+                if hcols is not None and col is not None and None not in hcols and col not in hcols:
+                    head.merged += (st,)
+                    head.lanes = True
+                    st.absorbed = True
+                    continue
+            head = st
             continue
         head = None
         if k == "If":
@@ -223,18 +241,37 @@ def assign_ordered(site_lists) -> list:
     program order form `groups` record slots per iteration (a head site and the sites merged
     into it share one record of `width` values), record number = iteration * groups + group -
     the reference's queue order (runtime.py:430-447: appended per iteration in program order,
-    sorted by (iteration, sequence number)).  Offsets are in units of the trip count."""
+    sorted by (iteration, sequence number)).  Offsets are in units of the trip count.
+
+    `cols` (a tuple of literal columns) marks a queue of ROW records: every group of the View is a
+    run of sites on the same literal columns of one row, the key is the row and value plane l goes
+    to column cols[l].  A View with lane groups that do not all name the same columns gives the
+    grouping up: each of those sites becomes a record of its own again."""
     entries, key_off, val_off = [], 0, 0
     for sites in site_lists:
         by_view: dict = {}
         for st in sites:
-            if st.mode in ("atomic", "staged_atomic") and not st.absorbed:
+            if st.mode in ("atomic", "staged_atomic"):
                 by_view.setdefault(st.view, []).append(st)
-        for view, heads in by_view.items():
+        for view, every in by_view.items():
+            lane_heads = [st for st in every if st.lanes]
+            cols = None
+            if lane_heads:
+                shapes = {tuple([_constant(st.stmt.target.indices[1])] + [_constant(m.stmt.target.indices[1]) for m in st.merged])
+                          for st in lane_heads}
+                heads_all = [st for st in every if not st.absorbed]
+                if len(shapes) == 1 and len(lane_heads) == len(heads_all):
+                    cols = next(iter(shapes))
+                else:
+                    for st in lane_heads:  # mixed shapes: back to one record per site
+                        for m in st.merged:
+                            m.absorbed = False
+                        st.merged, st.lanes = (), False
+            heads = [st for st in every if not st.absorbed]
             groups, width = len(heads), max(1 + len(st.merged) for st in heads)
             for g, st in enumerate(heads):
                 st.ord = (key_off, val_off, groups, width, g)
-            entries.append(dict(view=view, groups=groups, width=width, key_off=key_off, val_off=val_off))
+            entries.append(dict(view=view, groups=groups, width=width, key_off=key_off, val_off=val_off, cols=cols))
             key_off += groups
             val_off += groups * width
     return entries
@@ -709,16 +746,20 @@ class ModuleBuilder:
             site = sites.get(id(s)) if sites else None
             if site is not None and site.absorbed:
                 return  # its value travels with the preceding site's (merge_adjacent_atomics)
-            extra = []
+            extra, lane_offsets = [], []
             if site is not None and site.merged:
                 for j, m in enumerate(site.merged):
+                    if site.lanes:  # another literal column of the same row: its own bounds check
+                        head += f"krn_i64 o{j}_ = {self.offset(m.stmt.target, local)}; if (bad) {stop} "
+                        lane_offsets.append(f"o{j}_")
                     head += f"double u{j}_ = {self.value(m.stmt.value, local)}; if (bad) {stop} "
                     extra.append(f"u{j}_")
             ordered = None
             if site is not None and site.ord is not None:
                 ko, vo, G, W, g = site.ord
                 vals = (["t_"] + extra + ["-0.0"] * ORDERED_WIDTH)[:ORDERED_WIDTH]
-                ordered = f"krn_ord_put(E, {ko}, {vo}, {G}, {W}, {g}, i, o_, {', '.join(vals)});"
+                key = f"o_ / E.e1[{v}]" if site.lanes else "o_"  # row records: the key is the row
+                ordered = f"krn_ord_put(E, {ko}, {vo}, {G}, {W}, {g}, i, {key}, {', '.join(vals)});"
             if site is None:  # function scope: applies immediately (runtime.py:441-442)
                 out.append(head + f"E.v[{v}][o_] = E.v[{v}][o_] + t_; }}")
             elif site.mode == "gather" and site.index in self.stage_windows:
@@ -739,9 +780,14 @@ class ModuleBuilder:
                 # hardware reductions are exact only up to reassociation, so adjacent sites on one
                 # location issue one reduction with the sum of their values; the ordered policy
                 # keeps them apart (d + a) + b
-                total = "".join(f" t_ = t_ + {u};" for u in extra)
-                out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
-                           f"{{{total} krn_scatter(E, {v}, o_, t_); }} }}")
+                if site.lanes:
+                    total = "".join(f" krn_scatter(E, {v}, {o}, {u});" for o, u in zip(lane_offsets, extra))
+                    out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
+                               f"{{ krn_scatter(E, {v}, o_, t_);{total} }} }}")
+                else:
+                    total = "".join(f" t_ = t_ + {u};" for u in extra)
+                    out.append(head + (f"if (E.apol == 4) {{ {ordered} }} else " if ordered else "") +
+                               f"{{{total} krn_scatter(E, {v}, o_, t_); }} }}")
         elif k == "If":
             out.append(f"{pad}if {self.compare(s.cond, local)} {{")
             self.guards.append(s.cond)

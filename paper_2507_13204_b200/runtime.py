@@ -586,9 +586,16 @@ class OrderedStage:
         dev, n = self.dev, self.n
         for e in self.entries:
             v = self.views[e["view"]]
-            _cabi.check(dev.lib.krn_ordered_accumulate(
-                dev.h, C.c_void_p(v.device_ptr(dev)), v.size, C.c_void_p(self.keys.ptr + 4 * e["key_off"] * n),
-                C.c_void_p(self.vals.ptr + 8 * e["val_off"] * n), n * e["groups"], e["width"]))
+            keys = C.c_void_p(self.keys.ptr + 4 * e["key_off"] * n)
+            vals = C.c_void_p(self.vals.ptr + 8 * e["val_off"] * n)
+            if e.get("cols"):  # row records of a rank-2 target: key = row, one value plane per literal column
+                cols = (C.c_int * len(e["cols"]))(*e["cols"])
+                _cabi.check(dev.lib.krn_ordered_accumulate_rows(
+                    dev.h, C.c_void_p(v.device_ptr(dev)), v.extents[0], v.extents[1], cols, len(e["cols"]), keys, vals,
+                    n * e["groups"]))
+            else:
+                _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, C.c_void_p(v.device_ptr(dev)), v.size, keys, vals,
+                                                           n * e["groups"], e["width"]))
 
 
 def atomic_choice(dev, cfg, recipe, views, builder, n, static_smem: int = 0):

@@ -156,13 +156,35 @@ def test_dead_fills_and_scalars_disappear():
     plan = compiled.plan_for(g)
     groups = [s for s in plan.steps if s[0] == "group"]
     assert plan.launch_count == 1 and len(groups) == 1
-    assert [o.what for o in groups[0][1].ops] == ["deepcopy", "deepcopy", "kernel", "suminto", "kernel", "suminto"]
+    # the forward `deep_copy(t, 0.0)` and `t(i) += ...` only feed the dead forward sum: dropped too
+    assert [o.what for o in groups[0][1].ops] == ["deepcopy", "suminto", "kernel", "suminto"]
     stored = [p["view"] for p in groups[0][2]["promoted"] if p["store"]]
     assert stored == ["_d_src"]  # 16 B/row: read src, write _d_src
     fn, g = _grad("mean_shift")
     assert compiled.plan_for(fn).launch_count == 2       # gather, then fill + kernel + gather
     plan = compiled.plan_for(g)
-    assert plan.launch_count == 3 and not any(s[0] == "scalars" for s in plan.steps)
+    # forward `total = parallel_sum(v); deep_copy(w, total); w(i) += ...` feeds nothing the reverse sweep
+    # reads: what is left is the reversal kernel with its gather, then the broadcast of the gathered scalar
+    assert plan.launch_count == 2 and not any(s[0] == "scalars" for s in plan.steps)
+
+
+def test_dead_statements_that_could_raise_are_kept():
+    """a dead kernel whose accesses are not provably in range must still run: it may have to report
+    OutOfBounds like the reference (an indirect read, a neighbour read, a shorter View)"""
+    p = krn.parse("""fn f(v: view<f64,1>, idx: view<f64,1>, u: view<f64,1>) -> f64 {
+        let t: view<f64,1> = view("t", extent(v, 0));
+        let w: view<f64,1> = view("w", extent(v, 0));
+        parallel_for i in 0..extent(v, 0) { t(i) = v(idx(i)); }
+        parallel_for i in 0..extent(v, 0) { w(i) = u(i); }
+        parallel_for i in 0..extent(v, 0) { w(i) = v(i) + 1.0; }
+        s = parallel_sum(v);
+        return s; }""")
+    an = fusion.Analysis(p.functions[0])
+    ops = fusion.build_ops(p.functions[0], an, True)
+    kernels = [op[1] for op in ops if op[0] == "loop" and op[1].what == "kernel"]
+    # t(i) = v(idx(i)): indirect read - kept; w(i) = u(i): u may be shorter than v - kept;
+    # w(i) = v(i) + 1.0: provably in range and dead - dropped
+    assert len(kernels) == 2
 
 
 def test_a_fill_that_is_read_later_is_kept():

@@ -229,3 +229,64 @@ def test_hardware_policies_when_determinism_is_waived():
     krn.execute(gp, "gatherSquares_grad", got, ExecutionConfig(deterministic_reduction=False))
     assert dev.launches() - before == 1  # one fused kernel, no sort
     assert np.all(np.abs(got["_d_x"].buffer - want["_d_x"]) <= 1e-12 * np.abs(want["_d_x"]))
+
+
+@pytest.mark.parametrize("rows,ncols,cols", [(1, 3, (0, 1, 2)), (700, 3, (2, 0)), (5000, 3, (0, 1, 2)), (40_000, 5, (4, 1, 3, 0)),
+                                             (3, 100, (99, 0, 50)), (300_000, 3, (1,))])
+def test_row_records_with_column_planes(rows, ncols, cols):
+    """krn_ordered_accumulate_rows: one record per ROW, value plane l goes to column cols[l] - the
+    same as the flat queue in which every record is expanded into its per-element records"""
+    from oracle import cport
+
+    dev = Device.get()
+    rng = np.random.default_rng(rows + ncols)
+    for records in (1, 4097, 60_001):
+        for label, keys in _key_maps(records, rows, rng).items():
+            keys = np.asarray(keys).astype(np.uint32)
+            planes = len(cols)
+            vals = rng.normal(size=(records, planes)) * np.exp2(rng.integers(-12, 12, size=(records, planes)))
+            target = rng.normal(size=(rows, ncols))
+            # oracle: the flat queue, record r expanded in plane order (different columns never meet)
+            flat_keys = np.where(keys[:, None] < rows, keys[:, None].astype(np.int64) * ncols + np.array(cols)[None, :],
+                                 0xFFFFFFFF).astype(np.uint32).reshape(-1)
+            want = target.copy()
+            cport.apply_queue(want.reshape(-1), flat_keys, vals.reshape(-1), 1)
+            t = target.copy()
+            bufs = []
+            for a in (t, keys, np.ascontiguousarray(vals.T)):
+                p = dev.alloc(max(a.nbytes, 8))
+                dev.upload(p, a)
+                bufs.append(p)
+            carr = (C.c_int * planes)(*cols)
+            _cabi.check(dev.lib.krn_ordered_accumulate_rows(dev.h, C.c_void_p(bufs[0]), rows, ncols, carr, planes,
+                                                            C.c_void_p(bufs[1]), C.c_void_p(bufs[2]), records))
+            dev.download(t, bufs[0])
+            for p in bufs:
+                dev.free(p)
+            assert_bits(t, want, f"rows={rows} ncols={ncols} cols={cols} records={records} {label}")
+
+
+@pytest.mark.parametrize("policy", ["compiled", "statements"])
+def test_lane_groups_mixed_with_other_sites_fall_back_to_element_records(policy):
+    """a View whose lane groups do not all name the same columns (or that also has single-element
+    sites) gives the row records up: still the reference's bits"""
+    from oracle import interp
+
+    src = """fn f(idx: view<f64, 1>, v: view<f64, 1>, m: view<f64, 2>) {
+        parallel_for i in 0..extent(idx, 0) {
+            atomic_add(m(idx(i), 0), v(i));
+            atomic_add(m(idx(i), 2), 2.0 * v(i));
+            atomic_add(m(0, 1), v(i));
+            atomic_add(m(idx(i), 1), v(i) * v(i));
+            atomic_add(m(idx(i), 2), -v(i));
+        } }"""
+    p = parse(src)
+    rng = np.random.default_rng(1)
+    for n, rows in ((1, 1), (500, 7), (30_000, 9000)):
+        idx, v = rng.integers(0, rows, size=n).astype(np.float64), rng.normal(size=n)
+        want = {"idx": idx.copy(), "v": v.copy(), "m": np.ones((rows, 3))}
+        interp.run(p, "f", want)
+        got = {"idx": ViewStorage.from_values("idx", idx), "v": ViewStorage.from_values("v", v),
+               "m": ViewStorage.from_values("m", np.ones((rows, 3)))}
+        krn.execute(p, "f", got, ExecutionConfig(policy=policy))
+        assert_bits(got["m"].buffer, want["m"], f"{policy} n={n}")

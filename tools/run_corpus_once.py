@@ -1,5 +1,6 @@
 """Runs one corpus program (primal and gradient) a few times under one policy at one size, for ncu:
-python tools/run_corpus_once.py sum_squares compiled 67108864 [reps]"""
+python tools/run_corpus_once.py sum_squares compiled 67108864 [reps] [hardware]   (hardware: deterministic_reduction=False,
+i.e. hardware fp64 reductions instead of the ordered accumulation of atomic_add queues)"""
 import os
 import sys
 
@@ -27,7 +28,9 @@ for p in fn.params:
 wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
 gp = krn.differentiate(prog, fn.name, wrt)
 gfn = gp.functions[-1]
-cfg = ExecutionConfig(policy="compiled" if policy == "pointwise" else policy, fuse_neighbours=policy != "pointwise")
+hardware = len(sys.argv) > 5 and sys.argv[5] == "hardware"
+cfg = ExecutionConfig(policy="compiled" if policy == "pointwise" else policy, fuse_neighbours=policy != "pointwise",
+                      deterministic_reduction=not hardware)
 for rep in range(reps):
     call = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in base.items()}
     krn.execute(prog, fn.name, call, cfg)
