@@ -396,7 +396,12 @@ struct Env {
     unsigned *okeys;    // apol == 4 (ordered): the kernel only records (target offset, values) per site group,
     double *ovals;      //   krn_ordered_accumulate applies them afterwards in the reference's order
     krn_i64 on;         //   trip count of the kernel (records of one group: on)
-};
+    int *fin;           // check_finite inside fused kernels: fin[checkpoint * NV + view] = 1 when a value of the
+};                      //   View is non-finite after that statement (compiled._CompiledRun.finite_replay)
+__device__ __forceinline__ void krn_fin(const Env &E, int slot, double x)
+{
+    if ((__double2hiint(x) & 0x7ff00000) == 0x7ff00000) E.fin[slot] = 1;  // Inf or NaN: exponent all ones
+}
 extern __shared__ double krn_priv[];
 __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, double t)
 {
@@ -548,6 +553,9 @@ class ModuleBuilder:
         self.elide = None  # bounds-check elision context (tile kernels only)
         self.guards: list = []  # enclosing If conditions of the statement being generated
         self.tracing = False  # a dry, access-tagging replay of a kernel is being generated (kernel_trace)
+        self.track = None  # check_finite plans: id(source statement) -> checkpoint number (compiled.CompiledPlan)
+        self.init_tested: set = set()  # Views whose loaded values a tracked kernel tests (checkpoint 0)
+        self.touched_before: set = set()  # Views earlier kernels of the plan touched: their loads are not "as they came in"
         self.has_trace = False
         self.views: list = []  # view table: name -> index
         self.rank: dict = {}

@@ -73,18 +73,37 @@ def _host_evaluable(e, host_scalars) -> bool:
 
 
 class CompiledPlan:
-    def __init__(self, fn, windows: bool = True):
+    def __init__(self, fn, windows: bool = True, track: bool = False):
+        """`track`: a check_finite plan - nothing dead is dropped, every fused kernel tests the values its
+        statements leave behind and records them per (statement, View) (`checkpoints`, finite_replay);
+        raises tilegen.Untrackable when a statement cannot be watched from inside its kernel."""
         self.fn = fn
+        self.track = track
         an = self.an = fusion.Analysis(fn)
-        self.schedule = fusion.form_groups(fusion.build_ops(fn, an, windows), an, windows)
+        self.schedule = fusion.form_groups(fusion.build_ops(fn, an, windows, keep_dead=track), an, windows)
         self.windowed = any(item[0] == "group" and item[1].windowed for item in self.schedule)
         b = self.builder = codegen.ModuleBuilder(fn, host_scalars=an.host_scalars)
+        self.checkpoints: list = []
+        if track:
+            # checkpoint numbers in statement order (0 = the Views as they come in): the reference checks
+            # every View after each kernel / bulk statement and the scalar after each gather
+            # (runtime.py:624, 641, 651, 665)
+            b.track = {}
+            for item in self.schedule:
+                if item[0] == "raw":
+                    raise tilegen.Untrackable("a statement outside the fused kernels")
+                if item[0] == "group":
+                    for loop in item[1].ops:
+                        if id(loop.origin) not in b.track:
+                            b.track[id(loop.origin)] = len(b.track) + 1
         params = {p.name for p in fn.params if p.is_view}
         self.steps: list = []
         bound = set()
         fresh: set = set()  # local Views declared so far that no statement has touched: all +0.0
         for idx, item in enumerate(self.schedule):
             tag = item[0]
+            if track:
+                self._note_checkpoints(item)
             if tag == "declview":
                 fresh.add(item[1].name)
             elif tag != "group":
@@ -95,12 +114,14 @@ class CompiledPlan:
                     later |= _views_of(nxt)
                 item[1].fresh = frozenset(fresh)
                 fresh -= _views_of(item)
+                touched_now = _views_of(item)
                 if item[1].windowed:
                     plan = tilegen.plan_window_group(b, item[1], an, later)
                     self.steps.append(("group", item[1], tilegen.window_kernel(b, item[1], f"g{idx}", plan, an)))
                 else:
                     plan = tilegen.plan_group(b, item[1], an, later)
                     self.steps.append(("group", item[1], tilegen.tile_kernel(b, item[1], f"g{idx}", plan, an)))
+                b.touched_before |= touched_now
             elif tag == "raw":
                 s = item[1]
                 if kind(s) == "ParallelFor":
@@ -124,6 +145,28 @@ class CompiledPlan:
         self.source = b.source()
         self.nslots = max(len(b.slots), 1) + 1
         self.launch_count = sum(1 for s in self.steps if s[0] in ("group", "kernel", "scalars", "return", "gather"))
+
+
+    def _note_checkpoints(self, item):
+        b, tag = self.builder, item[0]
+        if tag == "declview":
+            self.checkpoints.append(("decl", item[1].name))
+        elif tag == "gather":
+            self.checkpoints.append(("scalar", item[1].dst))
+        elif tag == "group":
+            seen = []
+            for loop in item[1].ops:
+                cp = b.track[id(loop.origin)]
+                written = [loop.apply_of[0]] if loop.what == "apply" else \
+                    sorted({a.view for a in loop.accesses() if a.write and not a.atomic})
+                if seen and seen[-1][0] == cp:
+                    seen[-1][1].update(written)
+                else:
+                    seen.append((cp, set(written)))
+            for cp, written in seen:
+                self.checkpoints.append(("views", cp, sorted(written)))
+            if item[1].gather is not None:
+                self.checkpoints.append(("scalar", item[1].gather[0].dst))
 
 
 _plans: dict = {}
@@ -173,21 +216,25 @@ def retuned_module(dev, plan: CompiledPlan):
     return module
 
 
-def plan_for(fn, windows: bool = True) -> CompiledPlan:
+def plan_for(fn, windows: bool = True, track: bool = False):
     """Plan of `fn`; with `windows` the halo-recompute fusion is tried first (the plan's
-    `.windowed` says whether any group uses it)."""
-    key = (id(fn), bool(windows))
+    `.windowed` says whether any group uses it).  `track`: the check_finite variant, or None when
+    some statement of `fn` cannot be watched from inside a fused kernel."""
+    key = (id(fn), bool(windows), bool(track))
     hit = _plans.get(key)
     if hit is not None and hit[0] is fn:
         return hit[1]
     plan = None
     if windows:
         try:
-            plan = CompiledPlan(fn, True)
+            plan = CompiledPlan(fn, True, track)
         except ValueError:
             plan = None  # shape outside the window kernel: plain tile kernels
     if plan is None:
-        plan = CompiledPlan(fn, False)
+        try:
+            plan = CompiledPlan(fn, False, track)
+        except tilegen.Untrackable:
+            plan = None
     _plans[key] = (fn, plan)
     return plan
 
@@ -214,12 +261,17 @@ def run(dev, fn, views: dict, scalars: dict, cfg):
     group cannot preserve the reference's error behaviour."""
     from .runtime import _Run, _plan_for
 
-    plan = plan_for(fn, cfg.fuse_neighbours)
+    track = bool(cfg.check_finite)
+    plan = plan_for(fn, cfg.fuse_neighbours, track)
+    if plan is None:  # check_finite and a statement no fused kernel can watch
+        return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
     r = _CompiledRun(dev, plan, views, scalars, cfg)
     if not r.dry_check() and plan.windowed:
-        r = _CompiledRun(dev, plan_for(fn, False), views, scalars, cfg)
-        if r.dry_check():
-            return r.go()
+        alt = plan_for(fn, False, track)
+        if alt is not None:
+            r = _CompiledRun(dev, alt, views, scalars, cfg)
+            if r.dry_check():
+                return r.go()
         return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
     if not r.dry_check():
         return _Run(dev, _plan_for(fn), views, scalars, cfg).go()
@@ -313,6 +365,8 @@ class _CompiledRun:
                     for v in recipe["elided_views"]:
                         if n > ext[v][0]:
                             return False  # the elided checks assumed extent >= range
+                    if self.plan.track and any(ext[p["view"]][0] != n for p in recipe["promoted"]):
+                        return False  # check_finite: rows the kernel does not visit would go untested
                     for v in recipe.get("alt", ()):
                         if ext[v][0] > n + recipe["max_shift"]:
                             return False  # rows the kernel does not cover would be lost in the buffer swap
@@ -342,7 +396,11 @@ class _CompiledRun:
         for name, slot in b.hslots.items():
             h[slot] = float(self.H.get(name, 0.0))
         self._shared = 8 * atomic[0] if atomic[1] == 2 else 0
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqiiQQq", *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h, *atomic)
+        from .runtime import ENV_TAIL
+
+        fin = self.fin.ptr if getattr(self, "fin", None) is not None else 0
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d" + ENV_TAIL, *p, *e0, *e1, self.S.ptr, self.dev.status_ptr, *h,
+                           *atomic, fin)
 
     def launch_raw(self, name, grid_items, env_bytes, extra):
         env = C.create_string_buffer(env_bytes)
@@ -370,6 +428,9 @@ class _CompiledRun:
         else:
             self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
             dev.fill(self.S.ptr, self.plan.nslots, 0.0)
+        self.fin = None
+        if self.plan.track:
+            self.start_tracking()
         # scalar parameters the function redefines with device data (a gather into the parameter,
         # arithmetic on View elements) live in the slot array: start them at the caller's value
         for p in self.plan.fn.params:
@@ -378,6 +439,57 @@ class _CompiledRun:
         for step in self.plan.steps:
             getattr(self, "do_" + step[0])(*step[1:])
         return self.finish()
+
+    # ---- check_finite inside the fused kernels ---------------------------------------------------
+    def start_tracking(self):
+        """fin[checkpoint][view]: one int per (statement, View), set by the kernels when the statement
+        leaves a non-finite value in the View.  Row 0 is the state the Views come in with: parameter
+        Views that no kernel tests when it loads them are probed here (krn_check_finite), unless the
+        first statement overwrites them before the reference's first check."""
+        from .runtime import _DeviceBuffer
+
+        dev, b = self.dev, self.b
+        nv = max(len(b.views), 1)
+        rows = len(b.track) + 1
+        self.fin = _DeviceBuffer(dev, 4 * rows * nv)
+        _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.fin.ptr), 0, 4 * rows * nv))
+        first = next((c for c in self.plan.checkpoints if c[0] == "views"), None)
+        for p in self.plan.fn.params:
+            if not p.is_view or p.name in b.init_tested:
+                continue
+            v = self.views[p.name]
+            if v.size == 0 or v._zero or (first is not None and p.name in first[2]):
+                continue
+            dev.check_finite(v.device_ptr(dev, write=False), v.size, self.fin.ptr + 4 * b.vid(p.name))
+
+    def finite_replay(self):
+        """The reference's checks, replayed on the host from the recorded flags: after every kernel /
+        bulk statement the first View (parameters in order, then locals as declared) holding a
+        non-finite value raises; after every gather its scalar (runtime.py:624-676)."""
+        from .runtime import NonFiniteDetected
+
+        dev, b = self.dev, self.b
+        nv = max(len(b.views), 1)
+        flags = np.zeros((len(b.track) + 1, nv), dtype=np.int32)
+        dev.download(flags, self.fin.ptr)
+        slots = np.zeros(self.plan.nslots)
+        dev.download(slots, self.S.ptr)
+        order = [p.name for p in self.plan.fn.params if p.is_view]
+        bad = {name: bool(flags[0, b.vid(name)]) for name in order}
+        for cpt in self.plan.checkpoints:
+            if cpt[0] == "decl":
+                order.append(cpt[1])
+                bad[cpt[1]] = False
+            elif cpt[0] == "views":
+                for name in cpt[2]:
+                    bad[name] = bool(flags[cpt[1], b.vid(name)])
+                for name in order:
+                    if bad[name]:
+                        raise NonFiniteDetected(f"non-finite value in view '{name}'")
+            elif cpt[0] == "scalar":
+                value = float(slots[b.slot(cpt[1])]) if cpt[1] not in self.plan.an.host_scalars else float(self.H[cpt[1]])
+                if not np.isfinite(value):
+                    raise NonFiniteDetected(f"non-finite scalar {value!r}")
 
     def do_declview(self, s):
         from .runtime import ViewStorage, _index_value
@@ -599,9 +711,14 @@ class _CompiledRun:
             helper = _Run.__new__(_Run)
             helper.b, helper.views = self.b, self.views
             raise helper.error_from(st.copy())
-        if self.ret_slot is not None:
-            return float(dev.staging[64:72].view(np.float64)[0])
-        return self.host_value
+        value = float(dev.staging[64:72].view(np.float64)[0]) if self.ret_slot is not None else self.host_value
+        if self.plan.track:
+            from .runtime import NonFiniteDetected
+
+            self.finite_replay()
+            if value is not None and not np.isfinite(value):
+                raise NonFiniteDetected(f"non-finite scalar {value!r}")
+        return value
 
 
 def fusion_views(loop) -> set:

@@ -501,10 +501,12 @@ def _bulk_as_loop(stmt, an: Analysis, rank2: bool = False):
     return LoopOp(K, N.Extent(stmt.dst, 0), tuple(body), stmt, what, need_cols=need)
 
 
-def build_ops(fn, an: Analysis, windows: bool = True) -> list:
+def build_ops(fn, an: Analysis, windows: bool = True, keep_dead: bool = False) -> list:
     """Statement list -> op list.  Ops are ('loop', LoopOp) | ('gather', stmt, acc) |
     ('scalars', [stmts]) | ('hostscalar', stmt) | ('declview', stmt) | ('return', expr) |
-    ('raw', stmt) for statements the fusion pass does not model."""
+    ('raw', stmt) for statements the fusion pass does not model.  `keep_dead`: no dead-statement
+    elimination (check_finite runs: a statement nothing reads may still produce the non-finite value
+    the reference traps)."""
     ops: list = []
     bound = {p.name for p in fn.params if not p.is_view}
     run: list = []
@@ -560,7 +562,7 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
             loop = _bulk_as_loop(s, an, windows)
             ops.append(("loop", loop) if loop is not None else ("raw", s))
         elif k == "ParallelSum":
-            if s.dst not in an.live_scalars:
+            if s.dst not in an.live_scalars and not keep_dead:
                 bound.add(s.dst)
                 continue  # the sum is never read: dead statement
             ops.append(("gather", s, s.dst in bound))
@@ -570,7 +572,7 @@ def build_ops(fn, an: Analysis, windows: bool = True) -> list:
         else:
             raise TypeError(f"cannot execute {k}")
     flush()
-    return _drop_dead_fills(ops, fn, an)
+    return ops if keep_dead else _drop_dead_fills(ops, fn, an)
 
 
 def _op_views(op) -> set:

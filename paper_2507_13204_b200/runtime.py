@@ -562,6 +562,7 @@ SMEM_PRIVATE_MAX = 6144  # doubles: 48 KB of dynamic shared memory
 
 
 NO_ATOMICS = (0, 0, 0, 0, 0, 0)
+ENV_TAIL = "qiiQQqQ"  # Env: priv_rows, apol, priv_vid, okeys, ovals, on, fin (codegen._PREAMBLE)
 ORDERED_LIMIT = 1 << 31  # 32-bit keys and record numbers (krn_ordered_accumulate)
 
 
@@ -680,8 +681,8 @@ class _Run:
                 e0[i] = v.extents[0]
                 e1[i] = v.extents[1] if len(v.extents) == 2 else 1
         nh = max(len(self.b.hslots), 1)  # Env.H: unused on the statement path, but part of the layout
-        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}dqiiQQq", *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
-                           *([0.0] * nh), *atomic)
+        return struct.pack(f"{nv}Q{nv}q{nv}qQQ{nh}d" + ENV_TAIL, *ptrs, *e0, *e1, self.S.ptr, self.dev.status_ptr,
+                           *([0.0] * nh), *atomic, 0)
 
     def launch(self, name: str, n: int, extra=(), atomic=NO_ATOMICS, sequential=False):
         env = C.create_string_buffer(self.env(atomic))
@@ -1041,7 +1042,10 @@ def execute(program, fn_name: str, inputs: dict, cfg: ExecutionConfig | None = N
         if hit is not None and hit.applicable(views):
             return ExecResult(hit.run(dev, views, scalars, cfg))
     plan = _plan_for(fn)
-    if cfg.policy in ("fused", "compiled") and not cfg.check_finite and not plan.carried:
+    if cfg.policy in ("fused", "compiled") and not plan.carried and (cfg.synchronous or not cfg.check_finite):
+        # check_finite stays on the fused path: the kernels test what their statements leave behind and
+        # the reference's checks are replayed from the recorded flags (compiled.finite_replay); a function
+        # with a statement no fused kernel can watch takes the statement path inside compiled.run
         from . import compiled
 
         return ExecResult(compiled.run(dev, fn, views, scalars, cfg))

@@ -45,6 +45,26 @@ _TREE_SMEM = 128 * 8 + 32 * 8  # s_nodes + krn_final_tree's scratch
 
 
 
+class Untrackable(ValueError):
+    """check_finite cannot be folded into this fused group (a statement writes a View through
+    global memory, or scatters with hardware atomics): the call takes the statement path."""
+
+
+def _tracked_writes(b, loop, in_kernel) -> tuple:
+    """(checkpoint number, Views the statement writes) of one op of a tracked (check_finite) plan;
+    every written View must live in registers / windows of the kernel."""
+    if any(st.mode != "gather" for st in loop.sites):
+        raise Untrackable("hardware-atomic sites")
+    if loop.what == "apply":
+        written = [loop.apply_of[0]]
+    else:
+        written = sorted({a.view for a in loop.accesses() if a.write and not a.atomic})
+    for v in written:
+        if v not in in_kernel:
+            raise Untrackable(f"{v} is written through global memory")
+    return b.track[id(loop.origin)], written
+
+
 def _first_access_is_full_store(group, view, ops_with_full_range, col=None) -> bool:
     """True when, in program order, the first statement of the group touching `view`
     (column `col` of it, for a rank-2 View) is an unguarded top-level `view(i) = rhs` whose
@@ -244,6 +264,9 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             ld = "krn_ld4_rmw" if p["written"] else "krn_ld4_stream"
             w(f"        if (full) {{ krn_d4 q = {ld}(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
+        if b.track is not None and p["view"] not in b.touched_before:  # initial status of a loaded View (checkpoint 0)
+            w(f"        for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
+            b.init_tested.add(p["view"])
         w("    }")
     w("    }")
     # ---- the steps of the batch, one after the other ------------------------------------------
@@ -302,6 +325,10 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
                         b.interior = None
                     w(f"            {tgt} = acc;")
                     w("        }")
+                    if b.track is not None:
+                        cp, written = _tracked_writes(b, loop, regs)
+                        for tv in written:
+                            w(f"        krn_fin(E, {cp} * NV + {b.vid(tv)}, {regs[tv]}[e]);")
                     continue
                 sites = {id(st.stmt): st for st in loop.sites}
                 body: list = []
@@ -323,6 +350,10 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
                 w("        if (i < n) {" if (plan["max_shift"] and not interior) else "        {")
                 L.extend(body)
                 w("        }")
+                if b.track is not None:
+                    cp, written = _tracked_writes(b, loop, regs)
+                    for tv in written:
+                        w(f"        krn_fin(E, {cp} * NV + {b.vid(tv)}, {regs[tv]}[e]);")
         finally:
             b.promoted = {}
         w("    }")
@@ -577,9 +608,13 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 w(f"            if (full || (act_[e] && it_[e] < E.e0[{v}])) {{")
                 for c in lc:
                     w(f"                {r}c{c}[e] = E.v[{v}][it_[e] * ld_ + {c}];")
+                    if b.track is not None and p["view"] not in b.touched_before:
+                        w(f"                krn_fin(E, {v}, {r}c{c}[e]);")
                 w("            }")
                 w("        }")
                 w("    }")
+                if b.track is not None and p["view"] not in b.touched_before:
+                    b.init_tested.add(p["view"])
             continue
         w(f"    double {r}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
         if p["load"]:
@@ -588,6 +623,9 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
             w(f"        else {{ for (int e = 0; e < 4; ++e) if (act_[e] && it_[e] < E.e0[{v}]) {r}[e] = E.v[{v}][it_[e]]; }}")
             if p["halo"]:
                 w(f"        if (act_[4] && it_[4] < E.e0[{v}]) {r}[4] = E.v[{v}][it_[4]];")
+            if b.track is not None and p["view"] not in b.touched_before:  # initial status: own rows only (checkpoint 0)
+                w(f"        for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
+                b.init_tested.add(p["view"])
             w("    }")
     for idx in sorted(stage_reg_sites):
         w(f"    double T{idx}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
@@ -610,6 +648,11 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w(f"            for (int u = 0; u < {NQ}; ++u) {{ const krn_i64 g_ = wlo + lane_ + 32 * u; "
           f"if (lane_ + 32 * u < {WN} && g_ >= 0 && g_ < E.e0[{v}] && g_ < n_launch) {wn}r[u] = E.v[{v}][g_]; }}")
         w("        }")
+        if b.track is not None and p["view"] not in b.touched_before:  # own positions of the window only: [HLO, HLO + 128)
+            w("#pragma unroll")
+            w(f"        for (int u = 0; u < {NQ}; ++u) if (lane_ + 32 * u >= {HLO} && lane_ + 32 * u < {HLO + 128}) "
+              f"krn_fin(E, {v}, {wn}r[u]);")
+            b.init_tested.add(p["view"])
         w("    }")
 
     def emit_apply(view, sites, producer, interior: bool):
@@ -658,6 +701,25 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
             w(f"            {tgt} = acc;")
             w("            }")
 
+    def emit_tests(loop):
+        """check_finite plans: the Views this statement wrote, tested on the iteration's own slot"""
+        if b.track is None:
+            return
+        cp, written = _tracked_writes(b, loop, in_kernel_views)
+        for tv in written:
+            v = b.vid(tv)
+            if tv in wins:
+                w(f"        if (e < 4) krn_fin(E, {cp} * NV + {v}, {wins[tv]}[wq]);")
+                continue
+            rec = next(p for p in promoted if p["view"] == tv)
+            if "cols" in rec:
+                cols = sorted(c for c, wr in _columns(type("G", (), {"ops": [loop]})(), tv).items() if wr) \
+                    if loop.what != "apply" else sorted({st.column for st in loop.apply_of[1]})
+                for c in cols:
+                    w(f"        if (e < 4) krn_fin(E, {cp} * NV + {v}, {regs[tv]}c{c}[e]);")
+            else:
+                w(f"        if (e < 4) krn_fin(E, {cp} * NV + {v}, {regs[tv]}[e]);")
+
     def emit_step(interior: bool):
         # ---- windows in (values were fetched into registers by the prologue, all loads in flight at once)
         loaded = False
@@ -704,6 +766,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                         w(f"        if ({' && '.join(conds) if conds else 'true'}) {{  // deferred atomic adds landing on row i, reference order")
                         emit_apply(view, sites, producer, interior)
                         w("        }")
+                        emit_tests(loop)
                         continue
                     sites = {id(st.stmt): st for st in loop.sites}
                     body: list = []
@@ -730,6 +793,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                     L.extend(x.replace("continue;", "break;") for x in body)
                     w("        } while (0);")
                     w("        if (bad) continue;")
+                    emit_tests(loop)
                 w("    }")
                 w("    __syncwarp();")
         finally:
