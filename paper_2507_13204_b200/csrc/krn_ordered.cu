@@ -53,9 +53,8 @@ constexpr int kScanChunk = kThreads * 8;
 constexpr int kMaxWidth = 4;
 constexpr int kMaxPassBits = 10;           // digits of a partition pass
 constexpr int kMaxLocalBits = 12;          // low key bits resolved inside shared memory
-constexpr int kChunk = 2048;               // records a bucket's block stages per round
-constexpr int kSlotBits = 11;              // log2(kChunk): packed word = (low key << kSlotBits) | slot
-constexpr int kChunkSpan = kChunk / kWarps;  // consecutive chunk records ranked by one warp
+// a bucket's block stages 256 * PER records per round (PER = 8 for one value per record, 4 for wider
+// records: the staged values must leave room for 3 blocks per SM); packed word = (low key << slot bits) | slot
 constexpr u32 kNone = 0xffffffffu;
 
 __device__ __forceinline__ u32 lanemask_lt()
@@ -430,15 +429,15 @@ ord_mark(const u32 *__restrict__ keys, size_t m, int lb, u32 hmask, u32 *__restr
 
 // ---- phase B: one block per bucket ---------------------------------------------------------
 // Stable ranking pass over the packed words in[0, cnt) by the 4 bits at `shift`, inside shared
-// memory.  Thread t owns the kChunk / 256 = 8 CONSECUTIVE words [8t, 8t + 8) and counts their digits
+// memory.  Thread t owns the PER CONSECUTIVE words [PER*t, PER*t + PER) and counts their digits
 // in 16 counters of its own (plain loads and stores: no ballots, no atomics); an exclusive scan of
 // the counter matrix in (digit, thread) order - thread-major within a digit, i.e. input order - turns
 // every counter into the first output slot of that thread's words with that digit.  0.8 instead of
 // 3.3 warp instructions per record and pass compared with ballot ranking (which pays per digit BIT
 // and per 32 records; it stays the choice of the partition passes, whose digits are 7-10 bits wide).
 constexpr int kLocalBits = 4;
-constexpr int kPerThread = kChunk / kThreads;  // 8
 
+template <int kPerThread>
 __device__ __forceinline__ void local_pass4(const u32 *in, u32 *out, int cnt, int shift, unsigned short *c16,
                                             u32 *s_wsum)
 {
@@ -447,9 +446,10 @@ __device__ __forceinline__ void local_pass4(const u32 *in, u32 *out, int cnt, in
     for (int d = 0; d < 16; ++d) c16[d * kThreads + t] = 0;
     u32 w[kPerThread];
     unsigned char r[kPerThread];
-    {
-        const uint4 a = reinterpret_cast<const uint4 *>(in)[2 * t], b = reinterpret_cast<const uint4 *>(in)[2 * t + 1];
-        w[0] = a.x, w[1] = a.y, w[2] = a.z, w[3] = a.w, w[4] = b.x, w[5] = b.y, w[6] = b.z, w[7] = b.w;
+#pragma unroll
+    for (int g = 0; g < kPerThread / 4; ++g) {
+        const uint4 a = reinterpret_cast<const uint4 *>(in)[(kPerThread / 4) * t + g];
+        w[4 * g] = a.x, w[4 * g + 1] = a.y, w[4 * g + 2] = a.z, w[4 * g + 3] = a.w;
     }
 #pragma unroll
     for (int j = 0; j < kPerThread; ++j) {
@@ -515,13 +515,15 @@ struct Cols {
 // to column cols.c[l] of it (sites that name the literal columns of one row: one record instead of
 // WIDTH) - different locations, so their mutual order is immaterial, while every location still
 // receives its records in queue order.  target_size = number of keys (elements / rows).
-template <int WIDTH, bool LANES>
+template <int WIDTH, bool LANES, int PER>
 __global__ void __launch_bounds__(kThreads)
 ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, size_t m,
                 double *__restrict__ target, size_t target_size, int ncols, Cols cols, int lb,
                 const u32 *__restrict__ start, const u32 *__restrict__ end)
 {
     constexpr int width = WIDTH;
+    constexpr int kChunk = kThreads * PER;
+    constexpr int kSlotBits = PER == 8 ? 11 : 10;
     const u32 b = blockIdx.x;
     const u32 s0 = start[b];
     if (s0 == kNone) return;
@@ -554,7 +556,7 @@ ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, s
         __syncthreads();
         u32 *fin = wa, *other = wb;
         for (int pass = 0; pass < passes; ++pass) {
-            local_pass4(fin, other, cnt, kSlotBits + kLocalBits * pass, c16, s_wsum);
+            local_pass4<PER>(fin, other, cnt, kSlotBits + kLocalBits * pass, c16, s_wsum);
             u32 *swap = fin;
             fin = other;
             other = swap;
@@ -746,8 +748,8 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
     const int nbits = bit_length(target_size - 1);  // bits of the largest real key
     int lb = nbits - kMaxPassBits;
     if (lb < 0) lb = 0;
-    int lb_max = kMaxLocalBits;  // a bucket's targets (rows x ncols doubles) take at most 48 KB of shared memory
-    while (lanes && lb_max > 0 && (size_t(ncols) << lb_max) > 6144) --lb_max;
+    int lb_max = kMaxLocalBits;  // a bucket's targets: 32 KB of shared memory (rows x ncols doubles: 24 KB)
+    while (lanes && lb_max > 0 && (size_t(ncols) << lb_max) > 3072) --lb_max;
     if (lb > lb_max) lb = lb_max;
     int high = nbits - lb;
     if (high < 1) high = 1;
@@ -821,16 +823,18 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
         const size_t blocks = (records + 4 * kThreads - 1) / (4 * kThreads);
         ord_mark<<<unsigned(blocks), kThreads, 0, ctx->stream>>>(src_keys, records, lb, hmask, start, end);
         const size_t tile_elems = ((size_t(lanes ? ncols : 1) << lb) + 1) & ~size_t(1);
-        const size_t smem = tile_elems * 8 + size_t(width) * kChunk * 8 + 2 * size_t(kChunk) * 4 + size_t(16) * kThreads * 2;
+        const size_t chunk = size_t(kThreads) * (width == 1 ? 8 : 4);
+        const size_t smem = tile_elems * 8 + size_t(width) * chunk * 8 + 2 * chunk * 4 + size_t(16) * kThreads * 2;
         Cols cc;
         for (int l = 0; l < kMaxWidth; ++l) cc.c[l] = (lanes && l < width) ? cols[l] : 0;
         // real buckets only: ids beyond the last target hold sites that did not execute
         const size_t real = ((target_size - 1) >> lb) + 1;
 #define KRN_FOLD(W, L)                                                                                            \
     do {                                                                                                          \
-        e = cudaFuncSetAttribute(ord_bucket_fold<W, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));  \
+        constexpr int per = W == 1 ? 8 : 4;                                                                       \
+        e = cudaFuncSetAttribute(ord_bucket_fold<W, L, per>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         if (e == cudaSuccess)                                                                                     \
-            ord_bucket_fold<W, L><<<unsigned(real), kThreads, smem, ctx->stream>>>(                               \
+            ord_bucket_fold<W, L, per><<<unsigned(real), kThreads, smem, ctx->stream>>>(                          \
                 src_keys, src_vals, records, d_target, target_size, ncols, cc, lb, start, end);                   \
     } while (0)
         switch (width * 2 + (lanes ? 1 : 0)) {
