@@ -16,7 +16,7 @@ def _load(name):
 
 
 def test_committed_bench_line_has_the_contract_keys():
-    d = _load("r1_bench_n1.json")
+    d = _load("r2_bench_n1.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
               "gpu_launches", "clocks"):
@@ -35,15 +35,26 @@ def test_committed_bench_line_has_the_contract_keys():
     assert d["steps"] >= 1 and d["warmup"] >= 3
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     # BASELINE.json configs: [1] headline, [2] sweep, [3] 2-D Views
-    assert d["ratio_grad_primal"] <= 2.17 and "headline" in d and len(d["sweep"]) == 4 and "two_d_views" in d
+    ratio = d["ratio_grad_primal"]  # one object: the paper's size (latency bound) and the bandwidth-bound pair
+    assert ratio["at_10k_entries_fused_one_launch_per_side"] <= 2.17 and ratio["at_10k_entries_statement_granular"] <= 2.17
+    assert ratio["large_n_zero_shadows_40_over_24_bytes"] <= 2.17 < ratio["compulsory_bytes_ratio_accumulate"]
+    assert "headline" in d and len(d["sweep"]) == 4 and "two_d_views" in d
+    acc = d["two_d_views"]["gather_rows_rank2"]["accumulation"]  # configs[3]: both accumulation policies
+    assert acc["ordered"]["bit_identical_to_reference"] and not acc["hardware_atomics"]["bit_identical_to_reference"]
+    runs = c["interpreter"]["runs"]
+    assert {(r["rows"], r["threads"] == 1) for r in runs} == {(10_000, True), (10_000, False), (100_000, True), (100_000, False)}
+    assert d["generated_kernels"]["ld256"] is True
 
 
 def test_committed_reference_arm_line():
-    d = _load("r1_bench_reference_arm.json")
-    assert d["impl"] == "reference" and d["metric"] == _load("r1_bench_n1.json")["metric"]
+    d = _load("r2_bench_reference_arm.json")
+    mine = _load("r2_bench_n1.json")
+    assert d["impl"] == "reference" and d["metric"] == mine["metric"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["e2e"]["value"] == d["value"] and d["cpu_baseline"]["value"] == d["value"]
-    assert d["config"] == _load("r1_bench_n1.json")["config"]
+    # the arm times the size its config names (round 1 labelled 125 M rows and timed 25 M)
+    assert d["config"]["rows_per_gpu"] == mine["config"]["rows_per_gpu"] and d["config"]["rate_normalised"] is False
+    assert d["config"]["workload"] == mine["config"]["workload"]
 
 
 def test_reference_arm_runs_here():
