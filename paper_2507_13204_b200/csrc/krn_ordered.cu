@@ -744,7 +744,10 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
 
     // Buckets of 2^lb targets; `high` bits above them are sorted in HBM.  At least 2^10 buckets when
     // the target is large enough (one block per bucket must fill the machine); the all-ones key of a
-    // site that did not execute must fall into a bucket beyond the last real one.
+    // site that did not execute must fall into a bucket beyond the last real one.  (Measured: making lb
+    // as large as shared memory allows so that targets of up to 4 M elements need ONE 9-10 bit pass is
+    // slower than two balanced 5-6 bit passes - 1 M targets 0.74 against 0.61 ms: a 10-bit pass ranks
+    // with ten ballots, leaves the tile in runs of four records, and the fold gets a quarter of the blocks.)
     const int nbits = bit_length(target_size - 1);  // bits of the largest real key
     int lb = nbits - kMaxPassBits;
     if (lb < 0) lb = 0;
