@@ -271,7 +271,8 @@ def assign_ordered(site_lists) -> list:
             groups, width = len(heads), max(1 + len(st.merged) for st in heads)
             for g, st in enumerate(heads):
                 st.ord = (key_off, val_off, groups, width, g)
-            entries.append(dict(view=view, groups=groups, width=width, key_off=key_off, val_off=val_off, cols=cols))
+            entries.append(dict(view=view, groups=groups, width=width, key_off=key_off, val_off=val_off, cols=cols,
+                                guarded=any(st.guards for st in every)))
             key_off += groups
             val_off += groups * width
     return entries

@@ -393,6 +393,8 @@ ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in,
 #pragma unroll
         for (int r = 0; r < kItems; ++r) {
             const u32 t = u32(warp) * kWarpSpan + u32(r) * 32 + lane;
+            // (the values of a site that did not execute travel along unread: the producer of the queue
+            // clears them when it has guarded sites, OrderedStage in runtime.py)
             if (t < live) s_val[slot[r]] = src[t];
         }
         __syncthreads();

@@ -578,6 +578,10 @@ class OrderedStage:
         self.vals = _DeviceBuffer(dev, 8 * n * sum(e["groups"] * e["width"] for e in entries))
         # all-ones key = "this site did not execute" (guarded sites, iterations that failed a check)
         _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.keys.ptr), 0xFF, 4 * n * groups))
+        for e in entries:  # values of guarded sites that do not execute are never written: defined, not garbage
+            if e.get("guarded"):
+                _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.vals.ptr + 8 * e["val_off"] * n), 0,
+                                               8 * n * e["groups"] * e["width"]))
 
     @staticmethod
     def feasible(entries, views: dict, n: int) -> bool:

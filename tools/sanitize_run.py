@@ -17,7 +17,7 @@ rng = np.random.default_rng(0)
 ran = 0
 for stem in ("laplacian", "stencil_smooth", "rowscale_rank2", "gather_indirect", "mean_shift", "copy_chain",
              "window_wide", "window_partial", "window_war", "window_scatter", "rank2_bulk", "gather_rows_rank2",
-             "taped_overwrites"):
+             "taped_overwrites", "stride2_scatter", "stride2_collide", "rank2_row_offset"):
     prog = krn.load_program(stem)
     fn = prog.functions[0]
     for n in (1, 129, 1030, 9000):
@@ -27,6 +27,8 @@ for stem in ("laplacian", "stencil_smooth", "rowscale_rank2", "gather_indirect",
                 data[p.name] = 0.75
             elif p.name == "idx":
                 data[p.name] = rng.integers(0, n, size=n).astype(np.float64)
+            elif p.name == "fine":
+                data[p.name] = rng.normal(size=2 * n + 1)
             elif p.type.rank == 2:
                 data[p.name] = rng.normal(size=(n, 3))
             else:
@@ -46,5 +48,40 @@ for stem in ("laplacian", "stencil_smooth", "rowscale_rank2", "gather_indirect",
                 call[sp.name] = ViewStorage.zeros(sp.name, np.shape(data[w]))
             krn.execute(gp, gfn.name, call, cfg)
             ran += 1
+            if n == 1030:  # the same gradient with check_finite on the fused path and with hardware reductions
+                for extra in (ExecutionConfig(policy=policy, check_finite=True),
+                              ExecutionConfig(policy=policy, deterministic_reduction=False)):
+                    call = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in data.items()}
+                    for sp, w in zip(gfn.params[len(fn.params):], wrt):
+                        call[sp.name] = ViewStorage.zeros(sp.name, np.shape(data[w]))
+                    krn.execute(gp, gfn.name, call, extra)
+# the ordered queue through the raw ABI: holes, hot keys, widths, row records
+import ctypes as C  # noqa: E402
+
+from paper_2507_13204_b200 import _cabi  # noqa: E402
+
+dev = krn.Device.get()
+for records, size in ((1, 1), (4097, 300), (70_001, 5000), (70_001, 1 << 20)):
+    keys = rng.integers(0, size, size=records).astype(np.uint32)
+    keys[rng.random(records) < 0.2] = 0xFFFFFFFF
+    keys[: records // 3] = 7 % size
+    for width in (1, 2, 4):
+        vals = rng.normal(size=records * width)
+        bufs = [dev.alloc(8 * size), dev.alloc(4 * records), dev.alloc(8 * records * width)]
+        dev.fill(bufs[0], size, 0.0)
+        dev.upload(bufs[1], keys)
+        dev.upload(bufs[2], vals)
+        _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, C.c_void_p(bufs[0]), size, C.c_void_p(bufs[1]),
+                                                   C.c_void_p(bufs[2]), records, width))
+        if size % 3 == 0:
+            cols = (C.c_int * 3)(2, 0, 1)
+            k2 = np.where(keys == 0xFFFFFFFF, keys, keys % (size // 3)).astype(np.uint32)
+            dev.upload(bufs[1], k2)
+            if width * records >= 3 * records:
+                _cabi.check(dev.lib.krn_ordered_accumulate_rows(dev.h, C.c_void_p(bufs[0]), size // 3, 3, cols, 3,
+                                                                C.c_void_p(bufs[1]), C.c_void_p(bufs[2]), records))
+        dev.sync()
+        for b in bufs:
+            dev.free(b)
 krn.Device.get().sync()
 print("sanitize_run: done,", ran, "gradient runs")
