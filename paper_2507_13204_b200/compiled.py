@@ -80,7 +80,8 @@ class CompiledPlan:
         self.fn = fn
         self.track = track
         an = self.an = fusion.Analysis(fn)
-        self.schedule = fusion.form_groups(fusion.build_ops(fn, an, windows, keep_dead=track), an, windows)
+        self.schedule = fusion.form_groups(fusion.build_ops(fn, an, windows, keep_dead=track), an, windows,
+                                           side_gathers=track)
         self.windowed = any(item[0] == "group" and item[1].windowed for item in self.schedule)
         b = self.builder = codegen.ModuleBuilder(fn, host_scalars=an.host_scalars)
         self.checkpoints: list = []
@@ -115,6 +116,8 @@ class CompiledPlan:
                 item[1].fresh = frozenset(fresh)
                 fresh -= _views_of(item)
                 touched_now = _views_of(item)
+                for stmt, _, _ in item[1].sides:
+                    b.slot(stmt.dst)
                 if item[1].windowed:
                     plan = tilegen.plan_window_group(b, item[1], an, later)
                     self.steps.append(("group", item[1], tilegen.window_kernel(b, item[1], f"g{idx}", plan, an)))
@@ -154,8 +157,12 @@ class CompiledPlan:
         elif tag == "gather":
             self.checkpoints.append(("scalar", item[1].dst))
         elif tag == "group":
-            seen = []
-            for loop in item[1].ops:
+            g = item[1]
+            seen = []  # [checkpoint, Views] runs and side-gather scalars, in statement order
+            for k, loop in enumerate(g.ops):
+                for stmt, _, pos in g.sides:
+                    if pos == k:
+                        seen.append(("scalar", stmt.dst))
                 cp = b.track[id(loop.origin)]
                 written = [loop.apply_of[0]] if loop.what == "apply" else \
                     sorted({a.view for a in loop.accesses() if a.write and not a.atomic})
@@ -163,10 +170,13 @@ class CompiledPlan:
                     seen[-1][1].update(written)
                 else:
                     seen.append((cp, set(written)))
-            for cp, written in seen:
-                self.checkpoints.append(("views", cp, sorted(written)))
-            if item[1].gather is not None:
-                self.checkpoints.append(("scalar", item[1].gather[0].dst))
+            for stmt, _, pos in g.sides:
+                if pos == len(g.ops):
+                    seen.append(("scalar", stmt.dst))
+            for first, second in seen:
+                self.checkpoints.append(("scalar", second) if first == "scalar" else ("views", first, sorted(second)))
+            if g.gather is not None:
+                self.checkpoints.append(("scalar", g.gather[0].dst))
 
 
 _plans: dict = {}
@@ -586,20 +596,28 @@ class _CompiledRun:
         # tree, a ticket and a partial per block and run best with 8 (4: -4%, 1: -50%); kernels without
         # one run best with 2 (8: -2..4%, 1: -2..5%).  Small problems are latency bound: as many
         # blocks as possible.
-        steps = 1 if n_launch <= (1 << 20) else (8 if g.gather is not None else 2)
+        reduces = g.gather is not None or bool(g.sides)
+        steps = 1 if n_launch <= (1 << 20) else (8 if reduces else 2)
         nblocks = (n_launch + 1024 * steps - 1) // (1024 * steps)
-        if g.gather is not None:
-            # the context's reduction workspace: no allocation inside the launch sequence
+        side_args = [C.c_void_p(0), C.c_int(0)] * fusion.MAX_SIDES
+        if reduces:
+            # the context's reduction workspace: no allocation inside the launch sequence; one run of
+            # nblocks partials for the fused gather, one more per side gather
             pa, sc, tk = C.c_void_p(), C.c_void_p(), C.c_void_p()
-            _cabi.check(dev.lib.krn_reduce_workspace(dev.h, nblocks * max(1, recipe.get("gather_cols", 0)),
-                                                     C.byref(pa), C.byref(sc), C.byref(tk)))
+            _cabi.check(dev.lib.krn_reduce_workspace(
+                dev.h, nblocks * (max(1, recipe.get("gather_cols", 0)) + len(g.sides)), C.byref(pa), C.byref(sc),
+                C.byref(tk)))
             extra += [pa, sc, tk, C.c_void_p(red_out), C.c_int(acc)]
+            for j, (stmt, accumulate, _) in enumerate(g.sides):
+                side_args[2 * j] = C.c_void_p(self.S.ptr + 8 * self.b.slot(stmt.dst))
+                side_args[2 * j + 1] = C.c_int(int(accumulate))
         else:
             extra += [C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_void_p(0), C.c_int(0)]
         extra.append(C.c_int(steps))
         if recipe.get("window"):
             order = list(recipe["alt"]) + [None] * (fusion.MAX_ALT - len(recipe["alt"]))
             extra += [C.c_void_p(alt_bufs[v].ptr if v is not None else 0) for v in order]
+        extra += side_args
         self.launch_tile(recipe["name"], nblocks, env, extra)
         for name, buf in alt_bufs.items():
             self.views[name]._adopt(buf)

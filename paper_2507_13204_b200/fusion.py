@@ -365,6 +365,10 @@ class Group:
     name: str = ""
     fresh: frozenset = frozenset()  # local Views still untouched (all +0.0) when the group starts
     windowed: bool = False  # formed through window_plan: runs as a window kernel (tilegen.window_kernel)
+    # check_finite plans: gathers whose result nothing reads (the dead forward sum of a gradient) but whose
+    # value the reference checks - reduced as a SIDE output of the kernel, which goes on:
+    # (ParallelSum stmt, accumulate, number of ops of the group that precede it)
+    sides: list = _dc.field(default_factory=list)
 
 
 class Analysis:
@@ -723,7 +727,10 @@ def _reads_scalar(group: "Group", name: str) -> bool:
     return False
 
 
-def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
+MAX_SIDES = 2
+
+
+def form_groups(ops: list, an: Analysis, windows: bool = True, side_gathers: bool = False) -> list:
     """Greedy left-to-right grouping.  Returns a schedule of
     ('group', Group) | the non-loop ops unchanged.  `windows`: also merge across
     neighbour dependencies when a halo-recompute plan exists (window_plan)."""
@@ -787,6 +794,10 @@ def form_groups(ops: list, an: Analysis, windows: bool = True) -> list:
                         and group_columns(g.ops, src) == set(range(len(group_columns(g.ops, src))))
                 elif an.rank.get(src) != 1:
                     fusable = False
+                if fusable and side_gathers and an.rank.get(src) == 1 and stmt.dst not in an.live_scalars \
+                        and len(g.sides) < MAX_SIDES:
+                    g.sides.append((stmt, op[2], len(g.ops)))  # the group stays open
+                    continue
                 if fusable:
                     g.gather = (stmt, op[2])
                     close()

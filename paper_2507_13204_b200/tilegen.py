@@ -198,8 +198,13 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     w(f"#ifndef KRN_MINB_{name}\n#define KRN_MINB_{name}\n#endif")  # see window_kernel
     w(f'extern "C" __global__ void __launch_bounds__(256 KRN_MINB_{name}) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
       "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
-      "unsigned int *ticket, double *red_out, int accumulate, int steps)")
+      "unsigned int *ticket, double *red_out, int accumulate, int steps"
+      ", double *side_out0, int side_acc0, double *side_out1, int side_acc1)")
     w("{")
+    w("    (void)side_out0; (void)side_acc0; (void)side_out1; (void)side_acc1;")
+    sides = list(group.sides)
+    for j in range(len(sides)):
+        w(f"    __shared__ double s_side{j}[128];  // [warp][step]: nodes of side reduction {j}")
     strided = plan["strided"]
     # a warp owns 128*steps consecutive iterations, a block 1024*steps (an aligned power-of-two
     # chunk of the reduction tree); `steps` > 1 amortises block start-up and the block-level
@@ -280,6 +285,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w(f"    double {regs[p['view']]}[4] = {{0.0, 0.0, 0.0, 0.0}};")
     for (_, idx) in plan["stage_cols"]:
         w(f"    double T{idx}[4] = {{0.0, 0.0, 0.0, 0.0}};")
+    for j in range(len(sides)):
+        w(f"    double SG{j}[4] = {{0.0, 0.0, 0.0, 0.0}};  // side reduction {j}: the source as it is at that statement")
     # ---- body ------------------------------------------------------------------------
     # interior step: every iteration of the warp (and every iteration an apply loop looks back or
     # ahead to) lies far enough inside the range for the index guards to be decided at compile time
@@ -297,7 +304,12 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w("        if (i >= n_launch) continue;")
         b.promoted = regs
         try:
-            for loop in group.ops:
+            for k_op, loop in enumerate(list(group.ops) + [None]):
+                for j, (sstmt, _, pos) in enumerate(sides):
+                    if pos == k_op:
+                        w(f"        SG{j}[e] = {regs[sstmt.src]}[e];")
+                if loop is None:
+                    break
                 if loop.what == "apply":
                     view, sites, producer = loop.apply_of
                     v, r = b.vid(view), regs.get(view)
@@ -395,6 +407,16 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w("        double node = krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));")
         w(_TREE_PUSH)
         w("    }")
+    for j in range(len(sides)):
+        w("    {")
+        w("        double R[4];")
+        w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = SG{j}[e]; }}")
+        w("        else { for (int e = 0; e < 4; ++e) R[e] = (KRN_IT(e) < n) ? "
+          f"SG{j}[e] : krn_tree_pad((krn_u64)KRN_IT(e), (krn_u64)n); }}")
+        w("        double node = " + ("krn_warp_tree4(R[0], R[1], R[2], R[3]);" if strided else
+                                      "krn_warp_tree((R[0] + R[1]) + (R[2] + R[3]));"))
+        w(f"        if (lane_ == 0) s_side{j}[(threadIdx.x >> 5) * steps + t] = node;")
+        w("    }")
     w("    }  // step of the batch")
     w("    }  // steps")
     _specialise_interior_chunks(
@@ -407,21 +429,38 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     w("#undef KRN_IT")
     if direct:
         w("    krn_priv_end(E);")
-    if gather is not None:
-        w("    {")
-        w("        const int warp = threadIdx.x >> 5;")
-        w("        __syncthreads();")
-        w("        if (warp == 0) { double v = krn_smem_tree(s_nodes, 8 * steps, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
-        w("        if (krn_last_block(ticket, gridDim.x)) {")
-        w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
-        w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
-        w("        }")
-        w("    }")
+    if gather is not None or sides:
+        _emit_reduce_epilogue(w, gather is not None, len(sides), "threadIdx.x >> 5")
     w("}")
     b.parts.append("\n".join(L))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
                 gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct,
-                ordered=ordered, static_smem=_TREE_SMEM if gather is not None else 0)
+                ordered=ordered, static_smem=(_TREE_SMEM if (gather is not None or sides) else 0) + 1024 * len(sides))
+
+
+def _emit_reduce_epilogue(w, main: bool, nsides: int, warp_expr: str, partial_slots: int = 1):
+    """Block partial(s) -> arrival ticket -> the last block folds the partials of every reduction of the
+    kernel (the fused gather and the side reductions of a check_finite plan), one after the other."""
+    w("    {")
+    w(f"        const int warp = {warp_expr};")
+    w("        __syncthreads();")
+    w("        if (warp == 0) {")
+    if main:
+        w("            { double v = krn_smem_tree(s_nodes, 8 * steps, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
+    for j in range(nsides):
+        w(f"            {{ double v = krn_smem_tree(s_side{j}, 8 * steps, lane_); "
+          f"if (lane_ == 0) partials[(krn_i64)gridDim.x * {partial_slots + j} + blockIdx.x] = v; }}")
+    w("        }")
+    w("        if (krn_last_block(ticket, gridDim.x)) {")
+    if main:
+        w("            { double root = krn_final_tree(partials, scratch, gridDim.x);")
+        w("              if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root; }")
+    for j in range(nsides):
+        w("            __syncthreads();  // krn_final_tree's scratch is reused")
+        w(f"            {{ double root = krn_final_tree(partials + (krn_i64)gridDim.x * {partial_slots + j}, scratch, gridDim.x);")
+        w(f"              if (threadIdx.x == 0) *side_out{j} = (side_acc{j} ? *side_out{j} : 0.0) + root; }}")
+    w("        }")
+    w("    }")
 
 
 # ---------------------------------------------------------------------------------------
@@ -557,9 +596,13 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     w(f'extern "C" __global__ void __launch_bounds__(256 KRN_MINB_{name}) {name}(Env E, krn_i64 n, krn_i64 n_launch, '
       "krn_i64 n_safe, unsigned zero_mask, double *stage, krn_i64 ld, double *partials, double *scratch, "
       "unsigned int *ticket, double *red_out, int accumulate, int steps, double *alt0, double *alt1, "
-      "double *alt2, double *alt3)")
+      "double *alt2, double *alt3, double *side_out0, int side_acc0, double *side_out1, int side_acc1)")
     w("{")
     w("    (void)alt0; (void)alt1; (void)alt2; (void)alt3;")
+    w("    (void)side_out0; (void)side_acc0; (void)side_out1; (void)side_acc1;")
+    sides = list(group.sides)
+    for j in range(len(sides)):
+        w(f"    __shared__ double s_side{j}[128];  // [warp][step]: nodes of side reduction {j}")
     w("    const int lane_ = threadIdx.x & 31, warp_ = threadIdx.x >> 5;")
     for wn in list(wins.values()) + list(stage_win_sites.values()):
         w(f"    __shared__ double {wn}_[8][{WN}];")
@@ -629,6 +672,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
             w("    }")
     for idx in sorted(stage_reg_sites):
         w(f"    double T{idx}[5] = {{0.0, 0.0, 0.0, 0.0, 0.0}};")
+    for j in range(len(sides)):
+        w(f"    double SG{j}[4] = {{0.0, 0.0, 0.0, 0.0}};  // side reduction {j}: the source as it is at that statement")
     # window contents: fetched into registers here so that every global load of the step is in
     # flight before the first one is consumed
     NQ = (WN + 31) // 32
@@ -701,6 +746,13 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
             w(f"            {tgt} = acc;")
             w("            }")
 
+    def emit_side_capture(position):
+        """side reductions that sit before op `position`: copy the source's current value (own slots)"""
+        for j, (sstmt, _, pos) in enumerate(sides):
+            if pos == position:
+                val = f"{regs[sstmt.src]}[e]" if sstmt.src in regs else f"{wins[sstmt.src]}[wq]"
+                w(f"        if (e < 4) SG{j}[e] = {val};")
+
     def emit_tests(loop):
         """check_finite plans: the Views this statement wrote, tested on the iteration's own slot"""
         if b.track is None:
@@ -751,6 +803,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 w("        const int wq = wq_[e]; (void)wq;")
                 w("        bool bad = false;")
                 for k in phase:
+                    emit_side_capture(k)
                     loop = group.ops[k]
                     hlo, hhi = wp.halo[k]
                     conds = []
@@ -794,6 +847,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                     w("        } while (0);")
                     w("        if (bad) continue;")
                     emit_tests(loop)
+                if phase is wp.phases[-1]:
+                    emit_side_capture(len(group.ops))
                 w("    }")
                 w("    __syncwarp();")
         finally:
@@ -868,6 +923,14 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
         w(_TREE_PUSH)
         w("    }")
+    for j in range(len(sides)):
+        w("    {")
+        w("        double R[4];")
+        w(f"        if (full) {{ for (int e = 0; e < 4; ++e) R[e] = SG{j}[e]; }}")
+        w(f"        else {{ for (int e = 0; e < 4; ++e) R[e] = (it_[e] < n) ? SG{j}[e] : krn_tree_pad((krn_u64)it_[e], (krn_u64)n); }}")
+        w("        double node = krn_warp_tree4(R[0], R[1], R[2], R[3]);")
+        w(f"        if (lane_ == 0) s_side{j}[warp_ * steps + t] = node;")
+        w("    }")
     w("    __syncwarp();")
     w("    }  // steps")
     _specialise_interior_chunks(
@@ -910,15 +973,8 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
         w("        }")
         w("    }")
-    elif gather is not None:
-        w("    {")
-        w("        __syncthreads();")
-        w("        if (warp_ == 0) { double v = krn_smem_tree(s_nodes, 8 * steps, lane_); if (lane_ == 0) partials[blockIdx.x] = v; }")
-        w("        if (krn_last_block(ticket, gridDim.x)) {")
-        w("            double root = krn_final_tree(partials, scratch, gridDim.x);")
-        w("            if (threadIdx.x == 0) *red_out = (accumulate ? *red_out : 0.0) + root;")
-        w("        }")
-        w("    }")
+    elif gather is not None or sides:
+        _emit_reduce_epilogue(w, gather is not None, len(sides), "warp_")
     w("}")
     b.parts.append("\n".join(L))
     every = promoted + windows
@@ -926,5 +982,5 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 gather=gather, max_shift=plan["max_shift"],
                 elided_views=sorted(elided | {p["view"] for p in windows}), atomic_views=direct, ordered=ordered,
                 window=True, alt=alts, hlo=HLO, hhi=HHI, gather_cols=gcols,
-                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites)) + (_TREE_SMEM if gather is not None else 0)
-                + 8 * (8 * 128 + 8) * gcols)
+                static_smem=8 * 8 * WN * (len(wins) + len(stage_win_sites))
+                + (_TREE_SMEM if (gather is not None or sides) else 0) + 1024 * len(sides) + 8 * (8 * 128 + 8) * gcols)
