@@ -67,4 +67,17 @@ print(f"energy gradient    : {dev.launches() - before} kernel launch(es) for "
 probe = {"u": [0, 1, n // 2, n - 1]}
 fd = krn.finite_difference_gradient(mine, "energy", {"u": u}, ("u",), entries=probe)["u"]
 print(f"finite differences : {fd}  vs AD {du[probe['u']]}")
+
+# 5. a NON-injective scatter (the adjoint of x(idx(i))): the reference applies its queue of atomic_adds in
+#    (iteration, program order); so does the default policy here (stable partition by target + in-order
+#    fold on the GPU), which makes the gradient bit-identical to the reference and to itself on every run.
+#    deterministic_reduction=False trades that for hardware fp64 reductions (relative 1e-12).
+gather = krn.load_program("gather_indirect")
+m = min(n, 1 << 20)
+xs, idx = rng.normal(size=m), rng.integers(0, m, size=m).astype(np.float64)
+runs = [krn.ad_gradient(gather, "gatherSquares", {"x": xs, "idx": idx}, ("x",))["x"].copy() for _ in range(2)]
+fast = krn.ad_gradient(gather, "gatherSquares", {"x": xs, "idx": idx}, ("x",),
+                       cfg=krn.ExecutionConfig(deterministic_reduction=False))["x"]
+print(f"indirect scatter   : two runs identical = {np.array_equal(runs[0], runs[1])}; hardware reductions differ by at most "
+      f"{np.max(np.abs(fast - runs[0]) / np.maximum(np.abs(runs[0]), 1e-300)):.1e} (relative)")
 print("done")

@@ -99,3 +99,71 @@ def test_order_dependent_kernels_are_recognised():
         prog = krn.load_program(stem)
         for fn in (prog.functions[0], _grad(stem)):
             assert not _plan_for(fn).carried
+
+
+def test_injective_affine_targets_are_updated_directly():
+    """general affine gather form (row N2): sites `a*i + c` on one View with one writing iteration per
+    location are 'direct'; sites that share a residue mod a with different constants are not"""
+    from paper_2507_13204_b200 import compiled
+
+    def modes(stem, wrt):
+        prog = krn.load_program(stem)
+        g = krn.differentiate(prog, prog.functions[0].name, wrt).functions[-1]
+        out = {}
+        for loop in _loops(g):
+            for st in codegen.plan_atomics(loop):
+                out.setdefault(st.view, set()).add(st.mode)
+        return g, out
+
+    g, m = modes("stride2_scatter", ("fine", "w"))
+    assert m == {"_d_fine": {"direct"}, "_d_w": {"gather"}}
+    assert compiled.plan_for(g).launch_count == 1  # the in-order update lives inside the window kernel
+    g, m = modes("stride2_collide", ("fine", "w"))
+    assert m == {"_d_fine": {"atomic"}, "_d_w": {"gather"}}  # 2i - 1 and 2i + 1 meet: the ordered queue
+    g, m = modes("rank2_row_offset", ("m", "r"))
+    assert m == {"_d_m": {"gather"}} and compiled.plan_for(g).launch_count == 1
+    # reversal: one site, a = -1 -> direct; two sites on a reversed index with different constants -> not
+    p = krn.parse("""fn f(v: view<f64,1>, a: view<f64,1>, b: view<f64,1>) {
+        parallel_for i in 0..extent(v, 0) {
+            atomic_add(a(extent(v, 0) - 1 - i), v(i));
+            atomic_add(b(extent(v, 0) - 1 - i), v(i));
+            if (i != 0) { atomic_add(b(extent(v, 0) - i), v(i)); }
+        } }""")
+    got = {st.view: st.mode for st in codegen.plan_atomics(p.functions[0].body[0])}
+    assert got == {"a": "direct", "b": "atomic"}
+    # a kernel that also READS the target must not update it early (deferral)
+    p = krn.parse("""fn f(v: view<f64,1>, a: view<f64,1>) {
+        parallel_for i in 0..extent(v, 0) { v(i) = a(2 * i); atomic_add(a(2 * i + 1), v(i)); } }""")
+    assert [st.mode for st in codegen.plan_atomics(p.functions[0].body[0])] == ["staged_atomic"]
+
+
+def test_ordered_queue_layout():
+    """records of the ordered policy: groups per iteration in program order, merged sites share a
+    record, sites on the literal columns of one row share a ROW record"""
+    gi = _loops(_grad("gather_indirect"))[1]
+    sites = codegen.plan_atomics(gi)
+    assert codegen.assign_ordered([sites]) == [dict(view="_d_x", groups=1, width=2, key_off=0, val_off=0, cols=None,
+                                                    guarded=False)]
+    assert sites[0].ord == (0, 0, 1, 2, 0) and sites[1].absorbed
+    prog = krn.load_program("gather_rows_rank2")
+    g = krn.differentiate(prog, "rowGather", ("q", "w")).functions[-1]
+    sites = codegen.plan_atomics(_loops(g)[1])
+    assert [(s.lanes, s.absorbed) for s in sites] == [(True, False), (False, True), (False, True)]
+    assert codegen.assign_ordered([sites]) == [dict(view="_d_q", groups=1, width=3, key_off=0, val_off=0, cols=(0, 1, 2),
+                                                    guarded=False)]
+    # two targets, a guarded site, lane groups with DIFFERENT column sets: back to one record per site
+    p = krn.parse("""fn f(idx: view<f64,1>, v: view<f64,1>, m: view<f64,2>, a: view<f64,1>) {
+        parallel_for i in 0..extent(idx, 0) {
+            atomic_add(m(idx(i), 0), v(i)); atomic_add(m(idx(i), 2), v(i));
+            if (i != 0) { atomic_add(a(idx(i)), v(i)); }
+            atomic_add(m(idx(i), 1), v(i)); atomic_add(m(idx(i), 2), v(i));
+        } }""")
+    sites = codegen.plan_atomics(p.functions[0].body[0])
+    entries = codegen.assign_ordered([sites])
+    assert entries == [dict(view="m", groups=4, width=1, key_off=0, val_off=0, cols=None, guarded=False),
+                       dict(view="a", groups=1, width=1, key_off=4, val_off=4, cols=None, guarded=True)]
+    assert not any(s.absorbed or s.lanes for s in sites)
+    src = codegen.ModuleBuilder(p.functions[0])
+    src.kernel(p.functions[0].body[0], "k0")
+    text = src.source()
+    assert text.count("krn_ord_put(E, 0, 0, 4, 1,") == 4 and text.count("krn_ord_put(E, 4, 4, 1, 1, 0,") == 1
