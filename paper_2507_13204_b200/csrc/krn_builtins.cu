@@ -29,7 +29,7 @@ stream_kernel(double *__restrict__ dst, const double *__restrict__ src, size_t n
     const size_t tid = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const size_t nthreads = size_t(gridDim.x) * blockDim.x;
     const size_t nvec = VEC ? n / 4 : 0;
-    for (size_t q = tid; q < nvec; q += nthreads) {
+    for (size_t q = tid; VEC && q < nvec; q += nthreads) {
         double *p = dst + 4 * q;
         krn_d4 o;
         if (OP == Op::Fill) {

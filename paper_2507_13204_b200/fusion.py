@@ -310,8 +310,6 @@ def window_plan(ops: list, an: "Analysis"):
         for v, f in per[k].items():
             if f.wr and v not in in_kernel and not f.direct:
                 return None
-            if False:
-                return None  # its apply loop runs in another launch: contributions must be stored exactly once
             halo_views.add(v)
     for k, (hlo, hhi) in enumerate(H):
         for v, f in per[k].items():
