@@ -142,6 +142,22 @@ def cpu_interp_timing(rows: int = 10_000, threads: int = 1):
     return tp, tg
 
 
+def numpy_oracle_baseline(rows: int = 10_000_000):
+    """the vectorised numpy restatement (`laplacian_oracle`: value and both
+    gradients in one call, 1 core) - the "best CPU restatement" where the interpreter is infeasible."""
+    from paper_2507_13204_b200.verify import laplacian_oracle
+
+    rng = np.random.default_rng(0)
+    x, b = rng.uniform(-1.0, 1.0, rows), rng.uniform(-1.0, 1.0, rows)
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        laplacian_oracle(x, b)
+        best = min(best, time.perf_counter() - t0)
+    return {"rows": rows, "seconds": best, "entries_per_s": 2.0 * rows / best, "cores": 1,
+            "what": "verify.laplacian_oracle (numpy, value + both gradients), best of 3"}
+
+
 def interpreter_baseline():
     """the interpreter at 1e4 and 1e5 rows, threads=1 and
     threads=os.cpu_count().  The reference package itself cannot travel to the GPU box; this is its
@@ -216,7 +232,8 @@ def run_reference(args, rank, world):
                          "sample": f"{rows} rows per step, {len(per_step)} steps (oracle/krn_oracle.c, gcc -O2 -fopenmp, "
                                    "no FMA; OpenMP on the order-free loops, the deferred-atomic scatter and the "
                                    "pairwise tree are sequential by definition)",
-                         "host_cores": os.cpu_count(), "interpreter": interpreter_baseline()},
+                         "host_cores": os.cpu_count(), "interpreter": interpreter_baseline(),
+                         "numpy_oracle": numpy_oracle_baseline()},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -424,7 +441,8 @@ def main():
                                 "kind": "port",
                                 "sample": f"{crow} rows (oracle/krn_oracle.c, OpenMP on the order-free loops, best of 3)",
                                 "primal_s": tp, "grad_s": tg, "ratio_grad_primal": tg / tp,
-                                "host_cores": os.cpu_count(), "interpreter": interpreter_baseline()}
+                                "host_cores": os.cpu_count(), "interpreter": interpreter_baseline(),
+                                "numpy_oracle": numpy_oracle_baseline()}
     if dist is not None:
         # e2e needs every rank; keep the collective pattern symmetric
         dist.barrier()

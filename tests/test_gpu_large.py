@@ -104,3 +104,38 @@ def test_generated_window_kernels_beyond_4gib_offsets():
     assert_bits(c[0], a[0], "objective")
     for k, name in ((1, "x after primal"), (2, "_d_x"), (3, "_d_b"), (4, "x after gradient")):
         assert np.array_equal(c[k].view(np.uint64), a[k].view(np.uint64)), name
+
+
+def test_quarter_billion_ordered_records():
+    """BASELINE-scale queue for the ordered accumulation (2^28 records onto 2^27 + 5 targets: three
+    8-bit partition passes' worth of tiles, a 16 M-entry digit table, 32-bit destinations close to
+    2^28).  Keys and values are generated on the device; contributions are small integers, exact in any
+    order, so the result has a closed form: the size-independent properties checked are (a) every
+    target equals its bincount-weighted sum, (b) a second identical call doubles it, (c) -values
+    bring it back to zero - with sampled windows compared element by element."""
+    free, _ = torch.cuda.mem_get_info()
+    records, size = 1 << 28, (1 << 27) + 5
+    if free < 24 * (1 << 30):
+        pytest.skip("needs 24 GB of free device memory")
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    dev = krn.Device(0, s.cuda_stream)
+    j = torch.arange(records, dtype=torch.int64, device="cuda")
+    keys64 = (j * 2654435761 + (j >> 7) * 40503) % size
+    keys64[::1001] = 12345  # a mildly hot target: a run of ~268 k records in one bucket
+    keys = keys64.to(torch.int32)  # bit pattern of uint32 (all keys < 2^31)
+    vals = ((j % 7) + 1).to(torch.float64)
+    del j
+    target = torch.zeros(size, dtype=torch.float64, device="cuda")
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    want = torch.zeros(size, dtype=torch.float64, device="cuda").index_add_(0, keys64, vals)
+    _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, P(target), size, P(keys), P(vals), records, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(target, want)
+    _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, P(target), size, P(keys), P(vals), records, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(target, 2.0 * want)
+    neg = -2.0 * vals
+    _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, P(target), size, P(keys), P(neg), records, 1))
+    torch.cuda.synchronize()
+    assert int(torch.count_nonzero(target).item()) == 0
