@@ -133,6 +133,8 @@ def plan_group(builder, group, an, live_after: set) -> dict:
             e[1] = e[1] or a.write
     if group.gather is not None:
         accessed.setdefault(group.gather[0].src, [True, False])
+    for sstmt, _, _ in group.sides:
+        accessed.setdefault(sstmt.src, [True, False])
     full_range = {id(l) for l in group.ops if l.shift == 0}
     promoted = []
     for v, (pw, written) in accessed.items():
@@ -486,6 +488,9 @@ def plan_window_group(builder, group, an, live_after: set) -> dict:
     full_range = {id(l) for l in group.ops if l.shift == 0}
     if group.gather is not None and group.gather[0].src not in G:
         G[group.gather[0].src] = fusion.Facts(rd=True)
+    for sstmt, _, _ in group.sides:
+        if sstmt.src not in G:
+            G[sstmt.src] = fusion.Facts(rd=True)
     promoted, windows = [], []
     for v, f in G.items():
         if v.startswith("__stage"):

@@ -200,3 +200,18 @@ def test_a_fill_that_is_read_later_is_kept():
     ops = fusion.build_ops(p.functions[0], an, True)
     fills = [op[1].origin.src.value for op in ops if op[0] == "loop" and op[1].what == "deepcopy"]
     assert fills == [2.0, 3.0]  # the last one is dead, the others are read
+
+
+def test_side_reduction_over_a_view_the_group_never_touches():
+    """tracked plans keep side reductions in the open group; their source must be promoted even when no
+    statement of the group reads or writes it (a fresh zero local) - found by the random-program test"""
+    p = krn.parse("""fn f(a: view<f64,1>, b: view<f64,1>, m: view<f64,2>) -> f64 {
+        let t0: view<f64,1> = view("t0", extent(a, 0));
+        let q: view<f64,2> = view("q", extent(a, 0), extent(m, 1));
+        parallel_for i in 0..extent(a, 0) { q(i, 0) = a(i); }
+        parallel_for i in 0..extent(a, 0) { a(i) = 0.5 * a(i) + b(i); }
+        r = parallel_sum(t0);
+        return r; }""")
+    for windows in (False, True):
+        plan = compiled.plan_for(p.functions[0], windows, True)
+        assert plan is not None and plan.launch_count == 1
