@@ -403,6 +403,8 @@ __device__ __forceinline__ void krn_fin(const Env &E, int slot, double x)
 {
     if ((__double2hiint(x) & 0x7ff00000) == 0x7ff00000) E.fin[slot] = 1;  // Inf or NaN: exponent all ones
 }
+// the same test as one bit of a per-thread mask (tilegen._defer_finite_flags): !(|x| < Inf) is true for Inf and NaN
+#define KRN_FINB(k, x) (finbits_ |= (unsigned long long)(!(fabs(x) < __longlong_as_double(0x7ff0000000000000ll))) << (k))
 extern __shared__ double krn_priv[];
 __device__ __forceinline__ void krn_scatter(const Env &E, int v, krn_i64 o, double t)
 {

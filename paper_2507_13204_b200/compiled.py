@@ -439,8 +439,9 @@ class _CompiledRun:
             self.S = _DeviceBuffer(dev, 8 * self.plan.nslots)
             dev.fill(self.S.ptr, self.plan.nslots, 0.0)
         self.fin = None
+        self.block = None  # (capacity in slots) when status word, scalar slots and flags are one block
         if self.plan.track:
-            self.start_tracking()
+            self.start_tracking(slots.value, cap.value)
         # scalar parameters the function redefines with device data (a gather into the parameter,
         # arithmetic on View elements) live in the slot array: start them at the caller's value
         for p in self.plan.fn.params:
@@ -451,18 +452,24 @@ class _CompiledRun:
         return self.finish()
 
     # ---- check_finite inside the fused kernels ---------------------------------------------------
-    def start_tracking(self):
+    def start_tracking(self, slots: int, cap: int):
         """fin[checkpoint][view]: one int per (statement, View), set by the kernels when the statement
         leaves a non-finite value in the View.  Row 0 is the state the Views come in with: parameter
         Views that no kernel tests when it loads them are probed here (krn_check_finite), unless the
-        first statement overwrites them before the reference's first check."""
+        first statement overwrites them before the reference's first check.  The flags live behind the
+        scalar slots of the context's status block when they fit (krn_run_begin has cleared it): no
+        memset of their own, and status word, scalars and flags come back with ONE copy (finish)."""
         from .runtime import _DeviceBuffer
 
         dev, b = self.dev, self.b
         nv = max(len(b.views), 1)
         rows = len(b.track) + 1
-        self.fin = _DeviceBuffer(dev, 4 * rows * nv)
-        _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.fin.ptr), 0, 4 * rows * nv))
+        if isinstance(self.S, _Borrowed) and 8 * self.plan.nslots + 4 * rows * nv <= 8 * cap:
+            self.fin = _Borrowed(slots + 8 * self.plan.nslots)
+            self.block = cap
+        else:
+            self.fin = _DeviceBuffer(dev, 4 * rows * nv)
+            _cabi.check(dev.lib.krn_memset(dev.h, C.c_void_p(self.fin.ptr), 0, 4 * rows * nv))
         first = next((c for c in self.plan.checkpoints if c[0] == "views"), None)
         for p in self.plan.fn.params:
             if not p.is_view or p.name in b.init_tested:
@@ -480,10 +487,16 @@ class _CompiledRun:
 
         dev, b = self.dev, self.b
         nv = max(len(b.views), 1)
-        flags = np.zeros((len(b.track) + 1, nv), dtype=np.int32)
-        dev.download(flags, self.fin.ptr)
-        slots = np.zeros(self.plan.nslots)
-        dev.download(slots, self.S.ptr)
+        rows = len(b.track) + 1
+        if self.block is not None:  # already on the host: finish() fetched the whole block
+            slots = dev.staging[64 : 64 + 8 * self.plan.nslots].view(np.float64)
+            first = 64 + 8 * self.plan.nslots
+            flags = dev.staging[first : first + 4 * rows * nv].view(np.int32).reshape(rows, nv)
+        else:
+            flags = np.zeros((rows, nv), dtype=np.int32)
+            dev.download(flags, self.fin.ptr)
+            slots = np.zeros(self.plan.nslots)
+            dev.download(slots, self.S.ptr)
         order = [p.name for p in self.plan.fn.params if p.is_view]
         bad = {name: bool(flags[0, b.vid(name)]) for name in order}
         for cpt in self.plan.checkpoints:
@@ -720,16 +733,21 @@ class _CompiledRun:
         dev = self.dev
         if not self.cfg.synchronous:
             return None
-        if self.ret_slot is not None:
-            out = dev.staging[64:72].view(np.float64)
-            dev.download_async(out, self.S.ptr + 8 * self.ret_slot)
         st = dev.staging[:64].view(np.int64)
-        dev.download(st, dev.status_ptr)
+        if self.block is not None:
+            # check_finite: status word, every scalar slot and the flags in one copy
+            dev.download(dev.staging[: 64 + 8 * self.block], dev.status_ptr)
+            out = dev.staging[64 + 8 * (self.ret_slot or 0) :][:8].view(np.float64)
+        else:
+            out = dev.staging[64:72].view(np.float64)
+            if self.ret_slot is not None:
+                dev.download_async(out, self.S.ptr + 8 * self.ret_slot)
+            dev.download(st, dev.status_ptr)
         if st[0] != 0:
             helper = _Run.__new__(_Run)
             helper.b, helper.views = self.b, self.views
             raise helper.error_from(st.copy())
-        value = float(dev.staging[64:72].view(np.float64)[0]) if self.ret_slot is not None else self.host_value
+        value = float(out[0]) if self.ret_slot is not None else self.host_value
         if self.plan.track:
             from .runtime import NonFiniteDetected
 

@@ -21,6 +21,8 @@ hand-written prelude, and is compiled with the same flags (--fmad=false).
 
 from __future__ import annotations
 
+import re
+
 from .lang import nodes as N
 from .lang.dataflow import normalize_index
 from .lang.nodes import kind, walk_statements
@@ -188,6 +190,30 @@ def _specialise_interior_chunks(L: list, start: int, end: int, cond: str, subst:
 
 
 
+_FIN_CALL = re.compile(r"krn_fin\(E, ([^,;]+), ([^;]+)\);")
+
+
+def _defer_finite_flags(text: str) -> str:
+    """check_finite tests of a fused kernel without branches or stores in the element loops: every
+    test site ORs one bit into a per-thread mask (an fp64 compare that sets a predicate and a predicated
+    LOP3, against test + branch + store per value) and the thread writes the flags of its set bits once,
+    when it is done.  Up to 64 distinct (statement, View) flags per kernel; beyond that the immediate
+    form stays."""
+    slots: list = []
+    for m in _FIN_CALL.finditer(text):
+        if m.group(1) not in slots:
+            slots.append(m.group(1))
+    if not slots or len(slots) > 64:
+        return text
+    text = _FIN_CALL.sub(lambda m: f"KRN_FINB({slots.index(m.group(1))}, {m.group(2)});", text)
+    head = text.index("{\n", text.index('extern "C" __global__')) + 2
+    flush = ["    if (finbits_) {"]
+    flush += [f"        if (finbits_ >> {k} & 1ull) E.fin[{slot}] = 1;" for k, slot in enumerate(slots)]
+    flush += ["    }"]
+    tail = text.rindex("}")
+    return text[:head] + "    unsigned long long finbits_ = 0ull;\n" + text[head:tail] + "\n".join(flush) + "\n" + text[tail:]
+
+
 def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     b = builder
     elided: set = set()
@@ -225,6 +251,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     # the number of loaded Views so the register file still holds 3+ blocks per SM.
     nload = sum(1 for p in promoted if p["load"])
     B = 2 if 1 <= nload <= 2 else 1  # measured on B200: 2 gains 1-3%, deeper batches cost occupancy
+    # (tracked - check_finite - kernels: B = 1, 2, 4 measured equal within 1 %)
     if strided:
         w("#define KRN_IT(e) (j0 + (e) * 32 + lane_)")
     else:
@@ -252,6 +279,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     else:
         w(f"    for (int t0 = 0; t0 < steps; t0 += {B}) {{")
     # ---- prologue: loads of the whole batch -------------------------------------------
+    init_tests: list = []  # tested in the compute part: a test right behind its load would serialise the batch's loads
     for k_, p in enumerate(promoted):
         if p["load"]:
             w(f"    double {regs[p['view']]}b_[{B}][4];")
@@ -272,7 +300,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             w(f"        if (full) {{ krn_d4 q = {ld}(E.v[{v}] + j0); {r}[0] = q.a; {r}[1] = q.b; {r}[2] = q.c; {r}[3] = q.d; }}")
         w(f"        else {{ for (int e = 0; e < 4; ++e) if (KRN_IT(e) < E.e0[{v}] && KRN_IT(e) < n_launch) {r}[e] = E.v[{v}][KRN_IT(e)]; }}")
         if b.track is not None and p["view"] not in b.touched_before:  # initial status of a loaded View (checkpoint 0)
-            w(f"        for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
+            init_tests.append((v, regs[p["view"]]))
             b.init_tested.add(p["view"])
         w("    }")
     w("    }")
@@ -289,6 +317,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w(f"    double T{idx}[4] = {{0.0, 0.0, 0.0, 0.0}};")
     for j in range(len(sides)):
         w(f"    double SG{j}[4] = {{0.0, 0.0, 0.0, 0.0}};  // side reduction {j}: the source as it is at that statement")
+    for v, r in init_tests:  # (slots that were not loaded hold 0.0)
+        w(f"    for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
     # ---- body ------------------------------------------------------------------------
     # interior step: every iteration of the warp (and every iteration an apply loop looks back or
     # ahead to) lies far enough inside the range for the index guards to be decided at compile time
@@ -434,7 +464,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     if gather is not None or sides:
         _emit_reduce_epilogue(w, gather is not None, len(sides), "threadIdx.x >> 5")
     w("}")
-    b.parts.append("\n".join(L))
+    b.parts.append(_defer_finite_flags("\n".join(L)))
     return dict(name=name, promoted=promoted, stage_cols=plan["stage_cols"], has_stage=has_stage,
                 gather=gather, max_shift=plan["max_shift"], elided_views=sorted(elided), atomic_views=direct,
                 ordered=ordered, static_smem=(_TREE_SMEM if (gather is not None or sides) else 0) + 1024 * len(sides))
@@ -641,6 +671,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     w(f"    it_[4] = lane_ < {HLO} ? wlo + lane_ : j0 + 128 + (lane_ - {HLO});")
     w(f"    act_[4] = live && lane_ < {HLO + HHI} && it_[4] >= 0 && it_[4] < n_launch;")
     # ---- prologue: registers ------------------------------------------------------------
+    late_tests: list = []  # check_finite tests of loaded values: a test right behind its load would serialise the loads
     for p in promoted:
         r, v = regs[p["view"]], b.vid(p["view"])
         if "cols" in p:
@@ -657,7 +688,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
                 for c in lc:
                     w(f"                {r}c{c}[e] = E.v[{v}][it_[e] * ld_ + {c}];")
                     if b.track is not None and p["view"] not in b.touched_before:
-                        w(f"                krn_fin(E, {v}, {r}c{c}[e]);")
+                        late_tests.append(f"    for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}c{c}[e]);")
                 w("            }")
                 w("        }")
                 w("    }")
@@ -672,7 +703,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
             if p["halo"]:
                 w(f"        if (act_[4] && it_[4] < E.e0[{v}]) {r}[4] = E.v[{v}][it_[4]];")
             if b.track is not None and p["view"] not in b.touched_before:  # initial status: own rows only (checkpoint 0)
-                w(f"        for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
+                late_tests.append(f"    for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
                 b.init_tested.add(p["view"])
             w("    }")
     for idx in sorted(stage_reg_sites):
@@ -699,11 +730,13 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
           f"if (lane_ + 32 * u < {WN} && g_ >= 0 && g_ < E.e0[{v}] && g_ < n_launch) {wn}r[u] = E.v[{v}][g_]; }}")
         w("        }")
         if b.track is not None and p["view"] not in b.touched_before:  # own positions of the window only: [HLO, HLO + 128)
-            w("#pragma unroll")
-            w(f"        for (int u = 0; u < {NQ}; ++u) if (lane_ + 32 * u >= {HLO} && lane_ + 32 * u < {HLO + 128}) "
-              f"krn_fin(E, {v}, {wn}r[u]);")
+            late_tests.append("#pragma unroll\n"
+                              f"    for (int u = 0; u < {NQ}; ++u) if (lane_ + 32 * u >= {HLO} && lane_ + 32 * u < {HLO + 128}) "
+                              f"krn_fin(E, {v}, {wn}r[u]);")
             b.init_tested.add(p["view"])
         w("    }")
+    for line in late_tests:  # behind every load of the step (slots that were not loaded hold 0.0)
+        w(line)
 
     def emit_apply(view, sites, producer, interior: bool):
         """`acc = target(row); acc += contributions landing on the row, reference order; target = acc`,
@@ -981,7 +1014,7 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
     elif gather is not None or sides:
         _emit_reduce_epilogue(w, gather is not None, len(sides), "warp_")
     w("}")
-    b.parts.append("\n".join(L))
+    b.parts.append(_defer_finite_flags("\n".join(L)))
     every = promoted + windows
     return dict(name=name, promoted=every, stage_cols=plan["stage_cols"], has_stage=bool(plan["stage_cols"]),
                 gather=gather, max_shift=plan["max_shift"],

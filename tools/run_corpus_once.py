@@ -1,6 +1,7 @@
 """Runs one corpus program (primal and gradient) a few times under one policy at one size, for ncu:
-python tools/run_corpus_once.py sum_squares compiled 67108864 [reps] [hardware]   (hardware: deterministic_reduction=False,
-i.e. hardware fp64 reductions instead of the ordered accumulation of atomic_add queues)"""
+python tools/run_corpus_once.py sum_squares compiled 67108864 [reps] [hardware|check]   (hardware:
+deterministic_reduction=False, i.e. hardware fp64 reductions instead of the ordered accumulation of atomic_add
+queues; check: check_finite=True)"""
 import os
 import sys
 
@@ -29,8 +30,9 @@ wrt = tuple(p.name for p in fn.params if p.is_view and p.name != "idx")
 gp = krn.differentiate(prog, fn.name, wrt)
 gfn = gp.functions[-1]
 hardware = len(sys.argv) > 5 and sys.argv[5] == "hardware"
+check = len(sys.argv) > 5 and sys.argv[5] == "check"  # check_finite=True: the tracked plan
 cfg = ExecutionConfig(policy="compiled" if policy == "pointwise" else policy, fuse_neighbours=policy != "pointwise",
-                      deterministic_reduction=not hardware)
+                      deterministic_reduction=not hardware, check_finite=check)
 for rep in range(reps):
     call = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in base.items()}
     krn.execute(prog, fn.name, call, cfg)
