@@ -403,6 +403,8 @@ __device__ __forceinline__ void krn_fin(const Env &E, int slot, double x)
 {
     if ((__double2hiint(x) & 0x7ff00000) == 0x7ff00000) E.fin[slot] = 1;  // Inf or NaN: exponent all ones
 }
+// element k (-4 .. 7, relative to the lane's own four) of a read-only View held as P[4] plus halo registers
+#define KRN_NBR(P, k) ((k) < 0 ? P##L[-(k) - 1] : (k) < 4 ? P[(k) < 0 ? 0 : (k) < 4 ? (k) : 0] : P##R[(k) - 4 < 0 ? 0 : (k) - 4])
 // the same test as one bit of a per-thread mask (tilegen._defer_finite_flags): !(|x| < Inf) is true for Inf and NaN
 #define KRN_FINB(k, x) (finbits_ |= (unsigned long long)(!(fabs(x) < __longlong_as_double(0x7ff0000000000000ll))) << (k))
 extern __shared__ double krn_priv[];
@@ -553,6 +555,7 @@ class ModuleBuilder:
         self.in_tile = False  # a window kernel is being generated
         self.interior = None  # dict(counter, trip, sym, lo, up) while an interior warp step is generated
         self.counter = None  # AST counter of the statement being generated (window kernels)
+        self.nbr = {}  # read-only Views read at i + c inside a tile kernel's interior steps: view -> register stem
         self.elide = None  # bounds-check elision context (tile kernels only)
         self.guards: list = []  # enclosing If conditions of the statement being generated
         self.tracing = False  # a dry, access-tagging replay of a kernel is being generated (kernel_trace)
@@ -600,6 +603,17 @@ class ModuleBuilder:
             if len(acc.indices) == 2:  # rank-2 row at the running index: one register column per literal column
                 return f"{r}c{_constant(acc.indices[1])}[e]"
             return f"{r}[e]"
+        nb = self.nbr.get(acc.view)
+        if nb is not None:
+            # neighbour registers (tilegen.tile_kernel): element e + c of the lane's four, or the halo
+            # values fetched from the adjacent lanes; only for accesses proven in range on interior steps
+            const = _unit_affine(acc.indices[0], self.counter) if len(acc.indices) == 1 else None
+            el = self.interior
+            if const is not None and el is not None and -const <= el["lo"] and const <= el["up"]:
+                if self.elide is not None:
+                    self.elide["views"].add(acc.view)  # the host verifies extent >= n before it launches
+                return f"KRN_NBR({nb}, e + ({const}))"
+            return None
         w = self.windows.get(acc.view)
         if w is not None:
             # every access to a window View is `counter + c`, proven in range when the group was formed

@@ -308,8 +308,7 @@ __global__ void __launch_bounds__(kThreads) scan_apply(u32 *data, size_t count, 
 template <int BITS>
 __global__ void __launch_bounds__(kThreads)
 ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in, u32 *__restrict__ keys_out,
-            double *__restrict__ vals_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles, int width,
-            int getenv_prefetch)
+            double *__restrict__ vals_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles, int width)
 {
     constexpr u32 mask = (1u << BITS) - 1u;
     constexpr int kRadix = 1 << BITS;
@@ -328,11 +327,10 @@ ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in,
     for (int k = threadIdx.x; k < kWarps * kRadix; k += kThreads) s_cnt[k] = 0;
     // the tile's values are not needed before the keys are ranked: start them towards L2 now (one 128-byte
     // line per thread and plane), so that their loads below do not pay the DRAM latency a second time
-    if (getenv_prefetch) {
-        for (int w = 0; w < width; ++w) {
-            const u32 first = u32(threadIdx.x) * 16u;
-            if (first < live) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + size_t(w) * m + base + first));
-        }
+    // (measured: 0.704 -> 0.690 ms per 16.7 M records together with the prefetch in the fold)
+    for (int w = 0; w < width; ++w) {
+        const u32 first = u32(threadIdx.x) * 16u;
+        if (first < live) asm volatile("prefetch.global.L2 [%0];" ::"l"(vals_in + size_t(w) * m + base + first));
     }
     __syncthreads();
 
@@ -539,7 +537,7 @@ template <int WIDTH, bool LANES, int PER>
 __global__ void __launch_bounds__(kThreads)
 ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, size_t m,
                 double *__restrict__ target, size_t target_size, int ncols, Cols cols, int lb,
-                const u32 *__restrict__ start, const u32 *__restrict__ end, int prefetch)
+                const u32 *__restrict__ start, const u32 *__restrict__ end)
 {
     constexpr int width = WIDTH;
     constexpr int kChunk = kThreads * PER;
@@ -561,7 +559,7 @@ ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, s
     unsigned short *c16 = reinterpret_cast<unsigned short *>(wb + kChunk);  // [16][kThreads] ranking counters
     __shared__ u32 s_wsum[kWarps];
 
-    if (prefetch) {
+    {
         // the first chunk's records: towards L2 while the tile is loaded (one 128-byte line per thread)
         const u32 cnt0 = e0 - s0 < u32(kChunk) ? e0 - s0 : u32(kChunk);
         if (u32(threadIdx.x) * 32u < cnt0) asm volatile("prefetch.global.L2 [%0];" ::"l"(keys + s0 + threadIdx.x * 32u));
@@ -711,7 +709,7 @@ cudaError_t launch_scatter(int bits, unsigned tiles, cudaStream_t st, const u32 
         e = cudaFuncSetAttribute(ord_scatter<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
         if (e == cudaSuccess)                                                                                    \
             ord_scatter<B><<<tiles, kThreads, smem, st>>>(keys_in, vals_in, keys_out, vals_out, table, m, shift, \
-                                                          ntiles, width, getenv("KRN_ORD_PREFETCH") ? atoi(getenv("KRN_ORD_PREFETCH")) : 0); \
+                                                          ntiles, width);                                        \
     } while (0)
     KRN_BITS_SWITCH(bits, KRN_CALL)
 #undef KRN_CALL
@@ -866,8 +864,7 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
         e = cudaFuncSetAttribute(ord_bucket_fold<W, L, per>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         if (e == cudaSuccess)                                                                                     \
             ord_bucket_fold<W, L, per><<<unsigned(real), kThreads, smem, ctx->stream>>>(                          \
-                src_keys, src_vals, records, d_target, target_size, ncols, cc, lb, start, end,                    \
-                getenv("KRN_ORD_PREFETCH") ? atoi(getenv("KRN_ORD_PREFETCH")) : 0);                               \
+                src_keys, src_vals, records, d_target, target_size, ncols, cc, lb, start, end);                   \
     } while (0)
         switch (width * 2 + (lanes ? 1 : 0)) {
         case 2: KRN_FOLD(1, false); break;

@@ -145,6 +145,28 @@ def plan_group(builder, group, an, live_after: set) -> dict:
             load = not _first_access_is_full_store(group, v, full_range) and v not in group.fresh
             store = written and (v in live_after)
             promoted.append(dict(view=v, load=load, store=store, written=written))
+    # Read-only Views read at i + c (|c| <= 4) - stencil neighbours: loaded like a promoted View (one
+    # 256-bit access per lane and step); the values beyond the lane's own four come from the adjacent
+    # lanes by shuffle, the warp's two ends from global memory.  Interior steps only (the guards'
+    # margins must cover the offsets, so that every such read is in range there); the other steps
+    # keep the bounds-checked loads.
+    if an is not None and group.ops and all(l.what == "kernel" and l.shift == 0 for l in group.ops):
+        from .codegen import _unit_affine
+
+        lo_m, up_m = _guard_margins(group, an)
+        for v, (pw, written) in accessed.items():
+            if pw or written or builder.rank.get(v) != 1 or v in direct_atomic or v in group.fresh:
+                continue
+            offs = []
+            for loop in group.ops:
+                for a in loop.accesses():
+                    if a.view != v:
+                        continue
+                    c = _unit_affine(a.indices[0], loop.counter) if len(a.indices) == 1 and not a.atomic else None
+                    offs.append(c)
+            if offs and all(c is not None and abs(c) <= 4 for c in offs) and -min(offs) <= lo_m and max(offs) <= up_m:
+                promoted.append(dict(view=v, load=True, store=False, written=False,
+                                     nbr=(max(0, -min(offs)), max(0, max(offs)))))
     stage_cols = []
     for loop in group.ops:
         if loop.what == "kernel":
@@ -168,6 +190,10 @@ def plan_group(builder, group, an, live_after: set) -> dict:
                 continue
             if terms == ((("counter", loop.counter), 1),):
                 strided = True
+    if strided and any(p.get("nbr") for p in promoted):
+        # neighbour registers are elements of the VECTOR layout; something else forces the strided one
+        # (another View read at i + c that cannot be held in registers): plain loads for all of them
+        promoted = [p for p in promoted if not p.get("nbr")]
     return dict(promoted=promoted, stage_cols=stage_cols, max_shift=max(l.shift for l in group.ops),
                 has_user_ops=any(l.what != "apply" for l in group.ops), strided=strided)
 
@@ -280,12 +306,23 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w(f"    for (int t0 = 0; t0 < steps; t0 += {B}) {{")
     # ---- prologue: loads of the whole batch -------------------------------------------
     init_tests: list = []  # tested in the compute part: a test right behind its load would serialise the batch's loads
+    nbrs = {p["view"]: p["nbr"] for p in promoted if p.get("nbr")}
+    # interior step: every iteration of the warp (and every iteration an apply loop looks back or
+    # ahead to) lies far enough inside the range for the index guards to be decided at compile time
+    LO, UP = _guard_margins(group, an) if an is not None else (0, 0)
+    OFF = max([abs(st.offset) for l in group.ops if l.what == "apply" for st in l.apply_of[1]] + [0])
+    span = 128 if strided else 4
+    interior_line = f"    const bool interior = full && j0 >= {LO + OFF} && j0 + {span + UP + OFF} <= n;"
     for k_, p in enumerate(promoted):
         if p["load"]:
             w(f"    double {regs[p['view']]}b_[{B}][4];")
+        if p.get("nbr"):
+            w(f"    double {regs[p['view']]}Lb_[{B}][4], {regs[p['view']]}Rb_[{B}][4];  // elements j0-1.., j0+4.. (warp ends)")
     w("#pragma unroll")
     w(f"    for (int b_ = 0; b_ < {B}; ++b_) {{")
     geometry()
+    if nbrs:
+        w(interior_line)
     for k_, p in enumerate(promoted):
         if not p["load"]:
             continue
@@ -303,6 +340,17 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
             init_tests.append((v, regs[p["view"]]))
             b.init_tested.add(p["view"])
         w("    }")
+        if p.get("nbr"):
+            # the values just outside the warp's 128 elements: lane 0 / lane 31 fetch them with the
+            # batch's other loads (in range on an interior step); the other lanes shuffle (below)
+            rs, (na, nb_) = regs[p["view"]], p["nbr"]
+            w(f"    for (int e = 0; e < 4; ++e) {{ {rs}Lb_[b_][e] = 0.0; {rs}Rb_[b_][e] = 0.0; }}")
+            w(f"    if (interior && !(zero_mask & {1 << k_}u)) {{")
+            if na:
+                w("        if (lane_ == 0) { " + " ".join(f"{rs}Lb_[b_][{k - 1}] = E.v[{v}][j0 - {k}];" for k in range(1, na + 1)) + " }")
+            if nb_:
+                w("        if (lane_ == 31) { " + " ".join(f"{rs}Rb_[b_][{k}] = E.v[{v}][j0 + {4 + k}];" for k in range(nb_)) + " }")
+            w("    }")
     w("    }")
     # ---- the steps of the batch, one after the other ------------------------------------------
     w("#pragma unroll")
@@ -320,12 +368,21 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     for v, r in init_tests:  # (slots that were not loaded hold 0.0)
         w(f"    for (int e = 0; e < 4; ++e) krn_fin(E, {v}, {r}[e]);")
     # ---- body ------------------------------------------------------------------------
-    # interior step: every iteration of the warp (and every iteration an apply loop looks back or
-    # ahead to) lies far enough inside the range for the index guards to be decided at compile time
-    LO, UP = _guard_margins(group, an) if an is not None else (0, 0)
-    OFF = max([abs(st.offset) for l in group.ops if l.what == "apply" for st in l.apply_of[1]] + [0])
-    span = 128 if strided else 4
-    w(f"    const bool interior = full && j0 >= {LO + OFF} && j0 + {span + UP + OFF} <= n;")
+    w(interior_line)
+    if nbrs:
+        # neighbour registers need the whole warp on the fast path (shuffles)
+        w("    const bool interior_w = __all_sync(KRN_FULL_MASK, interior);")
+        for p in promoted:
+            if not p.get("nbr"):
+                continue
+            r, (na, nb_) = regs[p["view"]], p["nbr"]
+            w(f"    double (&{r}L)[4] = {r}Lb_[b_]; double (&{r}R)[4] = {r}Rb_[b_];")
+            w("    if (interior_w) {")
+            for k in range(1, na + 1):
+                w(f"        {{ const double s_ = __shfl_up_sync(KRN_FULL_MASK, {r}[{4 - k}], 1); if (lane_ != 0) {r}L[{k - 1}] = s_; }}")
+            for k in range(nb_):
+                w(f"        {{ const double s_ = __shfl_down_sync(KRN_FULL_MASK, {r}[{k}], 1); if (lane_ != 31) {r}R[{k}] = s_; }}")
+            w("    }")
 
     def emit_body(interior: bool):
         w("#pragma unroll")
@@ -334,7 +391,8 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
         w("        bool bad = false;")
         if not interior:
             w("        if (i >= n_launch) continue;")
-        b.promoted = regs
+        b.promoted = {v_: r_ for v_, r_ in regs.items() if v_ not in nbrs}
+        b.nbr = {v_: regs[v_] for v_ in nbrs} if interior else {}
         try:
             for k_op, loop in enumerate(list(group.ops) + [None]):
                 for j, (sstmt, _, pos) in enumerate(sides):
@@ -377,6 +435,7 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
                 sites = {id(st.stmt): st for st in loop.sites}
                 body: list = []
                 local = {loop.counter}
+                b.counter = loop.counter
                 if an is not None:
                     try:
                         trip = an.trip(loop.upper)
@@ -400,9 +459,11 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
                         w(f"        krn_fin(E, {cp} * NV + {b.vid(tv)}, {regs[tv]}[e]);")
         finally:
             b.promoted = {}
+            b.nbr = {}
+            b.counter = None
         w("    }")
 
-    w("    if (interior) {")
+    w("    if (interior_w) {" if nbrs else "    if (interior) {")
     emit_body(True)
     w("    } else if (live) {")
     emit_body(False)

@@ -222,3 +222,26 @@ def test_side_reduction_over_a_view_the_group_never_touches():
         return r; }""")
     plan = compiled.plan_for(p.functions[0], False, True)
     assert plan is not None and plan.launch_count == 1
+
+
+def test_read_only_stencil_neighbours_become_registers():
+    """a read-only View read at i - 1, i, i + 1 under guards is loaded with one 256-bit access per lane;
+    the neighbours come from the adjacent lanes (interior steps), the layout stays the vector one"""
+    from paper_2507_13204_b200 import tilegen
+
+    fn = krn.load_program("stencil_smooth").functions[0]
+    plan = compiled.plan_for(fn, False)
+    recipe = [st[2] for st in plan.steps if st[0] == "group"][0]
+    u = [p for p in recipe["promoted"] if p["view"] == "u"][0]
+    assert u["nbr"] == (1, 1) and u["load"] and not u["store"]
+    src = plan.source
+    assert "KRN_NBR(P0" in src and "__shfl_up_sync" in src and "#define KRN_IT(e) (j0 + (e))" in src
+    assert "u" in recipe["elided_views"]  # the host must verify extent(u) >= n before it launches
+    # an unguarded neighbour read has no margin that proves it in range: bounds-checked loads stay
+    p = krn.parse("""fn f(u: view<f64,1>) -> f64 {
+        let d: view<f64,1> = view("d", extent(u, 0));
+        parallel_for i in 0..extent(u, 0) - 1 { d(i) = u(i + 1) - u(i); }
+        s = parallel_sum(d);
+        return s; }""")
+    plan = compiled.plan_for(p.functions[0], False)
+    assert "= KRN_NBR(" not in plan.source and "* KRN_NBR(" not in plan.source and "KRN_NBR(P0" not in plan.source
