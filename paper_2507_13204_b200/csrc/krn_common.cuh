@@ -32,6 +32,7 @@ void krn_set_error(const char *fmt, ...);
         if (e__ != cudaSuccess) {                                                    \
             krn_set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e__),   \
                           __FILE__, __LINE__);                                       \
+            (void)cudaGetLastError(); /* reported here: the next launch check must not see it again */ \
             return KRN_E_CUDA;                                                       \
         }                                                                            \
     } while (0)

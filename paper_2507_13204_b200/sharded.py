@@ -124,6 +124,7 @@ class ShardedLaplacian:
         self.offset, self.n_local = self.parts[self.rank]
         self.block_counts = [partial_count(length, self.span) for _, length in self.parts]
         self._peers = None
+        self.attach_failure = None  # why attach() fell back to the collective halo exchange, if it did
         self._halo_index = None
         self._ext_stream = None
 
@@ -202,13 +203,25 @@ class ShardedLaplacian:
 
         self._mapped = []
         peers = dict(x=x.data_ptr(), b=b.data_ptr(), xp=0, bp=0, xn=0, bn=0)
-        if self.rank > 0:
-            n_prev = self.parts[self.rank - 1][1]
-            peers["xp"] = open_(self.rank - 1, 0) + 8 * n_prev
-            peers["bp"] = open_(self.rank - 1, 1) + 8 * n_prev
-        if self.rank < self.world - 1:
-            peers["xn"] = open_(self.rank + 1, 0)
-            peers["bn"] = open_(self.rank + 1, 1)
+        failure = None
+        try:
+            if self.rank > 0:
+                n_prev = self.parts[self.rank - 1][1]
+                peers["xp"] = open_(self.rank - 1, 0) + 8 * n_prev
+                peers["bp"] = open_(self.rank - 1, 1) + 8 * n_prev
+            if self.rank < self.world - 1:
+                peers["xn"] = open_(self.rank + 1, 0)
+                peers["bn"] = open_(self.rank + 1, 1)
+        except _cabi.KrnNativeError as exc:  # no peer access between the two devices, handles not importable, ...
+            failure = str(exc)
+        # all or nothing: a rank that cannot map its neighbours takes everybody to the collective halo path
+        ok = torch.tensor([0 if failure else 1], dtype=torch.uint8)
+        if not bool(self._gather_bytes(ok).min()):
+            self._peers = peers  # (so that detach releases what this rank did map)
+            self.detach()
+            self.attach_failure = failure or "a neighbour could not map this rank's memory"
+            return self
+        self.attach_failure = None
         self._peers = peers
         self.fence()  # everybody has mapped (and the tensors' producers have finished) before anyone reads
         return self

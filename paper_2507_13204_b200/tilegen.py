@@ -278,6 +278,11 @@ def tile_kernel(builder, group, name: str, plan: dict, an=None) -> dict:
     nload = sum(1 for p in promoted if p["load"])
     B = 2 if 1 <= nload <= 2 else 1  # measured on B200: 2 gains 1-3%, deeper batches cost occupancy
     # (tracked - check_finite - kernels: B = 1, 2, 4 measured equal within 1 %)
+    if (nload == 1 and gather is not None and not any(p["store"] or p.get("nbr") for p in promoted)):
+        # one operand stream that ends in the reduction, nothing stored: 4 loads in flight per lane
+        # (measured at 134 M rows: sum_squares / copy_chain / fill_scale primal 0.180 -> 0.174 ms; with
+        # stores or neighbour registers in the kernel 4 is slower, 8 is slower everywhere)
+        B = 4
     if strided:
         w("#define KRN_IT(e) (j0 + (e) * 32 + lane_)")
     else:

@@ -135,6 +135,73 @@ def test_peer_halo_two_processes_one_device(world, n, own_stream):
     assert_bits(np.concatenate([p[8] for p in pieces]), db2, "_d_b after the inputs changed")
 
 
+def _fallback_worker(rank, world, port, n, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    import paper_2507_13204_b200 as krn
+    from paper_2507_13204_b200 import _cabi
+    from paper_2507_13204_b200.sharded import ShardedLaplacian
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+        dev = krn.Device(0, s.cuda_stream)
+        x, b, dx0, db0, *_ = _whole(n)
+        sh = ShardedLaplacian(n, dev)
+        o, l = sh.offset, sh.n_local
+        xt, bt = torch.from_numpy(x[o:o + l].copy()).cuda(), torch.from_numpy(b[o:o + l].copy()).cuda()
+        dxt, dbt = torch.from_numpy(dx0[o:o + l].copy()).cuda(), torch.from_numpy(db0[o:o + l].copy()).cuda()
+        xo = torch.empty_like(xt)
+        if rank == 1:  # this rank cannot import its neighbours' handles (no peer access, say)
+            garbage = (C.c_ubyte * 64)()
+            real = dev.lib.krn_ipc_open
+
+            def refuse(h, handle, flags, base, ptr):
+                return real(h, garbage, flags, base, ptr)
+
+            class Lib:  # the library with one entry point replaced
+                def __getattr__(self, name, _lib=dev.lib):
+                    return refuse if name == "krn_ipc_open" else getattr(_lib, name)
+
+            dev.lib = Lib()
+        sh.attach(xt, bt)
+        failure = sh.attach_failure
+        assert failure is not None and not sh._attached(xt, bt)
+        sh.grad(xt, xo, bt, dxt, dbt)
+        torch.cuda.synchronize()
+        dev.sync()
+        pieces = [None] * world
+        dist.all_gather_object(pieces, (xo.cpu().numpy(), dxt.cpu().numpy(), dbt.cpu().numpy(), failure))
+        if rank == 0:
+            out.put(pieces)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_a_rank_that_cannot_map_its_neighbours_takes_everybody_to_the_collective_path():
+    world, n = 2, 40_001
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, world, port, n, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    pieces = _collect(procs, out)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    x, b, dx0, db0, xo, dxo, dbo, f = _whole(n)
+    assert_bits(np.concatenate([p[0] for p in pieces]), xo, "3x")
+    assert_bits(np.concatenate([p[1] for p in pieces]), dxo, "_d_x")
+    assert_bits(np.concatenate([p[2] for p in pieces]), dbo, "_d_b")
+    assert "neighbour" in pieces[0][3] and pieces[1][3]  # rank 0 mapped fine but follows rank 1
+
+
 def _nccl_worker(port, n, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
