@@ -119,10 +119,32 @@ __device__ __forceinline__ void digit_scan(const u32 *tot, u32 *out, int radix, 
 // table[digit * tiles + tile]: scanned in this order it yields, for every (digit, tile), the
 // number of records with a smaller digit anywhere plus those with the same digit in earlier
 // tiles - the stable destination of the tile's first record with that digit.
+// The first pass also finds out whether the queue is ALREADY in bucket order (bucket id = (key >> lb) &
+// hmask never decreases from one record to the next): affine non-injective maps (restriction stencils),
+// sorted or block-clustered index maps.  Then no record has to move: *in_order stays kNone, every later
+// kernel of the partition returns at once, and boundaries + fold read the queue where it is.
+// (record p - 1 is the neighbouring lane's record of the same round: only lane 0 has to load it; the all-ones
+// mark of a site that did not execute is the largest bucket id with or without hmask)
+__device__ __forceinline__ bool out_of_order(const u32 *__restrict__ keys, size_t p, size_t m, u32 key, int lb)
+{
+    const u32 bucket = key >> lb;
+    u32 before = __shfl_up_sync(KRN_FULL_MASK, bucket, 1);
+    if ((threadIdx.x & 31) == 0) before = (p > 0 && p < m) ? keys[p - 1] >> lb : 0u;
+    return p < m && before > bucket;
+}
+// one store per BLOCK at most (a random queue has a violation at every other record: per-thread stores to
+// the one word were measured at +0.25 ms per 16.7 M records)
+__device__ __forceinline__ void publish_order(bool bad, u32 *in_order)
+{
+    if (__syncthreads_or(bad) && threadIdx.x == 0 && *in_order != 0u) *in_order = 0u;
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(kThreads)
-ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__restrict__ table)
+ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__restrict__ table, int lb, u32 hmask,
+         u32 *in_order, int check)
 {
+    if (!check && *in_order == kNone) return;
     // digits of 9 and 10 bits: per-warp counters, bumped by the lowest lane of every group of equal
     // digits (ballots) with a plain read-modify-write
     constexpr u32 mask = (1u << BITS) - 1u;
@@ -133,10 +155,16 @@ ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__re
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = size_t(blockIdx.x) * kTile + size_t(warp) * kWarpSpan;
     u32 key[kItems];
+    bool bad = false;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const size_t p = base + size_t(r) * 32 + lane;
         key[r] = p < m ? keys[p] : 0u;
+    }
+    if (check) {  // (behind ALL the loads: a test right behind its load would wait for it before the next is issued)
+#pragma unroll
+        for (int r = 0; r < kItems; ++r) bad |= out_of_order(keys, base + size_t(r) * 32 + lane, m, key[r], lb);
+        publish_order(bad, in_order);
     }
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
@@ -163,8 +191,10 @@ ord_hist(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__re
 // one word (four counts) per dp4a.
 template <int BITS>
 __global__ void __launch_bounds__(kThreads)
-ord_hist_bytes(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__restrict__ table)
+ord_hist_bytes(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32 *__restrict__ table, int lb,
+               u32 hmask, u32 *in_order, int check)
 {
+    if (!check && *in_order == kNone) return;
     constexpr u32 mask = (1u << BITS) - 1u;
     constexpr int kRadix = 1 << BITS;
     extern __shared__ __align__(16) unsigned char ord_smem[];
@@ -173,15 +203,40 @@ ord_hist_bytes(const u32 *__restrict__ keys, size_t m, int shift, u32 tiles, u32
     __syncthreads();
     const size_t base = size_t(blockIdx.x) * kTile;
     unsigned char *mine = ord_smem + 4 * (threadIdx.x & 63) + (threadIdx.x >> 6);
+    // which records a thread counts is immaterial for a histogram: four CONSECUTIVE records per 128-bit load
+    // (the tile starts at a multiple of 4096 records; a caller's queue need not be 16-byte aligned), four
+    // loads per thread
+    const bool vec = (reinterpret_cast<size_t>(keys) & 15u) == 0;
     u32 key[kItems];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const size_t p = base + size_t(r) * kThreads + threadIdx.x;
-        key[r] = p < m ? keys[p] : 0u;
+    for (int g = 0; g < kItems / 4; ++g) {
+        const size_t p = base + (size_t(g) * kThreads + threadIdx.x) * 4;
+        if (vec && p + 4 <= m) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(keys + p);
+            key[4 * g] = q.x, key[4 * g + 1] = q.y, key[4 * g + 2] = q.z, key[4 * g + 3] = q.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) key[4 * g + u] = p + u < m ? keys[p + u] : 0u;
+        }
+    }
+    if (check) {
+        // in bucket order?  Three comparisons inside the thread's four records, one with the record before
+        // them: the neighbouring lane's last one (lane 0 loads it).  Behind ALL the loads: a test right behind
+        // its load would wait for it before the next load is issued.
+        bool bad = false;
+#pragma unroll
+        for (int g = 0; g < kItems / 4; ++g) {
+            const size_t p = base + (size_t(g) * kThreads + threadIdx.x) * 4;
+            const u32 b0 = key[4 * g] >> lb, b1 = key[4 * g + 1] >> lb, b2 = key[4 * g + 2] >> lb, b3 = key[4 * g + 3] >> lb;
+            u32 before = __shfl_up_sync(KRN_FULL_MASK, b3, 1);
+            if ((threadIdx.x & 31) == 0) before = (p > 0 && p < m) ? keys[p - 1] >> lb : 0u;
+            bad |= (p < m && before > b0) | (p + 1 < m && b0 > b1) | (p + 2 < m && b1 > b2) | (p + 3 < m && b2 > b3);
+        }
+        publish_order(bad, in_order);
     }
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
-        if (base + size_t(r) * kThreads + threadIdx.x < m) {
+        if (base + (size_t(r / 4) * kThreads + threadIdx.x) * 4 + (r & 3) < m) {
             unsigned char *c = mine + (((key[r] >> shift) & mask) << 8);
             *c = (unsigned char)(*c + 1);
         }
@@ -257,8 +312,9 @@ __device__ __forceinline__ void store8(u32 *data, size_t first, size_t count, co
 }
 
 // one block walks the whole array, chunk after chunk (small tables, and the block sums of big ones)
-__global__ void __launch_bounds__(kThreads) scan_single(u32 *data, size_t count)
+__global__ void __launch_bounds__(kThreads) scan_single(u32 *data, size_t count, const u32 *in_order)
 {
+    if (*in_order == kNone) return;
     u32 carry = 0;
     for (size_t base = 0; base < count; base += kScanChunk) {
         u32 x[8];
@@ -269,8 +325,10 @@ __global__ void __launch_bounds__(kThreads) scan_single(u32 *data, size_t count)
     }
 }
 
-__global__ void __launch_bounds__(kThreads) scan_sums(const u32 *__restrict__ data, size_t count, u32 *__restrict__ sums)
+__global__ void __launch_bounds__(kThreads) scan_sums(const u32 *__restrict__ data, size_t count, u32 *__restrict__ sums,
+                                                       const u32 *in_order)
 {
+    if (*in_order == kNone) return;
     __shared__ u32 s_w[kWarps];
     const size_t first = size_t(blockIdx.x) * kScanChunk + size_t(threadIdx.x) * 8;
     u32 x[8], sum = 0;
@@ -288,8 +346,10 @@ __global__ void __launch_bounds__(kThreads) scan_sums(const u32 *__restrict__ da
     }
 }
 
-__global__ void __launch_bounds__(kThreads) scan_apply(u32 *data, size_t count, const u32 *__restrict__ sums)
+__global__ void __launch_bounds__(kThreads) scan_apply(u32 *data, size_t count, const u32 *__restrict__ sums,
+                                                        const u32 *in_order)
 {
+    if (*in_order == kNone) return;
     const size_t first = size_t(blockIdx.x) * kScanChunk + size_t(threadIdx.x) * 8;
     u32 x[8];
     load8(data, first, count, x);
@@ -308,8 +368,10 @@ __global__ void __launch_bounds__(kThreads) scan_apply(u32 *data, size_t count, 
 template <int BITS>
 __global__ void __launch_bounds__(kThreads)
 ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in, u32 *__restrict__ keys_out,
-            double *__restrict__ vals_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles, int width)
+            double *__restrict__ vals_out, const u32 *__restrict__ table, size_t m, int shift, u32 tiles, int width,
+            const u32 *in_order)
 {
+    if (*in_order == kNone) return;
     constexpr u32 mask = (1u << BITS) - 1u;
     constexpr int kRadix = 1 << BITS;
     extern __shared__ __align__(16) unsigned char ord_smem[];
@@ -413,13 +475,16 @@ ord_scatter(const u32 *__restrict__ keys_in, const double *__restrict__ vals_in,
 // ---- bucket boundaries -----------------------------------------------------------------------
 // records are sorted by bucket id = (key >> lb) & hmask: first / one-past-last position per bucket
 __global__ void __launch_bounds__(kThreads)
-ord_mark(const u32 *__restrict__ keys, size_t m, int lb, u32 hmask, u32 *__restrict__ start, u32 *__restrict__ end)
+ord_mark(const u32 *__restrict__ keys_moved, const u32 *__restrict__ keys_queue, const u32 *in_order, size_t m, int lb,
+         u32 hmask, u32 *__restrict__ start, u32 *__restrict__ end)
 {
-    // 4 consecutive records per thread (one 128-bit load; the buffers are 256-byte aligned)
+    const u32 *__restrict__ keys = *in_order == kNone ? keys_queue : keys_moved;
+    // 4 consecutive records per thread (one 128-bit load when the buffer is 16-byte aligned: the moved
+    // queue always is, a caller's queue need not be)
     const size_t p = (size_t(blockIdx.x) * kThreads + threadIdx.x) * 4;
     if (p >= m) return;
     u32 k[6];  // k[0] = predecessor of record p, k[5] = successor of record p + 3
-    if (p + 4 <= m) {
+    if ((reinterpret_cast<size_t>(keys) & 15u) == 0 && p + 4 <= m) {
         const uint4 q = *reinterpret_cast<const uint4 *>(keys + p);
         k[1] = q.x, k[2] = q.y, k[3] = q.z, k[4] = q.w;
     } else {
@@ -535,10 +600,14 @@ struct Cols {
 // receives its records in queue order.  target_size = number of keys (elements / rows).
 template <int WIDTH, bool LANES, int PER>
 __global__ void __launch_bounds__(kThreads)
-ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, size_t m,
+ord_bucket_fold(const u32 *__restrict__ keys_moved, const double *__restrict__ vals_moved,
+                const u32 *__restrict__ keys_queue, const double *__restrict__ vals_queue, const u32 *in_order, size_t m,
                 double *__restrict__ target, size_t target_size, int ncols, Cols cols, int lb,
                 const u32 *__restrict__ start, const u32 *__restrict__ end)
 {
+    const bool queue = *in_order == kNone;
+    const u32 *__restrict__ keys = queue ? keys_queue : keys_moved;
+    const double *__restrict__ vals = queue ? vals_queue : vals_moved;
     constexpr int width = WIDTH;
     constexpr int kChunk = kThreads * PER;
     constexpr int kSlotBits = PER == 8 ? 11 : 10;
@@ -669,14 +738,16 @@ ord_bucket_fold(const u32 *__restrict__ keys, const double *__restrict__ vals, s
     }
 
 cudaError_t launch_hist(int bits, unsigned tiles, cudaStream_t st, const u32 *keys, size_t m, int shift, u32 ntiles,
-                        u32 *table)
+                        u32 *table, int lb, u32 hmask, u32 *in_order, int check)
 {
     cudaError_t e = cudaSuccess;
     const size_t smem = size_t(256) << bits;  // 2^bits rows of 256 byte counters
 #define KRN_BYTES(B)                                                                                             \
     do {                                                                                                         \
         e = cudaFuncSetAttribute(ord_hist_bytes<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));     \
-        if (e == cudaSuccess) ord_hist_bytes<B><<<tiles, kThreads, smem, st>>>(keys, m, shift, ntiles, table);   \
+        if (e == cudaSuccess)                                                                                    \
+            ord_hist_bytes<B><<<tiles, kThreads, smem, st>>>(keys, m, shift, ntiles, table, lb, hmask, in_order, \
+                                                             check);                                             \
     } while (0)
     switch (bits) {
     case 1: KRN_BYTES(1); break;
@@ -687,8 +758,8 @@ cudaError_t launch_hist(int bits, unsigned tiles, cudaStream_t st, const u32 *ke
     case 6: KRN_BYTES(6); break;
     case 7: KRN_BYTES(7); break;
     case 8: KRN_BYTES(8); break;
-    case 9: ord_hist<9><<<tiles, kThreads, 0, st>>>(keys, m, shift, ntiles, table); break;
-    default: ord_hist<10><<<tiles, kThreads, 0, st>>>(keys, m, shift, ntiles, table); break;
+    case 9: ord_hist<9><<<tiles, kThreads, 0, st>>>(keys, m, shift, ntiles, table, lb, hmask, in_order, check); break;
+    default: ord_hist<10><<<tiles, kThreads, 0, st>>>(keys, m, shift, ntiles, table, lb, hmask, in_order, check); break;
     }
 #undef KRN_BYTES
     return e;
@@ -700,7 +771,8 @@ size_t scatter_smem(int bits)
 }
 
 cudaError_t launch_scatter(int bits, unsigned tiles, cudaStream_t st, const u32 *keys_in, const double *vals_in,
-                           u32 *keys_out, double *vals_out, const u32 *table, size_t m, int shift, u32 ntiles, int width)
+                           u32 *keys_out, double *vals_out, const u32 *table, size_t m, int shift, u32 ntiles, int width,
+                           const u32 *in_order)
 {
     const size_t smem = scatter_smem(bits);
     cudaError_t e = cudaSuccess;
@@ -709,7 +781,7 @@ cudaError_t launch_scatter(int bits, unsigned tiles, cudaStream_t st, const u32 
         e = cudaFuncSetAttribute(ord_scatter<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
         if (e == cudaSuccess)                                                                                    \
             ord_scatter<B><<<tiles, kThreads, smem, st>>>(keys_in, vals_in, keys_out, vals_out, table, m, shift, \
-                                                          ntiles, width);                                        \
+                                                          ntiles, width, in_order);                              \
     } while (0)
     KRN_BITS_SWITCH(bits, KRN_CALL)
 #undef KRN_CALL
@@ -796,7 +868,7 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
     const size_t val_bytes = round256(records * size_t(width) * sizeof(double));
     const int nbuf = passes > 1 ? 2 : 1;
     const size_t total = nbuf * (key_bytes + val_bytes) + round256(table_len * 4) + round256(sums_len * 4) +
-                         2 * round256(buckets * 4);
+                         2 * round256(buckets * 4) + 256;
     char *ws = nullptr;
     KRN_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&ws), total, ctx->stream));
     char *cursor = ws;
@@ -812,7 +884,9 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
     cursor += round256(table_len * 4);
     u32 *sums = reinterpret_cast<u32 *>(cursor);
     cursor += round256(sums_len * 4);
-    u32 *start = reinterpret_cast<u32 *>(cursor);
+    u32 *in_order = reinterpret_cast<u32 *>(cursor);  // kNone while no record has been seen out of bucket order
+    cursor += 256;
+    u32 *start = reinterpret_cast<u32 *>(cursor);  // (directly behind in_order: one memset sets both)
     cursor += round256(buckets * 4);
     u32 *end = reinterpret_cast<u32 *>(cursor);
 
@@ -821,28 +895,29 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
         krn_set_error("%s failed: %s", what, cudaGetErrorString(e));
         rc = KRN_E_CUDA;
     };
-    cudaError_t e = cudaMemsetAsync(start, 0xFF, buckets * 4, ctx->stream);
+    cudaError_t e = cudaMemsetAsync(in_order, 0xFF, 256 + buckets * 4, ctx->stream);
     if (e != cudaSuccess) fail(e, "cudaMemsetAsync");
     const u32 *src_keys = d_keys;
     const double *src_vals = d_vals;
     for (int pass = 0; pass < passes && rc == KRN_OK; ++pass) {
         const int shift = lb + pass * bits;
-        e = launch_hist(bits, unsigned(tiles), ctx->stream, src_keys, records, shift, u32(tiles), table);
+        e = launch_hist(bits, unsigned(tiles), ctx->stream, src_keys, records, shift, u32(tiles), table, lb, hmask,
+                        in_order, pass == 0);
         if (e != cudaSuccess) fail(e, "histogram launch");
         ctx->launches++;
         if (table_len <= size_t(kScanChunk) * 32) {
-            scan_single<<<1, kThreads, 0, ctx->stream>>>(table, table_len);
+            scan_single<<<1, kThreads, 0, ctx->stream>>>(table, table_len, in_order);
             ctx->launches++;
         } else {
-            scan_sums<<<unsigned(sums_len), kThreads, 0, ctx->stream>>>(table, table_len, sums);
-            scan_single<<<1, kThreads, 0, ctx->stream>>>(sums, sums_len);
-            scan_apply<<<unsigned(sums_len), kThreads, 0, ctx->stream>>>(table, table_len, sums);
+            scan_sums<<<unsigned(sums_len), kThreads, 0, ctx->stream>>>(table, table_len, sums, in_order);
+            scan_single<<<1, kThreads, 0, ctx->stream>>>(sums, sums_len, in_order);
+            scan_apply<<<unsigned(sums_len), kThreads, 0, ctx->stream>>>(table, table_len, sums, in_order);
             ctx->launches += 3;
         }
         u32 *dst_keys = key_buf[pass & 1];
         double *dst_vals = val_buf[pass & 1];
         e = launch_scatter(bits, unsigned(tiles), ctx->stream, src_keys, src_vals, dst_keys, dst_vals, table, records,
-                           shift, u32(tiles), width);
+                           shift, u32(tiles), width, in_order);
         ctx->launches++;
         src_keys = dst_keys;
         src_vals = dst_vals;
@@ -850,7 +925,7 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
     }
     if (rc == KRN_OK) {
         const size_t blocks = (records + 4 * kThreads - 1) / (4 * kThreads);
-        ord_mark<<<unsigned(blocks), kThreads, 0, ctx->stream>>>(src_keys, records, lb, hmask, start, end);
+        ord_mark<<<unsigned(blocks), kThreads, 0, ctx->stream>>>(src_keys, d_keys, in_order, records, lb, hmask, start, end);
         const size_t tile_elems = ((size_t(lanes ? ncols : 1) << lb) + 1) & ~size_t(1);
         const size_t chunk = size_t(kThreads) * (width == 1 ? 8 : 4);
         const size_t smem = tile_elems * 8 + size_t(width) * chunk * 8 + 2 * chunk * 4 + size_t(16) * kThreads * 2;
@@ -864,7 +939,8 @@ int ordered_impl(krn_ctx *ctx, double *d_target, size_t target_size, int ncols, 
         e = cudaFuncSetAttribute(ord_bucket_fold<W, L, per>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         if (e == cudaSuccess)                                                                                     \
             ord_bucket_fold<W, L, per><<<unsigned(real), kThreads, smem, ctx->stream>>>(                          \
-                src_keys, src_vals, records, d_target, target_size, ncols, cc, lb, start, end);                   \
+                src_keys, src_vals, d_keys, d_vals, in_order, records, d_target, target_size, ncols, cc, lb,      \
+                start, end);                                                                                      \
     } while (0)
         switch (width * 2 + (lanes ? 1 : 0)) {
         case 2: KRN_FOLD(1, false); break;

@@ -54,6 +54,23 @@ def _key_maps(records, size, rng):
     holes = rng.integers(0, size, size=records).astype(np.uint32)
     holes[rng.random(records) < 0.3] = 0xFFFFFFFF
     maps["with_holes"] = holes
+    # queues that are already in bucket order take the path on which no record moves (the in_order word of
+    # csrc/krn_ordered.cu): sorted maps, affine maps with collisions, sorted with unexecuted sites at the end;
+    # one unexecuted site or one early record in the middle puts the queue back on the partition path
+    srt = np.sort(rng.integers(0, size, size=records)).astype(np.uint32)
+    maps["sorted"] = srt
+    maps["affine_collisions"] = np.minimum((np.arange(records) // 3) * 2 + (np.arange(records) % 3), size - 1)
+    tail = srt.copy()
+    tail[records - records // 4:] = 0xFFFFFFFF
+    maps["sorted_holes_at_the_end"] = tail
+    mid = srt.copy()
+    if records > 2:
+        mid[records // 2] = 0xFFFFFFFF
+    maps["sorted_but_one_hole"] = mid
+    late = srt.copy()
+    if records > 2:
+        late[records - 1] = srt[0]
+    maps["sorted_but_the_last"] = late
     return maps
 
 
@@ -73,6 +90,34 @@ def test_queue_applied_like_the_reference(size, records):
             cport.apply_queue(want, keys, vals, width)
             got = _accumulate(target, keys, vals, width)
             assert_bits(got, want, f"size={size} records={records} width={width} {label}")
+
+
+def test_queues_that_are_not_16_byte_aligned():
+    """the second target of a launch starts wherever the first one's records end (key_off * n): the
+    kernels' 128-bit key loads must not assume more than the element's own alignment"""
+    from oracle import cport
+
+    dev = Device.get()
+    rng = np.random.default_rng(11)
+    records, size = 70_001, 5000
+    for label, keys in (("uniform", rng.integers(0, size, size=records)), ("sorted", np.sort(rng.integers(0, size, size=records)))):
+        keys = keys.astype(np.uint32)
+        vals = rng.normal(size=records)
+        target = rng.normal(size=size)
+        want = target.copy()
+        cport.apply_queue(want, keys, vals, 1)
+        for shift in (1, 2, 3):
+            d_t, d_k, d_v = dev.alloc(8 * size), dev.alloc(4 * (records + 4)), dev.alloc(8 * (records + 4))
+            dev.upload(d_t, target)
+            dev.upload(d_k + 4 * shift, keys)
+            dev.upload(d_v + 8 * shift, vals)
+            _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, C.c_void_p(d_t), size, C.c_void_p(d_k + 4 * shift),
+                                                       C.c_void_p(d_v + 8 * shift), records, 1))
+            got = np.empty(size)
+            dev.download(got, d_t)
+            for ptr in (d_t, d_k, d_v):
+                dev.free(ptr)
+            assert_bits(got, want, f"{label}, queue shifted by {shift} elements")
 
 
 def test_long_runs_and_signed_zeros():

@@ -41,6 +41,7 @@ def main():
             "uniform": rng.integers(0, rows, size=m),
             "clustered8": (np.arange(m) // 8) % rows,
             "hot90": np.where(rng.random(m) < 0.9, 3 % rows, rng.integers(0, rows, size=m)),
+            "sorted": np.sort(rng.integers(0, rows, size=m)),  # already in bucket order: no record moves
         }
         d_t = dev.alloc(8 * rows)
         for label, keys in maps.items():
