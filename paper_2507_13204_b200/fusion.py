@@ -841,6 +841,10 @@ def form_groups(ops: list, an: Analysis, windows: bool = True, side_gathers: boo
             classic = ok and not g.windowed
             if (producer and (has_producer or has_apply)) or (loop.what == "apply" and (has_producer or has_apply)):
                 classic = False
+            if classic and any(not acc.get(sstmt.src, (True,))[0] for sstmt, _, _ in g.sides):
+                # a side reduction (check_finite plans) reads its source from the registers of a pointwise
+                # View; this loop reads that View at i + c: no tile kernel (a window kernel may still do)
+                classic = False
             if classic:
                 for v, (pw, wr, at) in acc.items():
                     if v in gacc:

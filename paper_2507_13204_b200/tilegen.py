@@ -854,7 +854,14 @@ def window_kernel(builder, group, name: str, plan: dict, an) -> dict:
         """side reductions that sit before op `position`: copy the source's current value (own slots)"""
         for j, (sstmt, _, pos) in enumerate(sides):
             if pos == position:
-                val = f"{regs[sstmt.src]}[e]" if sstmt.src in regs else f"{wins[sstmt.src]}[wq]"
+                if sstmt.src in regs:
+                    val = f"{regs[sstmt.src]}[e]"
+                elif sstmt.src in wins:
+                    val = f"{wins[sstmt.src]}[wq]"
+                else:
+                    # a View the group only reads, at i + c somewhere (global loads): its own row, in range
+                    # because the reduction's extent IS the group's trip count
+                    val = f"E.v[{b.vid(sstmt.src)}][i]"
                 w(f"        if (e < 4) SG{j}[e] = {val};")
 
     def emit_tests(loop):

@@ -245,3 +245,20 @@ def test_read_only_stencil_neighbours_become_registers():
         return s; }""")
     plan = compiled.plan_for(p.functions[0], False)
     assert "= KRN_NBR(" not in plan.source and "* KRN_NBR(" not in plan.source and "KRN_NBR(P0" not in plan.source
+
+
+def test_side_reduction_whose_source_a_later_loop_reads_at_neighbours():
+    """tracked plans: the dead sum's source is untouched when the reduction joins the group, then a later
+    loop reads it at i - 1 / i + 1 (found by the random-program test): no tile kernel with the source
+    outside its registers; the window kernel captures the value from global memory"""
+    p = krn.parse("""fn f(a: view<f64,1>, b: view<f64,1>) -> f64 {
+        let t0: view<f64,1> = view("t0", extent(a, 0));
+        let t1: view<f64,1> = view("t1", extent(a, 0));
+        parallel_for i in 0..extent(a, 0) { t1(i) = t0(i); if (i != 0) { t1(i) += 1.5 * t0(i - 1); } }
+        s0 = parallel_sum(a);
+        parallel_for i in 0..extent(a, 0) { t1(i) = a(i); if (i != 0) { t1(i) += 0.125 * a(i - 1); } }
+        r = parallel_sum(t0);
+        return r; }""")
+    for windows in (True, False):
+        plan = compiled.plan_for(p.functions[0], windows, True)
+        assert plan is not None and plan.launch_count <= 2

@@ -168,6 +168,21 @@ def _checked(program, fn_name, inputs, extra):
 @settings(max_examples=int(__import__("os").environ.get("KRN_FUZZ", "60")), deadline=None, suppress_health_check=list(HealthCheck))
 @given(programs(), st.sampled_from([1, 2, 5, 33, 130, 1030]), st.integers(0, 10**6))
 def test_random_programs_match_the_oracle(prog, n, seed):
+    """(KRN_FUZZ_LOG=<file>: the FIRST failing example is written there as it fails - after a device fault
+    the context is dead, every later example fails too, and what hypothesis then shrinks to says nothing)"""
+    log = __import__("os").environ.get("KRN_FUZZ_LOG")
+    try:
+        _one_program(prog, n, seed)
+    except BaseException as exc:  # noqa: BLE001 - recorded and re-raised
+        if log and type(exc).__name__ not in ("UnsatisfiedAssumption", "Skipped") and not __import__("os").path.exists(log):
+            import traceback
+
+            with open(log, "w") as f:
+                f.write(f"n={n} seed={seed} flags={prog[1:]}\n{prog[0]}\n{traceback.format_exc()}")
+        raise
+
+
+def _one_program(prog, n, seed):
     from oracle import interp
 
     text, use_idx, use_c, use_m = prog
