@@ -568,9 +568,11 @@ class _CompiledRun:
                 # really hold their zeros (the kernel still skips the loads)
                 partial = "cols" in p and {c for c in p["cols"] if p["col_store"][c]} != set(range(v.extents[1]))
                 ptrs[p["view"]] = v.device_ptr(dev, discard=zero and not partial)
-            elif zero:
+            elif zero and not p.get("nbr"):
                 ptrs[p["view"]] = 0
             else:
+                # (neighbour registers: the first and last steps of the range read the View through
+                # bounds-checked loads, so a lazily zero one needs its buffer all the same)
                 ptrs[p["view"]] = v.device_ptr(dev, write=False)
         ld = ((n_launch + 3) // 4) * 4 + tilegen.STRIDE_PAD
         stage_ptr = 0

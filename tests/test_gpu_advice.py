@@ -107,3 +107,30 @@ def test_headline_gradient_with_shadows_longer_than_x():
             krn.execute(gp, "normRes1DLaplacianSQ_grad", got)
             for k in want:
                 assert_bits(got[k].buffer, want[k], f"n={n} lazy={lazy} {k}")
+
+
+@pytest.mark.parametrize("fuse_neighbours", [True, False])
+@pytest.mark.parametrize("n", [1, 5, 130, 1030, 70_001])
+def test_neighbour_registers_of_a_view_that_is_still_lazily_zero(n, fuse_neighbours):
+    """a local nobody has written is not allocated; a tile kernel that holds its stencil neighbours in
+    registers still reads it through bounds-checked loads on the first and last steps of the range
+    (found by the random-program test: the pointer must not be null)"""
+    from oracle import interp
+
+    src = """fn f(a: view<f64,1>) -> f64 {
+        let t1: view<f64,1> = view("t1", extent(a, 0));
+        let t2: view<f64,1> = view("t2", extent(a, 0));
+        parallel_for i in 0..extent(a, 0) {
+            t2(i) = t1(i) + a(i);
+            if (i != 0) { t2(i) += 2.0 * t1(i - 1) + a(i - 1); }
+            if (i != extent(a, 0) - 1) { t2(i) -= 0.125 * t1(i + 1); }
+        }
+        r = parallel_sum(t2);
+        return r; }"""
+    p = parse(src)
+    a = np.random.default_rng(n).normal(size=n)
+    want = {"a": a.copy()}
+    wv = interp.run(p, "f", want)
+    got = {"a": ViewStorage.from_values("a", a)}
+    gv = krn.execute(p, "f", got, ExecutionConfig(policy="compiled", fuse_neighbours=fuse_neighbours)).value
+    assert_bits(gv, wv, "value")
