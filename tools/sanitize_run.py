@@ -55,6 +55,23 @@ for stem in ("laplacian", "stencil_smooth", "rowscale_rank2", "gather_indirect",
                     for sp, w in zip(gfn.params[len(fn.params):], wrt):
                         call[sp.name] = ViewStorage.zeros(sp.name, np.shape(data[w]))
                     krn.execute(gp, gfn.name, call, extra)
+# neighbour registers over a local that is still lazily zero, and over a parameter (tile kernels, both layouts)
+zero_local = krn.parse("""fn f(a: view<f64,1>) -> f64 {
+    let t1: view<f64,1> = view("t1", extent(a, 0));
+    let t2: view<f64,1> = view("t2", extent(a, 0));
+    parallel_for i in 0..extent(a, 0) {
+        t2(i) = t1(i) + a(i);
+        if (i != 0) { t2(i) += 2.0 * t1(i - 1) + a(i - 1); }
+        if (i != extent(a, 0) - 1) { t2(i) -= 0.125 * t1(i + 1); }
+    }
+    r = parallel_sum(t2);
+    return r; }""")
+for n in (1, 5, 130, 1030, 9000):
+    for fuse in (True, False):
+        for check in (False, True):
+            krn.execute(zero_local, "f", {"a": ViewStorage.from_values("a", rng.normal(size=n))},
+                        ExecutionConfig(policy="compiled", fuse_neighbours=fuse, check_finite=check))
+            ran += 1
 # the ordered queue through the raw ABI: holes, hot keys, widths, row records
 import ctypes as C  # noqa: E402
 
@@ -80,6 +97,22 @@ for records, size in ((1, 1), (4097, 300), (70_001, 5000), (70_001, 1 << 20)):
             if width * records >= 3 * records:
                 _cabi.check(dev.lib.krn_ordered_accumulate_rows(dev.h, C.c_void_p(bufs[0]), size // 3, 3, cols, 3,
                                                                 C.c_void_p(bufs[1]), C.c_void_p(bufs[2]), records))
+        dev.sync()
+        for b in bufs:
+            dev.free(b)
+# queues that are already in bucket order (no record moves) and queues that are not 16-byte aligned
+for records, size in ((4097, 300), (70_001, 1 << 20)):
+    srt = np.sort(rng.integers(0, size, size=records)).astype(np.uint32)
+    srt[records - records // 5:] = 0xFFFFFFFF
+    vals = rng.normal(size=records)
+    for shift in (0, 1, 3):
+        bufs = [dev.alloc(8 * size), dev.alloc(4 * (records + 4)), dev.alloc(8 * (records + 4))]
+        dev.fill(bufs[0], size, 0.0)
+        for keys in (srt, rng.integers(0, size, size=records).astype(np.uint32)):
+            dev.upload(bufs[1] + 4 * shift, keys)
+            dev.upload(bufs[2] + 8 * shift, vals)
+            _cabi.check(dev.lib.krn_ordered_accumulate(dev.h, C.c_void_p(bufs[0]), size, C.c_void_p(bufs[1] + 4 * shift),
+                                                       C.c_void_p(bufs[2] + 8 * shift), records, 1))
         dev.sync()
         for b in bufs:
             dev.free(b)
