@@ -253,6 +253,8 @@ def localize(stmt, lo: int, n_global: int, replicated=frozenset()):
             return _dc.replace(s, rhs=in_value(s.rhs))
         if k == "AssignScalar":
             return _dc.replace(s, rhs=in_value(s.rhs))
+        if k == "AtomicAdd":
+            return _dc.replace(s, value=in_value(s.value))
         if k == "DeclScalar":
             return _dc.replace(s, init=in_value(s.init))
         if k == "ParallelFor":

@@ -190,6 +190,26 @@ def test_guards_float_i_and_extents_are_localised(world):
     assert_bits(whole["a"], want["a"], "a")
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_number_in_an_atomic_contribution_is_localised(world):
+    """float(i) inside the VALUE of an atomic_add (the generated adjoint of `t(i) = i * m(i, c)`): found
+    by the random-program test below - the contribution was computed with the rank-local row"""
+    prog = krn.parse("""fn f(a: view<f64, 1>, m: view<f64, 2>) -> f64 {
+        let t0: view<f64, 1> = view("t0", extent(a, 0));
+        parallel_for i in 0..extent(a, 0) { t0(i) = (i * (m(i, 0) + m(i, 1))) + a(i); }
+        r = parallel_sum(t0);
+        return r;
+    }""")
+    rng = np.random.default_rng(7)
+    n = 37
+    gp = krn.differentiate(prog, "f", ("a", "m"))
+    gfn = gp.functions[-1]
+    assert any(type(s).__name__ == "AtomicAdd" for s in krn.lang.nodes.walk_statements(gfn.body))
+    data = {"a": rng.normal(size=n), "m": rng.normal(size=(n, 3)),
+            "_d_a": rng.normal(size=n), "_d_m": rng.normal(size=(n, 3))}
+    _check(gp, gfn.name, data, world, exact_views=True)
+
+
 def test_segments_are_plain_functions_of_the_language():
     prog = krn.load_program("mean_shift")
     sp = shard_program.ShardedProgram(prog, "shiftedEnergy", 100, 25, comm=ThreadComm(1).view(0))
@@ -297,7 +317,11 @@ def test_random_programs_sharded_against_the_whole_problem():
 
     ran = [0]
 
-    @settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck), database=None)
+    # the default run draws the same 150 programs every time; KRN_FUZZ=<n> explores n fresh ones
+    import os
+
+    @settings(max_examples=int(os.environ.get("KRN_FUZZ", "150")), deadline=None, suppress_health_check=list(HealthCheck),
+              derandomize="KRN_FUZZ" not in os.environ, database=None)
     @given(programs(), st.sampled_from([2, 3]), st.integers(0, 10**6))
     def run(prog, world, seed):
         text, use_idx, use_c, use_m = prog
