@@ -118,7 +118,11 @@ def test_random_programs_taped_gradient_against_finite_differences():
 
     checked = [0]
 
-    @settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck), database=None)
+    import os
+
+    # the default run draws the same 120 programs every time; KRN_FUZZ=<n> explores n fresh ones
+    @settings(max_examples=int(os.environ.get("KRN_FUZZ", "120")), deadline=None, suppress_health_check=list(HealthCheck),
+              derandomize="KRN_FUZZ" not in os.environ, database=None)
     @given(programs(), st.integers(0, 10**6))
     def run(prog, seed):
         text, use_idx, use_c, use_m = prog
