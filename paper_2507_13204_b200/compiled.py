@@ -300,7 +300,6 @@ class _Borrowed:
 class _CompiledRun:
     def __init__(self, dev, plan: CompiledPlan, views, scalars, cfg):
         self.dev, self.plan, self.views, self.cfg = dev, plan, views, cfg
-        self.scalars = scalars
         self.b = plan.builder
         self.H = {k: np.float64(v) for k, v in scalars.items()}
         self.stage: dict = {}
@@ -749,16 +748,7 @@ class _CompiledRun:
         if st[0] != 0:
             helper = _Run.__new__(_Run)
             helper.b, helper.views = self.b, self.views
-            first = helper.error_from(st.copy())
-            if self.plan.an.speculative:
-                # a dead statement that would have raised EARLIER than the one that did was dropped
-                # (fusion._raises_only_with): the statement path names the reference's error - every
-                # error condition of such a function depends on extents and unwritten index data only,
-                # so the second execution meets the same ones
-                from .runtime import _plan_for
-
-                _Run(dev, _plan_for(self.plan.fn), self.views, self.scalars, self.cfg).go()
-            raise first
+            raise helper.error_from(st.copy())
         value = float(out[0]) if self.ret_slot is not None else self.host_value
         if self.plan.track:
             from .runtime import NonFiniteDetected

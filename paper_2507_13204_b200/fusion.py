@@ -43,7 +43,6 @@ ranges) simply stays an unfused statement and runs through the statement path.
 from __future__ import annotations
 
 import dataclasses as _dc
-import os
 
 from . import codegen
 from .lang import nodes as N
@@ -390,7 +389,6 @@ class Analysis:
                         pass
         self.host_scalars = self._host_scalars()
         self.live_scalars = self._live_scalars()
-        self.speculative = False  # set by _drop_dead_fills: a dead statement that may raise was dropped
         # literal columns with which each rank-2 View is accessed anywhere in the function
         self.columns: dict = {}
         for s in walk_statements(fn.body):
@@ -649,85 +647,6 @@ def _cannot_raise(loop: "LoopOp", an) -> bool:
     return True
 
 
-def _index_key(e, counter: str):
-    """Structural key of an index expression with the loop counter made anonymous; None when it
-    reads anything but the counter, literals and Views (a scalar's value may differ between loops)."""
-    k = kind(e)
-    if k == "Counter":
-        return ("i",) if e.name == counter else None
-    if k == "IntLiteral":
-        return ("n", e.value)
-    if k == "IdxBinary":
-        a, b = _index_key(e.lhs, counter), _index_key(e.rhs, counter)
-        return None if a is None or b is None else ("b", e.op, a, b)
-    if k == "ViewAccess":
-        sub = tuple(_index_key(i, counter) for i in e.indices)
-        return None if any(x is None for x in sub) else ("v", e.view, sub)
-    return None
-
-
-def _stable_indexing(fn) -> bool:
-    """No View that appears in an index position is written anywhere in the function: every
-    OutOfBounds / bad-index condition of the call is then a function of the extents and of data no
-    statement changes - executing the function a second time reports the same first error."""
-    index_views: set = set()
-    written: set = set()
-    for s in walk_statements(fn.body):
-        k = kind(s)
-        if k in ("AssignView", "AtomicAdd"):
-            written.add(s.target.view)
-        elif k in ("DeepCopy", "ParallelSumInto"):
-            written.add(s.dst)
-        for e in N.statement_exprs(s):
-            for n in walk_expr(e):
-                if kind(n) == "ViewAccess":
-                    for i in n.indices:
-                        index_views |= {m.view for m in walk_expr(i) if kind(m) == "ViewAccess"}
-    return not (index_views & written)
-
-
-def _raises_only_with(loop: "LoopOp", later: list, an) -> bool:
-    """True when every access of `loop` that may leave its View is repeated, unguarded and with the
-    same index expression over the same range, by a kept loop further down (`later`): whenever the
-    loop would raise, a kept statement raises as well.  WHICH error the reference reports is then
-    settled by executing the call again statement by statement (compiled._CompiledRun.finish); that
-    needs `_stable_indexing`."""
-    if loop.what != "kernel" or loop.sites:
-        return False
-    if any(kind(s) == "If" for s in walk_statements(loop.body)):
-        return False
-    try:
-        trip = an.trip(loop.upper)
-    except (TypeError, ValueError):
-        return False
-    cover: set = set()
-    for other in later:
-        if other.what != "kernel":
-            continue
-        try:
-            if an.trip(other.upper) != trip:
-                continue
-        except (TypeError, ValueError):
-            continue
-        for acc, guards in guarded_accesses(other):
-            if not guards:
-                cover.add((acc.view, tuple(_index_key(i, other.counter) for i in acc.indices)))
-    for acc in loop.accesses():
-        in_range = False
-        if an.rank.get(acc.view, 1) == 1 and len(acc.indices) == 1 and kind(acc.indices[0]) == "Counter" \
-                and acc.indices[0].name == loop.counter:
-            try:
-                in_range = an.trip(N.Extent(acc.view, 0)) == trip
-            except (TypeError, ValueError):
-                in_range = False
-        if in_range:
-            continue
-        key = tuple(_index_key(i, loop.counter) for i in acc.indices)
-        if any(x is None for x in key) or (acc.view, key) not in cover:
-            return False
-    return True
-
-
 def _drop_dead_fills(ops: list, fn, an=None) -> list:
     """Dead statements: a statement all of whose results nothing reads afterwards, and whose
     execution cannot raise, is unobservable - locals die at the return (runtime.py: DeclView
@@ -741,8 +660,6 @@ def _drop_dead_fills(ops: list, fn, an=None) -> list:
     needed: set = set()
     needed_scalars: set = set()
     kept: list = []
-    # (KRN_NO_SPECULATIVE_DROP=1: measurement switch, tools/corpus_bench.py)
-    stable = an is not None and not os.environ.get("KRN_NO_SPECULATIVE_DROP") and _stable_indexing(fn)
 
     def scalar_reads(op) -> set:
         out: set = set()
@@ -782,14 +699,8 @@ def _drop_dead_fills(ops: list, fn, an=None) -> list:
             continue
         if op[0] == "loop" and an is not None and op[1].what in ("kernel", "suminto", "deepcopy"):
             written = {a.view for a in op[1].accesses() if a.write}
-            if written and written <= local and not (written & needed):
-                if _cannot_raise(op[1], an):
-                    continue  # writes only locals nothing reads afterwards
-                if stable and _raises_only_with(op[1], [o[1] for o in kept if o[0] == "loop"], an):
-                    # e.g. the verbatim forward sweep of a gradient whose indirect reads the reverse sweep
-                    # repeats: dropped, and an error status makes the run replay the statements
-                    an.speculative = True
-                    continue
+            if written and written <= local and not (written & needed) and _cannot_raise(op[1], an):
+                continue  # writes only locals nothing reads afterwards
         needed_scalars |= scalar_reads(op)
         if op[0] == "gather" and not op[2]:
             needed_scalars.discard(op[1].dst)  # assigned here (not accumulated): earlier values are dead

@@ -337,50 +337,21 @@ def test_lane_groups_mixed_with_other_sites_fall_back_to_element_records(policy)
         assert_bits(got["m"].buffer, want["m"], f"{policy} n={n}")
 
 
-# ---- dead forward sweeps that may raise (fusion._raises_only_with) -------------------------------
+# ---- errors of a gradient with indirect reads ---------------------------------------------------
 
 def _gather_rows_case(n, rows, rng):
     return {"q": rng.normal(size=(rows, 3)), "idx": rng.integers(0, rows, size=n).astype(np.float64),
             "w": rng.normal(size=n), "_d_q": rng.normal(size=(rows, 3)), "_d_w": rng.normal(size=n)}
 
 
-def test_dead_forward_sweep_with_indirect_reads_is_dropped():
-    """rowGather_grad: the verbatim forward sweep only feeds the dead forward sum, and every indirect
-    read of it is repeated by the reverse sweep - it is not executed (one generated kernel instead of
-    two), results stay bit-identical"""
-    from oracle import interp
-    from paper_2507_13204_b200 import compiled, fusion
-
-    prog = krn.load_program("gather_rows_rank2")
-    gp = krn.differentiate(prog, prog.functions[0].name, ("q", "w"))
-    gfn = gp.functions[-1]
-    an = fusion.Analysis(gfn)
-    ops = fusion.build_ops(gfn, an)
-    assert an.speculative and sum(1 for o in ops if o[0] == "loop" and o[1].what == "kernel") == 1
-    rng = np.random.default_rng(11)
-    data = _gather_rows_case(5000, 700, rng)
-    want = {k: v.copy() for k, v in data.items()}
-    interp.run(gp, gfn.name, want)
-    dev = Device.get()
-    for det in (True, False):
-        got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
-        krn.execute(gp, gfn.name, got, ExecutionConfig(policy="compiled", deterministic_reduction=det))  # compile
-        got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
-        before = dev.launches()
-        krn.execute(gp, gfn.name, got, ExecutionConfig(policy="compiled", deterministic_reduction=det))
-        launches = dev.launches() - before
-        if det:
-            for k in ("_d_q", "_d_w"):
-                assert_bits(got[k].buffer, want[k], k)
-        else:
-            assert launches == 1
-            np.testing.assert_allclose(got["_d_q"].buffer, want["_d_q"], rtol=1e-12, atol=0)
-
-
 @pytest.mark.parametrize("fault", ["bad_row", "nan_row", "short_w", "short_w_and_shadow", "bad_row_and_short_shadow"])
-def test_errors_of_a_dropped_sweep_are_the_references(fault):
-    """the statement the reference blames is the FORWARD sweep's (it runs first); the fused plan no
-    longer executes it, so an error status replays the call statement by statement"""
+def test_errors_of_a_gather_gradient_are_the_references(fault):
+    """rowGather_grad: the statement the reference blames is the verbatim FORWARD sweep's (it runs
+    first) even when the reverse sweep would fail as well; same exception class and message under the
+    fused plan (forward and reverse sweep are one kernel there) and the statement path.
+    (Measured and rejected in this round: NOT executing the dead forward sweep - every access of it is
+    repeated by the reverse sweep - and replaying the statements when a status comes back: no gain,
+    1.925 against 1.931 ms at 16.7 M rows; the sweep shares its loads with the reverse sweep.)"""
     from oracle import interp
 
     prog = krn.load_program("gather_rows_rank2")
@@ -401,8 +372,9 @@ def test_errors_of_a_dropped_sweep_are_the_references(fault):
         interp.run(gp, gfn.name, want)
     for policy in ("compiled", "statements"):
         got = {k: ViewStorage.from_values(k, v) for k, v in data.items()}
-        with pytest.raises(type(ref.value)) as mine:
+        with pytest.raises(Exception) as mine:
             krn.execute(gp, gfn.name, got, ExecutionConfig(policy=policy))
+        assert type(mine.value).__name__ == type(ref.value).__name__, (policy, mine.value, ref.value)
         assert str(mine.value) == str(ref.value), (policy, str(mine.value), str(ref.value))
     # the context is usable afterwards
     good = _gather_rows_case(300, 40, np.random.default_rng(6))
