@@ -241,3 +241,62 @@ def _one_program(prog, n, seed):
         _checked(gp, gfn.name, inputs, {s: ((n, 3) if s == "_d_m" else (n,)) for s in shadows})
     except AssertionError as e:
         raise AssertionError(f"check_finite grad n={n}\n{text}\n{krn.emit(gfn)}\n{e}") from None
+
+
+# the same generator with ONE poisoned entry in the index map: every policy must fail like the oracle
+# (same exception class, same message - the line of the first statement, in program order, that meets the
+# bad entry).  One bad entry = one failing iteration, so which failure is reported first is not a race.
+@settings(max_examples=int(__import__("os").environ.get("KRN_FUZZ", "40")), deadline=None, suppress_health_check=list(HealthCheck),
+          derandomize="KRN_FUZZ" not in __import__("os").environ, database=None)
+@given(programs(), st.sampled_from([2, 5, 33, 130, 1030]), st.integers(0, 10**6),
+       st.sampled_from(["high", "negative", "nan", "inf", "fraction"]))
+def test_random_programs_fail_like_the_oracle(prog, n, seed, poison):
+    from oracle import interp
+
+    text, use_idx, use_c, use_m = prog
+    assume(use_idx and "idx(i)" in text)
+    try:
+        program = krn.parse(text)
+    except (krn.ParseError, krn.ValidationError):
+        assume(False)
+    inputs = _inputs(n, use_idx, use_c, seed, use_m)
+    where = seed % n
+    inputs["idx"][where] = {"high": float(n), "negative": -1.0, "nan": np.nan, "inf": np.inf,
+                            "fraction": inputs["idx"][where] + 0.5}[poison]
+    cases = [(program, "f", inputs)]
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        try:
+            wrt = ("a", "b") + (("m",) if use_m else ())
+            gp = krn.differentiate(program, "f", wrt)
+            gfn = gp.functions[-1]
+            gdata = dict(inputs)
+            for s in [p.name for p in gfn.params[len(program.functions[0].params):]]:
+                gdata[s] = np.zeros((n, 3) if s == "_d_m" else n)
+            cases.append((gp, gfn.name, gdata))
+        except krn.NotFeasible:
+            pass
+
+    def outcome(run):
+        try:
+            return ("ok", run())
+        except Exception as e:  # noqa: BLE001 - the outcome IS the exception
+            return (type(e).__name__, str(e))
+
+    for pr, name, data in cases:
+        want = {k: np.array(v) if isinstance(v, np.ndarray) else v for k, v in data.items()}
+        with np.errstate(all="ignore"):
+            w = outcome(lambda: interp.run(pr, name, want))
+        for policy in ("compiled", "pointwise", "statements"):
+            got = {k: ViewStorage.from_values(k, v) if isinstance(v, np.ndarray) else v for k, v in data.items()}
+            g = outcome(lambda: krn.execute(pr, name, got, _cfg(policy)).value)
+            if w[0] == "ok":  # a fraction truncates to a valid row
+                assert g[0] == "ok", (policy, g, text)
+                assert_bits(g[1], w[1]) if w[1] is not None else None
+                for k, v in got.items():
+                    if isinstance(v, ViewStorage):
+                        assert_bits(v.buffer, want[k], f"{policy} {k}\n{text}")
+            else:
+                assert g == w, (policy, name, g, w, text)
