@@ -641,16 +641,29 @@ ord_bucket_fold(const u32 *__restrict__ keys_moved, const double *__restrict__ v
     for (u32 c = s0; c < e0; c += kChunk) {
         const int cnt = int(e0 - c < u32(kChunk) ? e0 - c : u32(kChunk));
         __syncthreads();  // the previous chunk's fold is done with wa/wb/cv (and the tile is loaded)
+        // A chunk whose keys never decrease (a hot location, a sorted or clustered index map, the
+        // restriction stencils) is in fold order as it stands: the local ranking passes are skipped.
+        // Every thread first tests ONE pair of neighbours (its first record against the one before it):
+        // a random chunk fails that test at once, at the price of one load per thread and no barrier of
+        // its own; only when all 256 sampled pairs rise are the remaining pairs compared.
+        bool rising = true;
         for (int q = threadIdx.x; q < cnt; q += kThreads) {
-            u32 kl = keys[c + q] - u32(t0);
+            const u32 key = keys[c + q];
+            if (q == int(threadIdx.x) && q > 0 && keys[c + q - 1] > key) rising = false;
+            u32 kl = key - u32(t0);
             if (kl >= u32(tn)) kl = u32(tn) - 1u;  // cannot happen for keys < target_size: never leave the tile
             wa[q] = (kl << kSlotBits) | u32(q);
 #pragma unroll
             for (int w = 0; w < width; ++w) cv[w * kChunk + q] = vals[size_t(w) * m + c + q];
         }
-        __syncthreads();
+        bool presorted = __syncthreads_and(rising) != 0;
+        if (presorted) {
+            for (int q = int(threadIdx.x) + kThreads; q < cnt; q += kThreads)
+                if ((wa[q - 1] >> kSlotBits) > (wa[q] >> kSlotBits)) rising = false;
+            presorted = __syncthreads_and(rising) != 0;
+        }
         u32 *fin = wa, *other = wb;
-        for (int pass = 0; pass < passes; ++pass) {
+        for (int pass = 0; pass < (presorted ? 0 : passes); ++pass) {
             local_pass4<PER>(fin, other, cnt, kSlotBits + kLocalBits * pass, c16, s_wsum);
             u32 *swap = fin;
             fin = other;
